@@ -1,0 +1,322 @@
+"""Pins for the CPU oracle (oracle/mnl_oracle.py) against what the paper and the
+mathematics fix -- never against the oracle itself.  `P:n` = PAPER.md line n."""
+import math
+
+import numpy as np
+import pytest
+from scipy.special import expit, log_expit
+
+import datagen
+import oracle as O
+
+
+def data_of(prob):
+    return O.Data(prob.X, prob.Y, prob.Z, prob.choice, prob.spec.K)
+
+
+def tiny(N=200, K=4, p=3, f=2, d=1, seed=1, coef_sd=0.5):
+    return datagen.custom(N, K, p, f, d, seed=seed, coef_sd=coef_sd)
+
+
+# --- parameter counting (Table 1) -------------------------------------
+
+def test_num_params_paper_counts():
+    # Fish: income + intercept (X, p=1), catch alt-specific (ABI Z, d=1), price generic (ABI Y, f=1): 11
+    assert O.num_params(K=4, p=1, f=1, d=1) == 11
+    # Table 1 problem X: 50 variables incl. intercept, K=100 -> 4950
+    assert O.num_params(K=100, p=49, f=0, d=0) == 4950
+    # BASELINE configs
+    assert [datagen.CONFIGS[c].n_params for c in ("c1", "c2", "c3", "c4", "c5")] == [18, 189, 969, 5049, 1779]
+
+
+# --- closed forms at theta = 0 ------------------------------------------------------------
+
+def test_loglik_at_zero_is_minus_N_log_K():
+    D = data_of(datagen.make("c1"))
+    assert O.loglik(D, np.zeros(D.n_p)) == pytest.approx(-1386.29436112, abs=1e-8)
+    # nnet's printed initial value for N=10^4, K=10: 23025.850930 = N ln K
+    pr = datagen.custom(10000, 10, 5, seed=3)
+    D2 = data_of(pr)
+    assert round(-O.loglik(D2, np.zeros(D2.n_p)), 6) == 23025.850930
+
+
+def test_probabilities_uniform_at_zero_and_rows_sum_to_one():
+    D = data_of(tiny())
+    P = O.probabilities(O.utilities(D, np.zeros(D.n_p)))
+    assert np.all(P == 0.25)
+    th = datagen.draw(D.n_p, 5, 99, datagen.NORMAL, 2.0)
+    P = O.probabilities(O.utilities(D, th))
+    assert np.max(np.abs(P.sum(axis=1) - 1.0)) < 1e-15 * 4
+
+
+def test_probabilities_overflow_safe():
+    V = np.array([[0.0, 1000.0, 0.0], [0.0, -1000.0, -999.0]])
+    P = O.probabilities(V)
+    assert np.all(np.isfinite(P))
+    assert P[0, 1] == 1.0 and P[0, 0] == 0.0
+    assert P[1, 0] == pytest.approx(1.0)
+    t = O.loglik_terms(V, np.array([1, 0]))
+    assert np.all(np.isfinite(t)) and t[0] == 0.0
+
+
+def test_gradient_at_zero_intercepts_is_count_minus_N_over_K():
+    pr = tiny(N=300, K=5, p=2, f=0, d=0, seed=4)
+    D = data_of(pr)
+    g = O.gradient(D, np.zeros(D.n_p))
+    q = D.p + 1
+    n = np.bincount(D.choice, minlength=D.K)
+    for k in range(1, D.K):
+        assert g[(k - 1) * q] == pytest.approx(n[k] - D.N / D.K, abs=1e-10)
+
+
+def test_intercept_only_hessian_closed_form():
+    # N=100, K=4, theta=0: diagonal -N(1/K)(1-1/K) = -18.75, off-diagonal N/K^2 = 6.25
+    pr = datagen.custom(100, 4, 0, seed=2)
+    D = data_of(pr)
+    H = O.hessian(D, np.zeros(D.n_p))
+    assert np.allclose(np.diag(H), -18.75, atol=1e-12, rtol=0)
+    off = H[~np.eye(3, dtype=bool)]
+    assert np.allclose(off, 6.25, atol=1e-12, rtol=0)
+    assert np.array_equal(O.hessian_entries(D, np.zeros(3), [0, 0], [0, 1]), np.array([-18.75, 6.25]))
+
+
+# --- K = 2 is binary logistic regression ------------------------------------------
+
+def test_K2_reduces_to_logistic_regression():
+    pr = datagen.custom(400, 2, 3, f=2, d=2, seed=7, coef_sd=0.7)
+    D = data_of(pr)
+    th = datagen.draw(D.n_p, 11, 1, datagen.NORMAL, 0.5)
+    # textbook design row in theta order: [1, x_i | -z_i0 | z_i1 | y_i1 - y_i0]
+    W = np.hstack([np.ones((D.N, 1)), D.X, -D.Z[:, 0, :], D.Z[:, 1, :], D.Y[:, 1, :] - D.Y[:, 0, :]])
+    eta = W @ th
+    y = (D.choice == 1).astype(float)
+    s = expit(eta)
+    l_ref = np.sum(y * log_expit(eta) + (1 - y) * log_expit(-eta))
+    g_ref = W.T @ (y - s)
+    H_ref = -(W.T * (s * (1 - s))) @ W
+    l, g, H = O.mnl_eval(D, th)
+    assert l == pytest.approx(l_ref, rel=1e-13)
+    assert np.max(np.abs(g - g_ref)) <= 1e-11 * np.max(np.abs(g_ref))
+    assert np.max(np.abs(H - H_ref)) <= 1e-12 * np.max(np.abs(H_ref))
+
+
+# --- finite differences -------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(150, 4, 3, 2, 1), (120, 3, 2, 0, 2), (100, 5, 2, 3, 0), (90, 4, 0, 2, 0)])
+def test_gradient_matches_central_fd(shape):
+    N, K, p, f, d = shape
+    D = data_of(tiny(N, K, p, f, d, seed=8))
+    th = datagen.draw(D.n_p, 12, 2, datagen.NORMAL, 0.4)
+    g = O.gradient(D, th)
+    fd = np.empty_like(g)
+    for r in range(D.n_p):
+        h = 1e-5 * max(1.0, abs(th[r]))
+        e = np.zeros(D.n_p); e[r] = h
+        fd[r] = (O.loglik(D, th + e) - O.loglik(D, th - e)) / (2 * h)
+    assert np.linalg.norm(fd - g) <= 1e-6 * np.linalg.norm(g)
+
+
+@pytest.mark.parametrize("shape", [(150, 4, 3, 2, 1), (120, 3, 2, 0, 2), (100, 5, 2, 3, 0)])
+def test_hessian_matches_central_fd_of_gradient(shape):
+    N, K, p, f, d = shape
+    D = data_of(tiny(N, K, p, f, d, seed=9))
+    th = datagen.draw(D.n_p, 13, 3, datagen.NORMAL, 0.4)
+    H = O.hessian(D, th)
+    fd = np.empty_like(H)
+    for r in range(D.n_p):
+        h = 1e-5 * max(1.0, abs(th[r]))
+        e = np.zeros(D.n_p); e[r] = h
+        fd[:, r] = (O.gradient(D, th + e) - O.gradient(D, th - e)) / (2 * h)
+    assert np.linalg.norm(fd - H) <= 1e-5 * np.linalg.norm(H)
+
+
+# --- the textbook dense form and the paper's block form ---
+
+def test_hessian_equals_textbook_dense_Xt_W_Xt_for_X_only():
+    pr = tiny(N=60, K=5, p=3, f=0, d=0, seed=10)
+    D = data_of(pr)
+    th = datagen.draw(D.n_p, 14, 4, datagen.NORMAL, 0.5)
+    P = O.probabilities(O.utilities(D, th))
+    N, K, q = D.N, D.K, D.p + 1
+    Xt1 = np.hstack([np.ones((N, 1)), D.X])
+    Xtil = np.kron(np.eye(K - 1), Xt1)                       # block-diagonal, (K-1)N x (K-1)q
+    Wtil = np.zeros(((K - 1) * N, (K - 1) * N))
+    for k in range(1, K):
+        for t in range(1, K):
+            w = P[:, k] * ((k == t) - P[:, t])               # diag(W_kt)_i = P_ik(delta_kt - P_it)
+            Wtil[(k - 1) * N:k * N, (t - 1) * N:t * N] = np.diag(w)
+    H_ref = -Xtil.T @ Wtil @ Xtil
+    yv = np.concatenate([(D.choice == k).astype(float) for k in range(1, K)])
+    Pv = np.concatenate([P[:, k] for k in range(1, K)])
+    g_ref = Xtil.T @ (yv - Pv)
+    l, g, H = O.mnl_eval(D, th)
+    assert np.max(np.abs(H - H_ref)) <= 1e-12 * np.max(np.abs(H_ref))
+    assert np.max(np.abs(g - g_ref)) <= 1e-12 * np.max(np.abs(g_ref))
+
+
+def block_form(D, th):
+    """Eq. "loglik gradient" and Eq. "hessian block", paper's chunks in
+    ABI letters: M = X~ for beta_k (k>=1), M = Z_k for alpha_k (k>=0), generic data Y~_k = Y_k - Y_0."""
+    P = O.probabilities(O.utilities(D, th))
+    N, K, p, f, d = D.N, D.K, D.p, D.f, D.d
+    Xt1 = np.hstack([np.ones((N, 1)), D.X])
+    chunks = [(k, Xt1) for k in range(1, K)] + [(k, D.Z[:, k, :]) for k in range(K)]
+    Yt = [None] + [D.Y[:, k, :] - D.Y[:, 0, :] for k in range(1, K)]
+    Yind = np.stack([(D.choice == k).astype(float) for k in range(K)], axis=1)
+    W = lambda n, m: P[:, n] * ((n == m) - P[:, m])
+    g_parts = [M.T @ (Yind[:, k] - P[:, k]) for k, M in chunks]
+    g_parts.append(sum(Yt[k].T @ (Yind[:, k] - P[:, k]) for k in range(1, K)) if f else np.zeros(0))
+    g = np.concatenate(g_parts)
+    rows = []
+    for n, Mn in chunks:
+        row = [-(Mn.T * W(n, m)) @ Mm for m, Mm in chunks]
+        row.append(-sum((Mn.T * W(n, k)) @ Yt[k] for k in range(1, K)) if f else np.zeros((Mn.shape[1], 0)))
+        rows.append(np.hstack(row))
+    if f:
+        last = [-sum((Yt[k].T * W(k, m)) @ Mm for k in range(1, K)) for m, Mm in chunks]
+        last.append(-sum((Yt[k].T * W(k, t)) @ Yt[t] for k in range(1, K) for t in range(1, K)))
+        rows.append(np.hstack(last))
+    return g, np.vstack(rows)
+
+
+@pytest.mark.parametrize("shape", [(80, 4, 3, 2, 1), (70, 3, 1, 1, 2), (50, 5, 0, 2, 2), (64, 6, 4, 0, 0)])
+def test_oracle_equals_paper_block_formulas(shape):
+    N, K, p, f, d = shape
+    D = data_of(tiny(N, K, p, f, d, seed=15))
+    th = datagen.draw(D.n_p, 16, 5, datagen.NORMAL, 0.5)
+    g_ref, H_ref = block_form(D, th)
+    _, g, H = O.mnl_eval(D, th)
+    assert np.max(np.abs(H - H_ref)) <= 1e-12 * np.max(np.abs(H_ref))
+    assert np.max(np.abs(g - g_ref)) <= 1e-12 * np.max(np.abs(g_ref))
+    rows = np.array([0, D.n_p - 1, D.n_p // 2, 1])
+    cols = np.array([D.n_p - 1, D.n_p - 1, 0, D.n_p // 3])
+    e = O.hessian_entries(D, th, rows, cols)
+    assert np.max(np.abs(e - H_ref[rows, cols])) <= 1e-12 * np.max(np.abs(H_ref))
+
+
+# --- structure and invariants ---------------------------------------------------------------
+
+def test_hessian_symmetric_negative_definite_and_choice_independent():
+    pr = datagen.make("c1")
+    D = data_of(pr)
+    H = O.hessian(D, pr.theta_true)
+    assert np.array_equal(H, H.T)
+    assert np.linalg.eigvalsh(-H).min() > 0
+    D2 = O.Data(pr.X, pr.Y, pr.Z, (pr.choice + 1) % pr.spec.K, pr.spec.K)
+    assert np.array_equal(O.hessian(D2, pr.theta_true), H)
+
+
+def test_duplicating_individuals_doubles_everything():
+    pr = tiny(N=90, seed=17)
+    D = data_of(pr)
+    D2 = O.Data(np.vstack([pr.X, pr.X]), np.vstack([pr.Y, pr.Y]), np.vstack([pr.Z, pr.Z]),
+                np.concatenate([pr.choice, pr.choice]), pr.spec.K)
+    th = datagen.draw(D.n_p, 18, 6, datagen.NORMAL, 0.5)
+    l, g, H = O.mnl_eval(D, th)
+    l2, g2, H2 = O.mnl_eval(D2, th)
+    assert l2 == pytest.approx(2 * l, rel=1e-14)
+    assert np.allclose(g2, 2 * g, rtol=1e-12, atol=1e-12)
+    assert np.allclose(H2, 2 * H, rtol=1e-12, atol=1e-12)
+
+
+def test_generic_data_shift_invariance():
+    # Only differences against the base matter: y_ik -> y_ik + c_i leaves l, g, H unchanged
+    pr = tiny(N=90, seed=19)
+    D = data_of(pr)
+    c = datagen.draw(pr.spec.N * pr.spec.f, 20, 7, datagen.NORMAL, 3.0).reshape(pr.spec.N, 1, pr.spec.f)
+    D2 = O.Data(pr.X, pr.Y + c, pr.Z, pr.choice, pr.spec.K)
+    th = datagen.draw(D.n_p, 21, 8, datagen.NORMAL, 0.5)
+    l, g, H = O.mnl_eval(D, th)
+    l2, g2, H2 = O.mnl_eval(D2, th)
+    assert l2 == pytest.approx(l, rel=1e-12)
+    assert np.allclose(g2, g, rtol=1e-9, atol=1e-10)
+    assert np.allclose(H2, H, rtol=1e-9, atol=1e-10)
+
+
+def test_concavity():
+    D = data_of(tiny(N=120, seed=22))
+    a = datagen.draw(D.n_p, 23, 9, datagen.NORMAL, 1.0)
+    b = datagen.draw(D.n_p, 24, 9, datagen.NORMAL, 1.0)
+    for lam in (0.1, 0.5, 0.8):
+        assert O.loglik(D, lam * a + (1 - lam) * b) >= lam * O.loglik(D, a) + (1 - lam) * O.loglik(D, b) - 1e-9
+
+
+# --- Newton-Raphson ------------------------------------------------------------------------
+
+def test_intercept_only_fit_closed_form():
+    # xi_k = ln(n_k / n_0), l = sum_k n_k ln(n_k / N)
+    pr = datagen.custom(500, 5, 0, seed=25, coef_sd=0.8)
+    D = data_of(pr)
+    fit = O.newton_fit(D, tol=1e-10)
+    n = np.bincount(D.choice, minlength=D.K).astype(float)
+    assert fit.status == O.MNL_OK
+    assert np.allclose(fit.coef, np.log(n[1:] / n[0]), rtol=0, atol=1e-8)
+    assert fit.loglik == pytest.approx(np.sum(n * np.log(n / D.N)), rel=1e-12)
+
+
+def test_fit_properties_moment_condition_monotone_and_unique():
+    pr = datagen.make("c1")
+    D = data_of(pr)
+    fit = O.newton_fit(D, tol=1e-9)
+    assert fit.status == O.MNL_OK and fit.grad_norm < 1e-9
+    ls = [h["l"] for h in fit.history] + [fit.loglik]
+    assert all(b >= a for a, b in zip(ls, ls[1:]))
+    # moment condition at the MLE with an intercept: sum_i P_ik = n_k
+    P = O.probabilities(O.utilities(D, fit.coef))
+    assert np.allclose(P.sum(axis=0), np.bincount(D.choice, minlength=D.K), atol=1e-7)
+    # global concavity: a second start reaches the same optimum
+    fit2 = O.newton_fit(D, coef0=datagen.random_start(pr), tol=1e-9)
+    assert np.linalg.norm(fit2.coef - fit.coef) <= 1e-8 * np.linalg.norm(fit.coef)
+
+
+def test_K2_fit_equals_independent_irls():
+    pr = datagen.custom(600, 2, 3, f=1, d=1, seed=26, coef_sd=0.6)
+    D = data_of(pr)
+    fit = O.newton_fit(D, tol=1e-10)
+    W = np.hstack([np.ones((D.N, 1)), D.X, -D.Z[:, 0, :], D.Z[:, 1, :], D.Y[:, 1, :] - D.Y[:, 0, :]])
+    y = (D.choice == 1).astype(float)
+    b = np.zeros(W.shape[1])
+    for _ in range(50):   # textbook IRLS (weighted least squares on the working response)
+        eta = W @ b
+        s = expit(eta)
+        w = s * (1 - s)
+        zr = eta + (y - s) / w
+        b_new = np.linalg.solve((W.T * w) @ W, (W.T * w) @ zr)
+        if np.max(np.abs(b_new - b)) < 1e-14:
+            b = b_new
+            break
+        b = b_new
+    assert np.linalg.norm(fit.coef - b) <= 1e-8 * np.linalg.norm(b)
+
+
+def test_line_search_halves_on_overshoot():
+    # A start far out on a flat ridge makes the full Newton step overshoot; halving must kick in
+    # and every accepted iterate must not lower l.
+    pr = datagen.custom(200, 3, 1, seed=27, coef_sd=0.5)
+    D = data_of(pr)
+    start = np.full(D.n_p, 6.0)
+    fit = O.newton_fit(D, coef0=start, tol=1e-8)
+    assert fit.status == O.MNL_OK
+    assert sum(h["halvings"] for h in fit.history) >= 1
+    assert all(h["l_new"] >= h["l"] - 1e-12 * abs(h["l"]) for h in fit.history)
+
+
+def test_maxiter_and_zero_iter():
+    D = data_of(tiny(seed=28))
+    fit = O.newton_fit(D, tol=1e-12, max_iter=1)
+    assert fit.status == O.MNL_MAXITER and fit.iters == 1
+    fit0 = O.newton_fit(D, tol=1e-12, max_iter=0)
+    assert fit0.status == O.MNL_MAXITER and fit0.iters == 0 and np.all(fit0.coef == 0)
+
+
+def test_recovery_of_true_coefficients_c2():
+    # statistical pin (north_star "recovery of the true coefficients"): z = (theta_hat - theta_true)/se
+    pr = datagen.make("c2")
+    D = data_of(pr)
+    fit = O.newton_fit(D, tol=1e-6)
+    assert fit.status == O.MNL_OK
+    H = O.hessian(D, fit.coef)
+    se = np.sqrt(np.diag(np.linalg.inv(-H)))
+    z = (fit.coef - pr.theta_true) / se
+    assert np.max(np.abs(z)) < 5.0
+    assert 0.85 < np.sqrt(np.mean(z * z)) < 1.15
