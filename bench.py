@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the mnlogit Newton-Raphson hot path on B200 (one JSON line on rank 0).
+
+A "step" is one full Newton-Raphson iteration through the C ABI (mnl_newton_fit with
+max_iter = 1 from a fixed start): pass-1 evaluation (utilities, softmax, loglik, gradient, P
+rows), Hessian assembly, Cholesky factor + solves, the step-halving line search (>= 1 more
+evaluation) and the stopping test — every row of SURVEY.md §8(a).  Each iteration forms exactly
+one Hessian, so the metric "Hessian evals/s" = Newton iterations/s.
+
+Workload: BASELINE.json configs[3] ("c4", N=500000, K=100, p=50, n_p=5049), the largest single-GPU
+config the metric is quoted on; inputs are synthetic (datagen, seed 0), resident in HBM and larger
+than L2 (X 200 MB, probability rows 416 MB), so no L2 flush is needed between steps.
+
+--gpus N > 1: replicas only (each rank runs its own full problem).
+--impl reference: the CPU oracle (oracle/) as it stands, timed on this host's cores on a bounded
+sample of the same workload (the only other place bench.py executes oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "Hessian evals/s (Newton iterations/s), FP64"
+UNIT = "hessian_evals/s"
+
+
+def load_peaks():
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    fp64 = None
+    try:
+        fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak_r1.json")))
+    except Exception:
+        pass
+    return peaks, fp64
+
+
+def fp64_peak_tflops():
+    """Roofline denominator for the DMMA kernel: the larger of
+    (a) the measured DMMA.8x8x4 sustained peak (tools/fp64_peak.cu -> profiles/fp64_peak_r1.json) and
+    (b) MEASURED_PEAKS bf16 x the guide's nominal FP64-tensor/BF16 ratio (45 / 2250)."""
+    peaks, fp64 = load_peaks()
+    cands = []
+    if fp64 and fp64.get("dmma_tflops"):
+        cands.append((float(fp64["dmma_tflops"]), "measured DMMA.8x8x4 sustained (profiles/fp64_peak_r1.json)"))
+    if peaks.get("bf16_tflops"):
+        cands.append((float(peaks["bf16_tflops"]) * 45.0 / 2250.0,
+                      "MEASURED_PEAKS bf16_tflops x nominal FP64/BF16 ratio 45/2250"))
+    if not cands:
+        cands.append((37.0, "fallback: nominal 148 SM x 64 FMA/clk x 1.965 GHz"))
+    return max(cands)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7 and parts[0].isdigit():
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[3 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def hess_flops(spec):
+    """Algorithmic flops of one Hessian assembly:
+    F_min: the beta-beta pairs x vech GEMM (2 N (K-1)K/2 q(q+1)/2) + the Z/Y blocks;
+    F_H:   the paper's method (every upper-triangular chunk-pair block as a full DGEMM)."""
+    N, K, q, d, f = spec.N, spec.K, spec.p + 1, spec.d, spec.f
+    pairs = (K - 1) * K // 2
+    vech = q * (q + 1) // 2
+    j1 = 2.0 * N * pairs * vech
+    n_b, n_a = (K - 1) * q, K * d
+    j2 = 2.0 * N * (n_b + n_a + f) * (n_a + f) if (d + f) else 0.0
+    ar = 2.0 * N * K * (q + d + f) * (d + f) if (d + f) else 0.0
+    # paper method: upper chunk pairs as full DGEMMs
+    chunks = [q] * (K - 1) + [d] * K if d else [q] * (K - 1)
+    s = sum(chunks)
+    # sum over upper chunk pairs (incl. diagonal) of 2 N c_i c_j = N (S^2 + sum c_i^2); generic part O(K)
+    F_H = N * (s * s + sum(c * c for c in chunks)) + (2.0 * N * K * f * (s + f) if f else 0.0)
+    return dict(j1=j1, j2=j2, arrow=ar, f_min=j1 + j2 + ar, f_paper=F_H)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1404_3177_b200 as M
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    M.load()
+
+    prob = datagen.make(args.config, seed=args.seed)
+    spec = prob.spec
+    X = torch.from_numpy(prob.X).to(dev)
+    Y = torch.from_numpy(prob.Y).to(dev) if spec.f else None
+    Z = torch.from_numpy(prob.Z).to(dev) if spec.d else None
+    ch = torch.from_numpy(prob.choice.astype(np.int32)).to(dev)
+    dp = M.problem(X, Y, Z, ch, K=spec.K)
+    coef0 = torch.zeros(spec.n_params, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return M.mnl_newton_fit(dp, coef0=coef0, tol=1e-300, max_iter=1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    gemm_ms, hess_ms, chol_ms = [], [], []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+            launches += M.last_launch_count()
+            gemm_ms.append(r.stats["gemm_ms"])
+            hess_ms.append(r.stats["hess_ms"])
+            chol_ms.append(r.stats["chol_ms"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+
+    result = None
+    if rank == 0:
+        fl = hess_flops(spec)
+        peak, peak_src = fp64_peak_tflops()
+        gemm_avg = float(np.mean(gemm_ms))
+        achieved = fl["j1"] / (gemm_avg / 1e3) / 1e12
+        traffic = None
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic_r1.json"))).get(args.config)
+        except Exception:
+            pass
+        # e2e: the same step through the host-buffer C ABI (H2D of inputs + D2H of the result inside)
+        e2e = None
+        if not args.no_e2e:
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+            hX, hY, hZ = pin(prob.X), pin(prob.Y), pin(prob.Z)
+            hch = pin(prob.choice.astype(np.int32))
+            hc0 = pin(np.zeros(spec.n_params))
+            M.mnl_newton_fit_host(hX, hY if spec.f else None, hZ if spec.d else None, hch, spec.K, coef0=hc0,
+                                  tol=1e-300, max_iter=1)
+            n_e2e = max(1, min(args.steps, 5))
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                M.mnl_newton_fit_host(hX, hY if spec.f else None, hZ if spec.d else None, hch, spec.K,
+                                      coef0=hc0, tol=1e-300, max_iter=1)
+            dt = (time.perf_counter() - t0) / n_e2e
+            bi = hX.nbytes + (hY.nbytes if spec.f else 0) + (hZ.nbytes if spec.d else 0) + hch.nbytes + hc0.nbytes
+            e2e = {"value": 1.0 / dt, "unit": UNIT, "h2d_bytes_per_step": int(bi),
+                   "d2h_bytes_per_step": int(spec.n_params * 8 + 8), "steps": n_e2e}
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen seed %d)" % args.seed,
+            "config": {"workload": f"{args.config}: N={spec.N} K={spec.K} p={spec.p} f={spec.f} d={spec.d} "
+                                   f"n_p={spec.n_params}, one Newton iteration from theta=0 per step",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": "replicas" if ws > 1 else "single-gpu"},
+            "s_per_newton_iter": ms_step / 1e3,
+            "hessian_ms": float(np.mean(hess_ms)), "cholesky_solve_ms": float(np.mean(chol_ms)),
+            "roofline": {"kernel": "k_gen_gemm<128,32> (beta-beta pairs x vech DMMA GEMM, J1)",
+                         "bound": "tensor", "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_flops_per_launch": fl["j1"], "avg_launch_ms": gemm_avg,
+                         "hessian_f_min_tflops": fl["f_min"] / (float(np.mean(hess_ms)) / 1e3) / 1e12,
+                         "hessian_paper_method_equiv_tflops": fl["f_paper"] / (float(np.mean(hess_ms)) / 1e3) / 1e12},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result, prob
+
+
+def oracle_iteration_seconds(prob, n_sample: int):
+    """One oracle Newton iteration (oracle/, as it stands) on the first n_sample individuals."""
+    import oracle as O
+    s = prob.spec
+    D = O.Data(prob.X[:n_sample], prob.Y[:n_sample], prob.Z[:n_sample], prob.choice[:n_sample], s.K)
+    t0 = time.perf_counter()
+    O.newton_fit(D, coef0=None, tol=1e-300, max_iter=1)
+    return time.perf_counter() - t0
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(prob, n_sample):
+    t = oracle_iteration_seconds(prob, n_sample)
+    scale = prob.spec.N / n_sample
+    return {"value": 1.0 / (t * scale), "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"one oracle Newton iteration on the first {n_sample} of {prob.spec.N} individuals "
+                      f"of {prob.spec.name} ({t:.2f} s), time scaled x{scale:.0f} (Hessian work is linear in N)"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return None
+    prob = datagen.make(args.config, seed=args.seed)
+    n = args.oracle_sample
+    for _ in range(args.warmup):
+        oracle_iteration_seconds(prob, n)
+    times = [oracle_iteration_seconds(prob, n) for _ in range(args.steps)]
+    scale = prob.spec.N / n
+    per_step = float(np.mean(times)) * scale
+    value = 1.0 / per_step
+    cb = {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+          "sample": f"each step: one oracle Newton iteration on the first {n} of {prob.spec.N} individuals "
+                    f"of {prob.spec.name}, time scaled x{scale:.0f}"}
+    spec = prob.spec
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen seed %d)" % args.seed,
+            "config": {"workload": f"{args.config}: N={spec.N} K={spec.K} p={spec.p} f={spec.f} d={spec.d} "
+                                   f"n_p={spec.n_params}, one Newton iteration from theta=0 per step",
+                       "l2": "n/a (CPU)", "parallelism": "host cores"},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=list(datagen.CONFIGS))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--oracle-sample", type=int, default=2000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res, prob = run_ours(args)
+    if res is None:
+        return
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(prob, args.oracle_sample)
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

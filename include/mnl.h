@@ -1,0 +1,153 @@
+/* mnl.h — C ABI of the B200 (sm_100a) multinomial-logit Newton-Raphson hot path.
+ *
+ * The operations follow the paper's statement of the problem (arXiv:1404.3177,
+ * `P:n` = PAPER.md line n; section / equation named beside each):
+ *   utility          Eq. "unormalized utility" P:104-107 and "normalized utility" P:129-138
+ *   probabilities    Eqs. "probability" / "base probability" P:140-152
+ *   log-likelihood   Eq. "log-lik function" P:348-351
+ *   gradient         Eq. "loglik gradient" P:433-443 (App. A)
+ *   Hessian          Eq. "hessian block" P:462-476 (App. A), symmetry P:484
+ *   Newton step      Eq. "NR update" P:361-367, step halving P:367-371, stopping P:219-220
+ *
+ * LETTERS (SURVEY.md §0.3 — the ABI swaps the paper's Y and Z):
+ *   U_ik = xi_k + x_i.beta_k + y_ik.gamma + z_ik.alpha_k        (alternative 0 is the base:
+ *                                                                xi_0 = 0, beta_0 = 0)
+ *   X[N][p]     individual-specific data, alternative-specific coefs beta_k (k = 1..K-1) plus an
+ *               implicit intercept xi_k (a unity-valued column), never stored in X
+ *   Y[N][K][f]  alternative-varying data with ONE generic coefficient vector gamma (paper's Z/alpha)
+ *   Z[N][K][d]  alternative-varying data with alternative-specific coefficients alpha_k,
+ *               k = 0..K-1, the base included (paper's Y/gamma_k)
+ *
+ * COEFFICIENT LAYOUT (Eq. "theta vec"), n_p = (K-1)(p+1) + K d + f:
+ *   theta = [ beta_1 | ... | beta_{K-1} | alpha_0 | ... | alpha_{K-1} | gamma ]
+ *   beta_k = [ xi_k, beta_k1 .. beta_kp ]
+ *   off_beta(k) = (k-1)(p+1),  off_alpha(k) = (K-1)(p+1) + k d,  off_gamma = (K-1)(p+1) + K d
+ *
+ * CONVENTIONS. All arrays are row-major and C-contiguous. Floating point is IEEE fp64 end to end.
+ * `grad` and `hess` are derivatives of l itself (hess is negative definite).
+ * `hess` is the full symmetric n_p x n_p matrix, exactly symmetric (mirrored).
+ * Results are deterministic run to run (fixed-order reductions, no floating-point atomics).
+ *
+ * OWNERSHIP. The caller owns every buffer passed in. Device pointers must be 16-byte aligned
+ * (torch allocations are). The library owns its scratch (probabilities, packed design rows,
+ * split-N partial tiles, Cholesky workspace), cached per device and freed by mnl_release().
+ *
+ * SYNCHRONISATION. Every call enqueues on `stream` (a cudaStream_t; NULL = legacy default
+ * stream), synchronises that stream before returning, and returns a final status code.
+ * Calls are serialised internally (one scratch cache per process).
+ *
+ * SIZE LIMITS OF THIS BUILD (MNL_ERR_ARG beyond them): 2 <= K <= 256, 0 <= p <= 255,
+ * 0 <= d <= 16, 0 <= f <= 64, 1 <= N < 2^31, n_p <= 16384.
+ */
+#ifndef MNL_H_
+#define MNL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MNL_OK = 0,             /* success */
+  MNL_ERR_ARG = 1,        /* bad argument: sizes, NULL pointer, misalignment, tol <= 0,
+                             max_iter < 0, a choice outside [0, K) (checked on device) */
+  MNL_ERR_CUDA = 2,       /* a CUDA runtime error (allocation, launch) */
+  MNL_ERR_NOT_SPD = 3,    /* Cholesky of -H failed: the singular-design case of P:777-790;
+                             the paper advises relaxing tolerances */
+  MNL_ERR_LINESEARCH = 4, /* more than 30 step halvings without a non-decreasing loglik */
+  MNL_ERR_NONFINITE = 5,  /* non-finite coefficient or log-likelihood */
+  MNL_MAXITER = 6         /* warning class: max_iter Newton updates taken; outputs are valid */
+} mnl_status;
+
+/* n_p = (K-1)(p+1) + K*d + f, or -1 for K < 2 or negative sizes. */
+int64_t mnl_num_params(int32_t K, int32_t p, int32_t f, int32_t d);
+
+/* One evaluation at `coef`: log-likelihood, gradient and, when
+ * `hess` != NULL, the full Hessian.
+ *   X      dev [N][p]     NULL iff p == 0
+ *   Y      dev [N][K][f]  NULL iff f == 0
+ *   Z      dev [N][K][d]  NULL iff d == 0
+ *   choice dev [N]        int32 in [0, K), 0 = base alternative
+ *   coef   dev [n_p]
+ *   loglik dev [1]        out
+ *   grad   dev [n_p]      out, or NULL
+ *   hess   dev [n_p*n_p]  out, or NULL
+ * Errors: MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NONFINITE (non-finite loglik). */
+int mnl_eval(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+             const double* X, const double* Y, const double* Z, const int32_t* choice,
+             const double* coef, double* loglik, double* grad, double* hess, void* stream);
+
+/* Newton-Raphson maximum-likelihood fit.
+ *   coef0   dev [n_p] start, or NULL => zeros (reading R9)
+ *   tol     ||grad||_2 threshold (gtol; reading R10), > 0
+ *   max_iter >= 0 Newton updates; 0 => evaluate only
+ *   coef    dev [n_p] out (may alias coef0)
+ *   iters   host out: accepted Newton updates
+ *   loglik  host out: l at the returned coef
+ * Each iteration: (l, g) at theta; stop if ||g|| < tol (before forming H, reading R11) or if
+ * iters == max_iter (MNL_MAXITER); H; Cholesky of -H (MNL_ERR_NOT_SPD); delta = (-H)^{-1} g;
+ * accept the first theta + delta/2^j, j = 0..30, with l_j >= l - 1e-12 max(1,|l|) (reading R7);
+ * else MNL_ERR_LINESEARCH. */
+int mnl_newton_fit(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                   const double* X, const double* Y, const double* Z, const int32_t* choice,
+                   const double* coef0, double tol, int32_t max_iter,
+                   double* coef, int32_t* iters, double* loglik, void* stream);
+
+/* Per-fit report (the paper's est.stat). */
+typedef struct {
+  int32_t iters;            /* accepted Newton updates */
+  int32_t halvings;         /* total step halvings (the paper's "linesearch iterations") */
+  int32_t evals;            /* log-likelihood evaluations */
+  int32_t status;
+  double grad_norm;         /* ||g||_2 at the returned coef */
+  double loglik;
+  double hess_ms;           /* device time in Hessian assembly, summed over iterations */
+  double chol_ms;           /* device time in Cholesky factor + solves */
+  double eval_ms;           /* device time in log-likelihood / gradient passes */
+  double total_ms;          /* wall time of the call */
+  double gemm_ms;           /* device time of the beta-beta DMMA GEMM kernel (J1), summed */
+  int32_t halvings_per_iter[64];  /* first 64 iterations */
+} mnl_fit_stats;
+
+/* mnl_newton_fit plus the report (stats may be NULL). */
+int mnl_newton_fit_ex(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                      const double* X, const double* Y, const double* Z, const int32_t* choice,
+                      const double* coef0, double tol, int32_t max_iter,
+                      double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats,
+                      void* stream);
+
+/* Host-buffer variants: every pointer is HOST memory (pinned or pageable). The call copies the
+ * inputs to the device, runs the same path and copies the outputs back, all inside the call. */
+int mnl_eval_host(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                  const double* X, const double* Y, const double* Z, const int32_t* choice,
+                  const double* coef, double* loglik, double* grad, double* hess);
+int mnl_newton_fit_host(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                        const double* X, const double* Y, const double* Z, const int32_t* choice,
+                        const double* coef0, double tol, int32_t max_iter,
+                        double* coef, int32_t* iters, double* loglik);
+
+/* Device-side pieces of the Newton step, exposed for tests and benchmarks. */
+/* Cholesky A = L L^T of the SPD dev [n][n] row-major A, in place (lower triangle holds L;
+ * the strict upper triangle is left undefined). MNL_ERR_NOT_SPD if a pivot is <= 0 or NaN. */
+int mnl_cholesky(int32_t n, double* A, void* stream);
+/* Solve (L L^T) x = b given the factor from mnl_cholesky; b and x dev [n], may alias. */
+int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, void* stream);
+
+/* Device times (ms, CUDA events on the call's stream) of the last Hessian assembly:
+ * out[0] beta-beta DMMA GEMM kernel (J1), out[1] its split-N reduction, out[2] the Z/Y blocks
+ * (J2 GEMM + reduction + same-alternative terms), out[3] the symmetric assembly. */
+int mnl_last_hessian_times(double out[4]);
+
+/* Kernel launches made by the last call on this thread (for the bench's gpu_launches). */
+int64_t mnl_last_launch_count(void);
+
+const char* mnl_status_string(int code);
+
+/* Free the library's cached device scratch. */
+void mnl_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MNL_H_ */

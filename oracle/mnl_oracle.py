@@ -179,11 +179,11 @@ def jac_row_support(D: Data, k: int) -> list[int]:
     return cols
 
 
-def jac_row_block(D: Data, k: int, cols: list[int]) -> np.ndarray:
-    """J_(k)[:, cols]: the N x |cols| matrix of J_i[k, c]."""
+def jac_row_block(D: Data, k: int, cols: list[int], cache: dict | None = None) -> np.ndarray:
+    """J_(k)[:, cols]: the N x |cols| matrix of J_i[k, c] (columns from jac_column, optionally cached)."""
     out = np.zeros((D.N, len(cols)))
     for j, c in enumerate(cols):
-        ks, vals = jac_column(D, c)
+        ks, vals = cache[c] if cache is not None and c in cache else jac_column(D, c)
         if k in ks:
             out[:, j] = vals[:, ks.index(k)]
     return out
@@ -225,9 +225,11 @@ def hessian(D: Data, theta, P: np.ndarray | None = None) -> np.ndarray:
     A = U.T @ U
     del U
     S = np.zeros((n_p, n_p))
+    shared = {c: jac_column(D, c) for c in range(D.off_alpha, D.off_alpha + D.d)}   # alpha_0: every row
+    shared.update({c: jac_column(D, c) for c in range(D.off_gamma, n_p)})          # gamma: every row
     for k in range(1, D.K):
         cols = jac_row_support(D, k)
-        Jk = jac_row_block(D, k, cols)
+        Jk = jac_row_block(D, k, cols, shared)
         S[np.ix_(cols, cols)] += Jk.T @ (P[:, k][:, None] * Jk)
     H = -(S - A)
     return 0.5 * (H + H.T)   # exact symmetry; both halves are the same sum up to rounding order

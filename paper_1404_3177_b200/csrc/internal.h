@@ -1,0 +1,88 @@
+// Internal declarations shared by the CUDA translation units of libmnl.so.
+// (Not part of the ABI; see include/mnl.h.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mnl {
+
+// Problem dimensions and the layout constants derived from them.
+struct Dims {
+  int64_t N;      // individuals
+  int K, p, f, d; // alternatives, X cols, Y (generic) cols, Z (alt-specific) cols
+  int q;          // p + 1 (intercept first)
+  int n_beta;     // (K-1) q
+  int n_alpha;    // K d
+  int n_p;        // n_beta + n_alpha + f
+  int off_alpha;  // = n_beta
+  int off_gamma;  // = n_beta + n_alpha
+};
+
+// Packed per-individual rows in library scratch.
+// Row strides are even (16-byte rows for bulk copies) and = 8 (mod 16) doubles, which makes
+// the 4-row x 8-column fragment gathers of the Hessian generator bank-conflict-free.
+struct Packed {
+  int64_t Npad;   // N rounded up to a multiple of kRowPad; rows >= N are zero
+  int ldX;        // Xp [Npad][ldX]: 1, x_i1..x_ip, 0...
+  int ldZ;        // Zp [Npad][ldZ]: z_i (K*d), 0...
+  int ldP;        // Pr [Npad][ldP]: P_i0..P_i,K-1, ybar_i1..ybar_if, 0...
+  double* Xp;
+  double* Zp;
+  double* Pr;
+};
+
+constexpr int kRowPad = 64;   // Npad multiple (>= the largest chunk KC)
+
+inline int pad8mod16(int n) {  // smallest m >= n with m % 16 == 8
+  int m = (n + 7) / 8 * 8;
+  if (m % 16 != 8) m += 8;
+  return m;
+}
+
+// ---- launch accounting --------------------------------------------------------------
+void count_launch(int n = 1);
+
+// ---- k_eval.cu -------------------------------------------------------------------------
+// Per-CTA partials layout: [2 + n_p] doubles: l_sum, l_comp, grad[n_p].
+struct EvalPlan {
+  int grid, block, kpl;
+  size_t smem;
+  int n_part;  // 2 + n_p
+};
+bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
+// Pass 1 (a1-a4): utilities, softmax, loglik partials, gradient partials (if want_grad),
+// and the probability rows Pr (if writeP). part: [grid][n_part].
+cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
+                        const double* Z, const int32_t* choice, const double* coef,
+                        const Packed* pk, bool want_grad, bool writeP, double* part, int* err,
+                        cudaStream_t st);
+// Fixed-order reduction of the CTA partials -> loglik, grad (optional); scal[0] = l,
+// scal[1] = ||g||^2, scal[2] = err flag (as double). `counter` is a zeroed int.
+cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const double* part,
+                                 bool want_grad, double* grad, double* loglik_out, double* scal,
+                                 const int* err, unsigned* counter, cudaStream_t st);
+cudaError_t launch_pack(const Dims& D, const Packed& pk, const double* X, const double* Z,
+                        cudaStream_t st);
+cudaError_t launch_axpy_pow2(int n, const double* theta, const double* delta, int j,
+                             double* out, cudaStream_t st);
+
+// ---- k_hess.cu -------------------------------------------------------------------------
+struct HessPlan;
+HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int device_sms);
+void hess_plan_destroy(HessPlan*);
+size_t hess_plan_bytes(const HessPlan*);
+// Assemble the Hessian from Pr/Xp/Zp (+ Y for the arrow part). sign = +1 writes H,
+// sign = -1 writes -H (the Newton system matrix). out: [n_p][ld_out].
+cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y,
+                           double* out, int ld_out, double sign, cudaStream_t st);
+// Phase times of the last launch_hessian (valid once the stream has passed it).
+void hess_last_times(HessPlan* hp, double out[4]);
+
+// ---- k_chol.cu -------------------------------------------------------------------------
+// In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.
+cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t st);
+// x = (L L^T)^{-1} b ; x may alias b; work: n doubles.
+cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, double* x,
+                              cudaStream_t st);
+
+}  // namespace mnl

@@ -1,0 +1,670 @@
+// Hessian assembly on the FP64 tensor pipe (DMMA).
+//
+// -H = sum_i J_i^T (diag p_i - p_i p_i^T) J_i is split into three contractions over the
+// individuals i, each a sum of rank-1 terms whose factors are generated on chip from the
+// per-individual rows Pr = [P_i | ybar_i], Xp = [1 | x_i], Zp = [z_i] (never an N x n_p matrix):
+//
+//  J1  beta-beta (Eq. "hessian block" case 1 with M = X):
+//        -H[(k,a),(l,b)] = sum_i w_kl,i x~_ia x~_ib,  w_kl,i = P_ik (delta_kl - P_il)
+//      computed for k <= l (block symmetry P:484) AND a <= b (each block is symmetric since
+//      x~ x~^T is): one GEMM  C1[pair(k,l)][vech(a,b)] = sum_i W[i][pair] * S[i][vech],
+//      W[i][(k,l)] = P_ik (delta_kl - P_il) and S[i][(a,b)] = x~_ia x~_ib generated in smem —
+//      each X tile is staged once and reused for every (k,l) weight pair of the output tile.
+//  J2  blocks touching the alternative-specific Z or the generic Y (cases 1-3 of P:469-471 with
+//      M = Z_k, and the O(K) regrouping of the generic blocks):
+//        U[i][r] = sum_k P_ik J_i[k][r]  (= P_ik m_ik for beta/alpha columns, ybar_i for gamma)
+//        C2 = U^T U restricted to columns alpha u gamma  (rows: all n_p)
+//  J3  the same-alternative ("delta_kl") terms of those blocks, per alternative k:
+//        T_k = sum_i P_ik e_ik f_ik^T,  e = [x~_i, z_ik, y_ik], f = [z_ik, y_ik]
+//  so that  -H = C1 (beta-beta)  and  -H = T - C2 (every other entry).
+//
+// J1/J2 run one persistent, warp-level DMMA kernel (mma.sync.m8n8k4.f64 — tcgen05 has no f64
+// kind on sm_100a): 128 x BN output tiles, 8 warps, inner dimension = individuals in chunks of
+// KC; per chunk the raw rows are fetched by one cp.async.bulk (TMA bulk copy) per segment into
+// a double-buffered stage, every thread generates its fragment-native operand elements
+// (v = R[o1] * (c0 + s R[o2])) into double-buffered smem, and the warps issue DMMAs from it.
+// Split-N partial tiles are reduced in a fixed order (deterministic), then k_assemble gathers
+// H (exactly symmetric) into the caller's row-major n_p x n_p buffer.
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "internal.h"
+
+namespace mnl {
+
+struct ColDesc {
+  int o1, ld1, o2, ld2;  // stage offsets (doubles) of the two factors for row 0, and row strides
+  double c0, s;          // value = R[o1] * (c0 + s * R[o2])
+};
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int NT = 256;
+
+struct GemmParams {
+  const ColDesc* descA;
+  const ColDesc* descB;
+  int tilesM, tilesN, splits;
+  int64_t nchunks;
+  double* C;
+  int ldc;
+  int64_t split_stride;
+  int nseg;
+  const double* seg_ptr[3];
+  int seg_ld[3];
+  int seg_off[3];
+  int stage_doubles;
+  unsigned stage_bytes;
+  unsigned* counter;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_stage(const GemmParams& P, double* dst, int64_t chunk, int KC,
+                                          uint64_t* bar) {
+  const unsigned b = smem_u32(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(P.stage_bytes)
+               : "memory");
+  for (int s = 0; s < P.nseg; ++s) {
+    const double* src = P.seg_ptr[s] + chunk * KC * (int64_t)P.seg_ld[s];
+    const unsigned bytes = (unsigned)(KC * P.seg_ld[s] * 8);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst + P.seg_off[s])),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+struct Gen {  // one generated column, pre-offset to this lane's row (i % 4)
+  int p1, s1, p2, s2;
+  double c0, s;
+};
+__device__ __forceinline__ Gen make_gen(const ColDesc& d, int r4) {
+  Gen g;
+  g.p1 = d.o1 + r4 * d.ld1;
+  g.s1 = 4 * d.ld1;
+  g.p2 = d.o2 + r4 * d.ld2;
+  g.s2 = 4 * d.ld2;
+  g.c0 = d.c0;
+  g.s = d.s;
+  return g;
+}
+__device__ __forceinline__ double gen_val(const double* R, const Gen& g, int ks) {
+  return R[g.p1 + ks * g.s1] * fma(g.s, R[g.p2 + ks * g.s2], g.c0);
+}
+
+template <int BN, int KC>
+__global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
+  constexpr int WARPS_M = (BN == 128) ? 2 : 4;
+  constexpr int WARPS_N = 8 / WARPS_M;
+  constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  constexpr int MT = WTM / 8, NTL = WTN / 8;
+  constexpr int KS = KC / 4;
+  constexpr int PBA = BM / 16, PBB = BN / 16;
+  constexpr int GA_D = KS * PBA * 64, GB_D = KS * PBB * 64;  // doubles per buffer
+  static_assert(PBA == 8, "A generator assumes 8 pair-blocks (one per warp)");
+
+  extern __shared__ __align__(128) double sm[];
+  double* GA = sm;                          // [2][KS][PBA][32][2]
+  double* GB = GA + 2 * GA_D;               // [2][KS][PBB][32][2]
+  double* RAW = GB + 2 * GB_D;              // [2][stage_doubles]
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ int s_item;
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w / WARPS_N, wn = w % WARPS_N;
+  const int r4 = lane & 3, cl = lane >> 2;
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int tiles = P.tilesM * P.tilesN;
+  const int total = tiles * P.splits;
+  unsigned gc = 0;  // chunks consumed by this CTA (buffer = gc & 1, parity = (gc >> 1) & 1)
+
+  for (;;) {
+    if (tid == 0) s_item = (int)atomicAdd(P.counter, 1u);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) break;
+    const int split = item / tiles, t = item - split * tiles;
+    const int tm = t / P.tilesN, tn = t - tm * P.tilesN;
+    const int64_t c_begin = split * P.nchunks / P.splits;
+    const int64_t c_end = (split + 1) * P.nchunks / P.splits;
+
+    // per-thread generator columns (constant over the item)
+    const Gen gA0 = make_gen(P.descA[tm * BM + (2 * w) * 8 + cl], r4);
+    const Gen gA1 = make_gen(P.descA[tm * BM + (2 * w + 1) * 8 + cl], r4);
+    const int pbB = w % PBB;
+    const Gen gB0 = make_gen(P.descB[tn * BN + (2 * pbB) * 8 + cl], r4);
+    const Gen gB1 = make_gen(P.descB[tn * BN + (2 * pbB + 1) * 8 + cl], r4);
+
+    if (tid == 0) {
+      for (int64_t c = c_begin; c < c_end && c < c_begin + 2; ++c) {
+        const unsigned b = (gc + (unsigned)(c - c_begin)) & 1u;
+        tma_stage(P, RAW + b * P.stage_doubles, c, KC, &mbar[b]);
+      }
+    }
+
+    double acc[MT][NTL][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int64_t c = c_begin; c < c_end; ++c, ++gc) {
+      const unsigned b = gc & 1u;
+      mbar_wait(&mbar[b], (gc >> 1) & 1u);
+      const double* R = RAW + b * P.stage_doubles;
+      double* ga = GA + b * GA_D;
+      double* gb = GB + b * GB_D;
+      // ---- generate operand fragments (fragment-native layout, one double2 per lane) ----
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        double2 v;
+        v.x = gen_val(R, gA0, ks);
+        v.y = gen_val(R, gA1, ks);
+        reinterpret_cast<double2*>(ga)[(ks * PBA + w) * 32 + lane] = v;
+      }
+#pragma unroll
+      for (int j = 0; j < (PBB * KS) / 8; ++j) {
+        const int ks = (w + 8 * j) / PBB;
+        double2 v;
+        v.x = gen_val(R, gB0, ks);
+        v.y = gen_val(R, gB1, ks);
+        reinterpret_cast<double2*>(gb)[(ks * PBB + pbB) * 32 + lane] = v;
+      }
+      __syncthreads();
+      if (tid == 0 && c + 2 < c_end) tma_stage(P, RAW + b * P.stage_doubles, c + 2, KC, &mbar[b]);
+      // ---- DMMA on this chunk ----
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        double af[MT], bf[NTL];
+#pragma unroll
+        for (int mp = 0; mp < MT / 2; ++mp) {
+          const double2 v = reinterpret_cast<const double2*>(ga)[(ks * PBA + wm * (MT / 2) + mp) * 32 + lane];
+          af[2 * mp] = v.x;
+          af[2 * mp + 1] = v.y;
+        }
+#pragma unroll
+        for (int np = 0; np < NTL / 2; ++np) {
+          const double2 v = reinterpret_cast<const double2*>(gb)[(ks * PBB + wn * (NTL / 2) + np) * 32 + lane];
+          bf[2 * np] = v.x;
+          bf[2 * np + 1] = v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    // ---- epilogue: this split's partial tile ----
+    double* Cb = P.C + split * P.split_stride;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int64_t row = (int64_t)tm * BM + wm * WTM + i * 8 + cl;
+#pragma unroll
+      for (int j = 0; j < NTL; ++j) {
+        const int col = tn * BN + wn * WTN + j * 8 + 2 * r4;
+        *reinterpret_cast<double2*>(Cb + row * P.ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+  }
+}
+
+// Fixed-order split reduction: dst[e] = sum_s src[s * stride + e]  (stride even).
+__global__ void k_reduce_splits(double* __restrict__ dst, const double* __restrict__ src, int64_t n,
+                                int S, int64_t stride) {
+  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 2; e < n;
+       e += (int64_t)gridDim.x * blockDim.x * 2) {
+    if (e + 1 < n) {
+      double2 acc = *reinterpret_cast<const double2*>(src + e);
+      for (int s = 1; s < S; ++s) {
+        const double2 v = *reinterpret_cast<const double2*>(src + s * stride + e);
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      *reinterpret_cast<double2*>(dst + e) = acc;
+    } else {
+      double acc = src[e];
+      for (int s = 1; s < S; ++s) acc += src[s * stride + e];
+      dst[e] = acc;
+    }
+  }
+}
+
+// J3: T_k = sum_i P_ik e_ik f_ik^T for one alternative k over a split of the individuals.
+// e = [x~_i (q; absent for k = 0), z_ik (d), y_ik (f)], f = [z_ik (d), y_ik (f)].
+constexpr int AR_TI = 32;
+__global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, int f, int splits,
+                                               int64_t nchunks, const double* __restrict__ Pr, int ldP,
+                                               const double* __restrict__ Xp, int ldX,
+                                               const double* __restrict__ Zp, int ldZ,
+                                               const double* __restrict__ Y, double* Tpart) {
+  extern __shared__ __align__(16) double sm[];
+  const int E = q + d + f, F = d + f;
+  double* Sv = sm;               // [AR_TI][E]  P_ik e_ik
+  double* Sh = Sv + AR_TI * E;   // [AR_TI][F]  f_ik
+  const int k = blockIdx.x % K, split = blockIdx.x / K;
+  const int64_t c_begin = split * nchunks / splits, c_end = (split + 1) * nchunks / splits;
+  const int tid = threadIdx.x;
+  const int n_ent = E * F;
+  const int64_t tstride = ((int64_t)K * n_ent + 1) / 2 * 2;
+  double* out = Tpart + split * tstride + (int64_t)k * n_ent;
+  for (int base = 0; base < n_ent; base += 256 * 8) {
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (int64_t c = c_begin; c < c_end; ++c) {
+      const int64_t i0 = c * AR_TI;
+      __syncthreads();
+      for (int e = tid; e < AR_TI * (E + F); e += 256) {
+        const int i = e / (E + F), r = e - i * (E + F);
+        const int64_t row = i0 + i;
+        double v = 0.0;
+        if (row < N) {
+          int rr = r < E ? r : r - E + q;  // Sh entries map to e-index q + (0..F)
+          if (rr < q) v = (k == 0) ? 0.0 : Xp[row * ldX + rr];
+          else if (rr < q + d) v = Zp[row * ldZ + k * d + (rr - q)];
+          else v = Y[(row * K + k) * f + (rr - q - d)];
+          if (r < E) v *= Pr[row * ldP + k];
+        }
+        if (r < E) Sv[i * E + r] = v;
+        else Sh[i * F + (r - E)] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int ent = base + tid + 256 * j;
+        if (ent < n_ent) {
+          const int r = ent / F, cc = ent - r * F;
+          double a = acc[j];
+          for (int i = 0; i < AR_TI; ++i) a = fma(Sv[i * E + r], Sh[i * F + cc], a);
+          acc[j] = a;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int ent = base + tid + 256 * j;
+      if (ent < n_ent) out[ent] = acc[j];
+    }
+  }
+}
+
+struct AsmArgs {
+  int K, q, d, f, n_beta, off_gamma, n_p;
+  const double* C1;  // [pairs_pad][ld1]  (reduced)
+  int ld1;
+  const double* C2;  // [n_p_pad][ld2]    (reduced)
+  int ld2;
+  const double* T;   // [K][E][F]         (reduced)
+  double* out;
+  int ld_out;
+  double sign;
+};
+
+__device__ __forceinline__ int64_t tri_index(int i, int j, int n) {  // i <= j < n, row-major upper
+  return (int64_t)i * n - (int64_t)i * (i - 1) / 2 + (j - i);
+}
+
+__global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
+  const int n_p = A.n_p, q = A.q, d = A.d, f = A.f;
+  const int E = q + d + f, F = d + f;
+  const int M = A.K - 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n_p * n_p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / n_p), c = (int)(e - (int64_t)r * n_p);
+    double negH;
+    if (r < A.n_beta && c < A.n_beta) {
+      int k1 = r / q, a1 = r - k1 * q, k2 = c / q, a2 = c - k2 * q;  // 0-based k-1
+      const int kl = min(k1, k2), kh = max(k1, k2), al = min(a1, a2), ah = max(a1, a2);
+      negH = A.C1[tri_index(kl, kh, M) * A.ld1 + tri_index(al, ah, q)];
+    } else {
+      const int lo = min(r, c), hi = max(r, c);
+      double u = A.C2[(int64_t)lo * A.ld2 + (hi - A.n_beta)];
+      // same-alternative / generic terms T (J3)
+      double tv = 0.0;
+      auto cls = [&](int x, int& kind, int& k, int& idx) {
+        if (x < A.n_beta) { kind = 0; k = x / q + 1; idx = x - (k - 1) * q; }
+        else if (x < A.off_gamma) { kind = 1; k = (x - A.n_beta) / d; idx = x - A.n_beta - k * d; }
+        else { kind = 2; k = -1; idx = x - A.off_gamma; }
+      };
+      int kl, kkl, il, kh, kkh, ih;
+      cls(lo, kl, kkl, il);
+      cls(hi, kh, kkh, ih);
+      // e-index of the row factor, f-index of the column factor (hi is alpha or gamma)
+      const int fi = (kh == 1) ? ih : d + ih;
+      if (kl == 2) {  // gamma-gamma: sum over alternatives
+        for (int k = 0; k < A.K; ++k) tv += A.T[((int64_t)k * E + q + d + il) * F + fi];
+      } else if (kh == 2) {  // beta/alpha x gamma: alternative of lo
+        const int ei = (kl == 0) ? il : q + il;
+        tv = A.T[((int64_t)kkl * E + ei) * F + fi];
+      } else if (kkl == kkh) {  // beta/alpha x alpha of the same alternative
+        if (kl == 0) tv = A.T[((int64_t)kkl * E + il) * F + fi];
+        else {
+          const int x = min(il, ih), y = max(il, ih);
+          tv = A.T[((int64_t)kkl * E + q + x) * F + y];
+        }
+      }
+      negH = tv - u;
+    }
+    A.out[(int64_t)r * A.ld_out + c] = -A.sign * negH;
+  }
+}
+
+template <int BN, int KC>
+size_t gemm_smem_bytes(int stage_doubles) {
+  constexpr int KS = KC / 4;
+  return (size_t)(2 * KS * 8 * 64 + 2 * KS * (BN / 16) * 64 + 2 * stage_doubles) * sizeof(double);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// Host plan
+// ------------------------------------------------------------------------------------------
+
+struct GemmJob {
+  int BN, KC;
+  int MA, MB, tilesM, tilesN, splits;
+  int64_t nchunks;
+  ColDesc* dA = nullptr;  // device
+  ColDesc* dB = nullptr;
+  double* Cpart = nullptr;  // [splits][tilesM*128][tilesN*BN]
+  double* Cred = nullptr;   // [tilesM*128][tilesN*BN]
+  int ldc;
+  int64_t split_stride;
+  int nseg;
+  int seg_id[3];
+  int stage_doubles;
+  size_t smem;
+};
+
+struct HessPlan {
+  bool has_j2;
+  GemmJob j1, j2;
+  int ar_splits;
+  int64_t ar_nchunks;
+  double* Tpart = nullptr;
+  double* T = nullptr;
+  size_t ar_smem;
+  unsigned* counters = nullptr;  // [2]
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t bytes = 0;
+  int sms;
+};
+
+static int choose_splits(int tiles, int64_t nchunks, int sms, int min_chunks) {
+  int best = 1;
+  double best_eff = -1.0;
+  for (int S = 1; S <= 256; ++S) {
+    if (nchunks / S < min_chunks && S > 1) break;
+    const int64_t items = (int64_t)tiles * S;
+    const int64_t waves = (items + sms - 1) / sms;
+    const double eff = (double)items / (double)(waves * sms);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = S; }
+    if (eff > 0.995) break;
+  }
+  return best;
+}
+
+static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vector<ColDesc>& B, int BN,
+                      int KC, const Packed& pk, const int* segs, int nseg, int sms, size_t* bytes) {
+  J.BN = BN;
+  J.KC = KC;
+  J.MA = (int)A.size();
+  J.MB = (int)B.size();
+  J.tilesM = (J.MA + BM - 1) / BM;
+  J.tilesN = (J.MB + BN - 1) / BN;
+  J.nchunks = pk.Npad / KC;
+  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms, 4);
+  J.ldc = J.tilesN * BN;
+  J.split_stride = (int64_t)J.tilesM * BM * J.ldc;
+  J.nseg = nseg;
+  int off = 0;
+  for (int s = 0; s < nseg; ++s) {
+    J.seg_id[s] = segs[s];
+    const int ld = segs[s] == 0 ? pk.ldP : (segs[s] == 1 ? pk.ldX : pk.ldZ);
+    off += KC * ld;
+  }
+  J.stage_doubles = off;
+  // descriptors padded to whole tiles; padding columns generate exact zeros
+  std::vector<ColDesc> hA(A), hB(B);
+  ColDesc zero{0, 0, 0, 0, 0.0, 0.0};
+  hA.resize((size_t)J.tilesM * BM, zero);
+  hB.resize((size_t)J.tilesN * BN, zero);
+  if (cudaMalloc(&J.dA, hA.size() * sizeof(ColDesc)) != cudaSuccess) return false;
+  if (cudaMalloc(&J.dB, hB.size() * sizeof(ColDesc)) != cudaSuccess) return false;
+  cudaMemcpy(J.dA, hA.data(), hA.size() * sizeof(ColDesc), cudaMemcpyHostToDevice);
+  cudaMemcpy(J.dB, hB.data(), hB.size() * sizeof(ColDesc), cudaMemcpyHostToDevice);
+  const size_t cbytes = (size_t)J.split_stride * sizeof(double);
+  if (cudaMalloc(&J.Cpart, cbytes * J.splits) != cudaSuccess) return false;
+  if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
+  *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
+  if (BN == 128 && KC == 32) J.smem = gemm_smem_bytes<128, 32>(J.stage_doubles);
+  else if (BN == 128 && KC == 16) J.smem = gemm_smem_bytes<128, 16>(J.stage_doubles);
+  else if (BN == 64 && KC == 32) J.smem = gemm_smem_bytes<64, 32>(J.stage_doubles);
+  else J.smem = gemm_smem_bytes<64, 16>(J.stage_doubles);
+  return J.smem <= 220 * 1024;
+}
+
+static void free_job(GemmJob& J) {
+  cudaFree(J.dA);
+  cudaFree(J.dB);
+  cudaFree(J.Cpart);
+  cudaFree(J.Cred);
+  J.dA = J.dB = nullptr;
+  J.Cpart = J.Cred = nullptr;
+}
+
+HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
+  HessPlan* hp = new HessPlan();
+  hp->sms = sms;
+  const int K = D.K, q = D.q, d = D.d, f = D.f;
+  // stage layouts: segment 0 = Pr, 1 = Xp, 2 = Zp; offsets are set per job below
+  auto seg_ld = [&](int s) { return s == 0 ? pk.ldP : (s == 1 ? pk.ldX : pk.ldZ); };
+  bool ok = true;
+  size_t bytes = 0;
+  {  // J1: pairs x vech over Pr + Xp
+    const int segs[2] = {0, 1};
+    for (int KC : {32, 16}) {
+      const int offP = 0, offX = KC * seg_ld(0);
+      std::vector<ColDesc> A, B;
+      for (int k = 1; k < K; ++k)
+        for (int l = k; l < K; ++l)
+          A.push_back(ColDesc{offP + k, pk.ldP, offP + l, pk.ldP, k == l ? 1.0 : 0.0, -1.0});
+      for (int a = 0; a < q; ++a)
+        for (int b = a; b < q; ++b) B.push_back(ColDesc{offX + a, pk.ldX, offX + b, pk.ldX, 0.0, 1.0});
+      // padding columns point at Xp[.][0] (finite) with c0 = s = 0
+      if (setup_job(hp->j1, A, B, 128, KC, pk, segs, 2, sms, &bytes)) break;
+      free_job(hp->j1);
+      if (KC == 16) ok = false;
+    }
+  }
+  hp->has_j2 = (d + f) > 0;
+  if (ok && hp->has_j2) {
+    const int segs[3] = {0, 1, 2};
+    const int nseg = d > 0 ? 3 : 2;
+    for (int KC : {32, 16}) {
+      const int offP = 0, offX = KC * seg_ld(0), offZ = offX + KC * seg_ld(1);
+      std::vector<ColDesc> A, B;
+      for (int k = 1; k < K; ++k)
+        for (int a = 0; a < q; ++a) A.push_back(ColDesc{offP + k, pk.ldP, offX + a, pk.ldX, 0.0, 1.0});
+      std::vector<ColDesc> AG;
+      for (int k = 0; k < K; ++k)
+        for (int c = 0; c < d; ++c) AG.push_back(ColDesc{offP + k, pk.ldP, offZ + k * d + c, pk.ldZ, 0.0, 1.0});
+      for (int e = 0; e < f; ++e) AG.push_back(ColDesc{offP + K + e, pk.ldP, offX + 0, pk.ldX, 0.0, 1.0});
+      A.insert(A.end(), AG.begin(), AG.end());
+      B = AG;
+      // choose BN: 64 unless the B side is large
+      const int BN = (int)B.size() > 96 * 2 ? 128 : 64;
+      if (setup_job(hp->j2, A, B, BN, KC, pk, segs, nseg, sms, &bytes)) break;
+      free_job(hp->j2);
+      if (KC == 16) ok = false;
+    }
+    const int E = q + d + f, F = d + f;
+    hp->ar_nchunks = pk.Npad / AR_TI;
+    int S = 1;
+    while ((int64_t)K * S < 2 * sms && hp->ar_nchunks / (S * 2) >= 4) S *= 2;
+    hp->ar_splits = S;
+    const size_t tb = ((size_t)K * E * F + 1) / 2 * 2 * sizeof(double);
+    if (cudaMalloc(&hp->Tpart, tb * S) != cudaSuccess) ok = false;
+    if (cudaMalloc(&hp->T, tb) != cudaSuccess) ok = false;
+    bytes += tb * (S + 1);
+    hp->ar_smem = (size_t)AR_TI * (E + F) * sizeof(double);
+  }
+  for (auto& e : hp->ev) cudaEventCreate(&e);
+  if (cudaMalloc(&hp->counters, 2 * sizeof(unsigned)) != cudaSuccess) ok = false;
+  else cudaMemset(hp->counters, 0, 2 * sizeof(unsigned));
+  hp->bytes = bytes;
+  if (!ok) {
+    hess_plan_destroy(hp);
+    return nullptr;
+  }
+  return hp;
+}
+
+void hess_plan_destroy(HessPlan* hp) {
+  if (!hp) return;
+  free_job(hp->j1);
+  free_job(hp->j2);
+  cudaFree(hp->Tpart);
+  cudaFree(hp->T);
+  cudaFree(hp->counters);
+  for (auto& e : hp->ev)
+    if (e) cudaEventDestroy(e);
+  delete hp;
+}
+
+size_t hess_plan_bytes(const HessPlan* hp) { return hp ? hp->bytes : 0; }
+
+template <int BN, int KC>
+static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st) {
+  GemmParams P;
+  P.descA = J.dA;
+  P.descB = J.dB;
+  P.tilesM = J.tilesM;
+  P.tilesN = J.tilesN;
+  P.splits = J.splits;
+  P.nchunks = J.nchunks;
+  P.C = J.Cpart;
+  P.ldc = J.ldc;
+  P.split_stride = J.split_stride;
+  P.nseg = J.nseg;
+  int off = 0;
+  for (int s = 0; s < J.nseg; ++s) {
+    const int id = J.seg_id[s];
+    P.seg_ptr[s] = id == 0 ? pk.Pr : (id == 1 ? pk.Xp : pk.Zp);
+    P.seg_ld[s] = id == 0 ? pk.ldP : (id == 1 ? pk.ldX : pk.ldZ);
+    P.seg_off[s] = off;
+    off += KC * P.seg_ld[s];
+  }
+  P.stage_doubles = off;
+  P.stage_bytes = (unsigned)(off * 8);
+  P.counter = counter;
+  static bool attr[4] = {false, false, false, false};
+  const int ai = (BN == 128 ? 0 : 2) + (KC == 32 ? 0 : 1);
+  if (!attr[ai]) {
+    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024);
+    if (e != cudaSuccess) return e;
+    attr[ai] = true;
+  }
+  const int items = J.tilesM * J.tilesN * J.splits;
+  const int grid = std::min(items, sms);
+  cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+  k_gen_gemm<BN, KC><<<grid, NT, J.smem, st>>>(P);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
+                           cudaEvent_t after_gemm = nullptr) {
+  cudaError_t e;
+  if (J.BN == 128 && J.KC == 32) e = run_gemm<128, 32>(J, pk, counter, sms, st);
+  else if (J.BN == 128) e = run_gemm<128, 16>(J, pk, counter, sms, st);
+  else if (J.KC == 32) e = run_gemm<64, 32>(J, pk, counter, sms, st);
+  else e = run_gemm<64, 16>(J, pk, counter, sms, st);
+  if (e != cudaSuccess) return e;
+  if (after_gemm) cudaEventRecord(after_gemm, st);
+  const int64_t n = J.split_stride;
+  const int blocks = (int)std::min<int64_t>((n / 2 + 255) / 256, 148 * 8);
+  k_reduce_splits<<<blocks, 256, 0, st>>>(J.Cred, J.Cpart, n, J.splits, J.split_stride);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y, double* out,
+                           int ld_out, double sign, cudaStream_t st) {
+  cudaEventRecord(hp->ev[0], st);
+  cudaError_t e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
+  if (e != cudaSuccess) return e;
+  cudaEventRecord(hp->ev[2], st);
+  if (hp->has_j2) {
+    e = run_job(hp->j2, pk, hp->counters + 1, hp->sms, st);
+    if (e != cudaSuccess) return e;
+    const int E = D.q + D.d + D.f, F = D.d + D.f;
+    k_arrow<<<D.K * hp->ar_splits, 256, hp->ar_smem, st>>>(D.N, D.K, D.q, D.d, D.f, hp->ar_splits, hp->ar_nchunks,
+                                                           pk.Pr, pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y,
+                                                           hp->Tpart);
+    count_launch();
+    const int64_t n = (int64_t)D.K * E * F;
+    k_reduce_splits<<<(int)std::min<int64_t>((n / 2 + 256) / 256, 1024), 256, 0, st>>>(hp->T, hp->Tpart, n,
+                                                                                       hp->ar_splits, (n + 1) / 2 * 2);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  cudaEventRecord(hp->ev[3], st);
+  AsmArgs A;
+  A.K = D.K; A.q = D.q; A.d = D.d; A.f = D.f;
+  A.n_beta = D.n_beta; A.off_gamma = D.off_gamma; A.n_p = D.n_p;
+  A.C1 = hp->j1.Cred; A.ld1 = hp->j1.ldc;
+  A.C2 = hp->has_j2 ? hp->j2.Cred : nullptr; A.ld2 = hp->has_j2 ? hp->j2.ldc : 0;
+  A.T = hp->T;
+  A.out = out; A.ld_out = ld_out; A.sign = sign;
+  const int64_t total = (int64_t)D.n_p * D.n_p;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_assemble<<<blocks, 256, 0, st>>>(A);
+  count_launch();
+  cudaEventRecord(hp->ev[4], st);
+  return cudaGetLastError();
+}
+
+void hess_last_times(HessPlan* hp, double out[4]) {
+  for (int i = 0; i < 4; ++i) {
+    float ms = 0.f;
+    if (!hp || cudaEventElapsedTime(&ms, hp->ev[i], hp->ev[i + 1]) != cudaSuccess) ms = 0.f;
+    out[i] = ms;
+  }
+}
+
+}  // namespace mnl

@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances are BASELINE.json north_star's: Hessian relative Frobenius 1e-9, loglik and gradient
+relative 1e-10, converged coefficients 1e-8 with identical iteration counts."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle as O
+from helpers import device_problem, oracle_data, sample_entries
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1404_3177_b200 as M  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def gpu_eval(dp, theta, hess=True):
+    ll, g, H = M.mnl_eval(dp, dev(theta), grad=True, hess=hess)
+    torch.cuda.synchronize()
+    return ll.item(), g.cpu().numpy(), (H.cpu().numpy() if hess else None)
+
+
+def check_lg(l, g, l_o, g_o):
+    assert abs(l - l_o) <= 1e-10 * abs(l_o), (l, l_o)
+    assert np.linalg.norm(g - g_o) <= 1e-10 * np.linalg.norm(g_o), np.linalg.norm(g - g_o) / np.linalg.norm(g_o)
+
+
+def thetas(prob):
+    return {"zero": np.zeros(prob.spec.n_params), "true": prob.theta_true, "perturbed": datagen.perturbed_theta(prob)}
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_eval_parity_full_hessian(cfg):
+    prob = datagen.make(cfg)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    for name, th in thetas(prob).items():
+        l_o, g_o, H_o = O.mnl_eval(D, th)
+        l, g, H = gpu_eval(dp, th)
+        check_lg(l, g, l_o, g_o)
+        rel = np.linalg.norm(H - H_o) / np.linalg.norm(H_o)
+        assert rel <= 1e-9, (cfg, name, rel)
+        assert np.array_equal(H, H.T)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_eval_parity_full_size_sampled(cfg):
+    """Full BASELINE size, bench launch configuration: loglik and gradient in full, the Hessian on
+    sampled entries computed one by one from the definition."""
+    prob = datagen.make(cfg)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    rows, cols = sample_entries(D, n_random=160 if cfg == "c4" else 256)
+    for name, th in thetas(prob).items():
+        if cfg == "c4" and name == "perturbed":
+            continue
+        V = O.utilities(D, th)
+        P = O.probabilities(V)
+        l_o = O.math.fsum(O.loglik_terms(V, D.choice))
+        g_o = O.gradient(D, th, P)
+        h_o = O.hessian_entries(D, th, rows, cols, P)
+        l, g, H = gpu_eval(dp, th)
+        check_lg(l, g, l_o, g_o)
+        fro = np.linalg.norm(H)
+        err = np.abs(H[rows, cols] - h_o)
+        assert err.max() <= 1e-9 * fro / 8, (cfg, name, err.max() / fro)
+        assert np.sqrt(np.mean(err ** 2)) * D.n_p <= 1e-9 * fro
+        assert np.array_equal(H, H.T)
+        # -H positive definite (concavity): check on a leading block cheaply
+        m = min(D.n_p, 600)
+        assert np.linalg.eigvalsh(-H[:m, :m]).min() > 0
+
+
+SHAPES = [  # ragged N (not a multiple of the 32/64-row tiles), K at KPL boundaries, empty blocks
+    (1, 2, 1, 0, 0), (33, 2, 3, 1, 1), (100, 3, 0, 0, 0), (257, 5, 0, 2, 0), (130, 4, 2, 0, 2),
+    (999, 7, 5, 3, 2), (300, 32, 4, 0, 0), (300, 33, 3, 1, 1), (200, 64, 2, 2, 0), (150, 65, 1, 0, 1),
+    (70, 129, 2, 0, 0), (40, 256, 1, 1, 1), (2049, 6, 17, 2, 3), (5000, 9, 63, 0, 0), (700, 3, 64, 5, 16),
+    (300, 4, 10, 64, 0),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[str(s) for s in SHAPES])
+def test_eval_parity_shapes(shape):
+    N, K, p, f, d = shape
+    prob = datagen.custom(N, K, p, f, d, seed=31, coef_sd=0.4, require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    for th in (prob.theta_true, datagen.perturbed_theta(prob, 0.3)):
+        l_o, g_o, H_o = O.mnl_eval(D, th)
+        l, g, H = gpu_eval(dp, th)
+        check_lg(l, g, l_o, g_o)
+        assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+        assert np.array_equal(H, H.T)
+
+
+def test_eval_without_grad_and_hess_and_determinism():
+    prob = datagen.make("c2")
+    dp = device_problem(prob)
+    th = dev(prob.theta_true)
+    ll1, g1, H1 = M.mnl_eval(dp, th, grad=True, hess=True)
+    ll2, g2, H2 = M.mnl_eval(dp, th, grad=True, hess=True)
+    ll3, _, _ = M.mnl_eval(dp, th, grad=False, hess=False)
+    torch.cuda.synchronize()
+    assert torch.equal(ll1, ll2) and torch.equal(g1, g2) and torch.equal(H1, H2)
+    assert torch.equal(ll1, ll3)
+    assert M.last_launch_count() >= 2
+
+
+def test_bad_choice_is_an_argument_error():
+    prob = datagen.custom(100, 4, 2, 0, 0, seed=3)
+    prob.choice[17] = 4
+    dp = device_problem(prob)
+    with pytest.raises(M.MnlError) as e:
+        M.mnl_eval(dp, dev(prob.theta_true))
+    assert e.value.code == M.MNL_ERR_ARG
+
+
+def test_eval_host_buffers_match_device():
+    prob = datagen.make("c1")
+    dp = device_problem(prob)
+    l, g, H = gpu_eval(dp, prob.theta_true)
+    l2, g2, H2 = M.mnl_eval_host(prob.X, prob.Y, prob.Z, prob.choice, prob.theta_true, K=prob.spec.K, hess=True)
+    assert l2 == l and np.array_equal(g2, g) and np.array_equal(H2, H)
+
+
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 130, 500, 1031])
+def test_cholesky_and_solve(n):
+    rng = np.random.default_rng(n)
+    B = rng.standard_normal((n, n + 3))
+    A = B @ B.T / n + np.eye(n) * 0.1
+    b = rng.standard_normal(n)
+    L_ref = np.linalg.cholesky(A)
+    x_ref = np.linalg.solve(A, b)
+    Ad = dev(A)
+    assert M.mnl_cholesky(Ad) == M.MNL_OK
+    L = np.tril(Ad.cpu().numpy())
+    assert np.max(np.abs(L - L_ref)) <= 1e-11 * np.max(np.abs(L_ref))
+    x = M.mnl_cholesky_solve(Ad, dev(b)).cpu().numpy()
+    assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
+
+
+def test_cholesky_not_spd():
+    A = np.eye(70)
+    A[40, 40] = -1.0
+    assert M.mnl_cholesky(dev(A)) == M.MNL_ERR_NOT_SPD
+
+
+def fit_parity(prob, fit_o, tol=1e-6, coef0=None):
+    dp = device_problem(prob)
+    r = M.mnl_newton_fit(dp, coef0=None if coef0 is None else dev(coef0), tol=tol, max_iter=50)
+    coef = r.coef.cpu().numpy()
+    assert r.status == M.MNL_OK
+    assert r.iters == fit_o["iters"], (r.iters, fit_o["iters"])
+    assert r.stats["halvings_per_iter"] == fit_o["halvings"], (r.stats["halvings_per_iter"], fit_o["halvings"])
+    assert np.linalg.norm(coef - fit_o["coef"]) <= 1e-8 * np.linalg.norm(fit_o["coef"])
+    assert abs(r.loglik - fit_o["loglik"]) <= 1e-10 * abs(fit_o["loglik"])
+    return r
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_fit_parity_small(cfg):
+    prob = datagen.make(cfg)
+    f = O.newton_fit(oracle_data(prob), tol=1e-6)
+    assert f.status == O.MNL_OK
+    fit_parity(prob, dict(iters=f.iters, halvings=[h["halvings"] for h in f.history], coef=f.coef, loglik=f.loglik))
+
+
+def test_fit_parity_random_start_with_halvings():
+    prob = datagen.custom(400, 4, 2, 1, 1, seed=40, coef_sd=0.5)
+    start = np.full(prob.spec.n_params, 3.0)
+    f = O.newton_fit(oracle_data(prob), coef0=start, tol=1e-8)
+    assert sum(h["halvings"] for h in f.history) >= 1
+    fit_parity(prob, dict(iters=f.iters, halvings=[h["halvings"] for h in f.history], coef=f.coef,
+                          loglik=f.loglik), tol=1e-8, coef0=start)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_fit_parity_golden(cfg):
+    path = os.path.join(GOLDEN, f"{cfg}_fit.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (tools/make_golden_fits.py)")
+    g = json.load(open(path))
+    prob = datagen.make(cfg)
+    fit_parity(prob, dict(iters=g["iters"], halvings=g["halvings"], coef=np.array(g["coef"]), loglik=g["loglik"]),
+               tol=g["tol"])
+
+
+def test_fit_maxiter_and_zero_iter():
+    prob = datagen.make("c1")
+    dp = device_problem(prob)
+    r = M.mnl_newton_fit(dp, tol=1e-14, max_iter=2)
+    assert r.status == M.MNL_MAXITER and r.iters == 2
+    r0 = M.mnl_newton_fit(dp, tol=1e-14, max_iter=0)
+    assert r0.status == M.MNL_MAXITER and r0.iters == 0 and float(r0.coef.abs().max()) == 0.0

@@ -1,0 +1,90 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/mnl.h declares, and
+rejects bad arguments before touching a device (no compute calls here: there is no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1404_3177_b200 as M
+from paper_1404_3177_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mnl.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return M.load()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mnl_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("mnl_eval", "mnl_newton_fit", "mnl_num_params", "mnl_status_string"):
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+        assert isinstance(getattr(lib, name), ctypes._CFuncPtr)
+    assert set(M.EXPORTED) <= set(declared_functions())
+
+
+def test_num_params_and_status_strings(lib):
+    assert M.num_params(4, 1, 1, 1) == 11          # Fish model
+    assert M.num_params(100, 49) == 4950           # Table 1 problem X
+    assert M.num_params(100, 50) == 5049           # c4
+    assert M.num_params(50, 30, 10, 5) == 1779     # c5
+    assert M.num_params(1, 3) == -1
+    assert M.status_string(0) == "MNL_OK"
+    assert M.status_string(3) == "MNL_ERR_NOT_SPD"
+    assert M.status_string(6) == "MNL_MAXITER"
+    assert M.status_string(99) == "MNL_UNKNOWN"
+
+
+def test_argument_errors_are_reported_without_a_device(lib):
+    fake = ctypes.c_void_p(1 << 20)  # never dereferenced: validation fails first
+    # K < 2
+    assert lib.mnl_eval(10, 1, 2, 0, 0, fake, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    # negative sizes / too large
+    assert lib.mnl_eval(10, 4, -1, 0, 0, fake, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    assert lib.mnl_eval(10, 300, 2, 0, 0, fake, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    # N < 1
+    assert lib.mnl_eval(0, 4, 2, 0, 0, fake, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    # X required iff p > 0; Y iff f > 0; Z iff d > 0
+    assert lib.mnl_eval(10, 4, 2, 0, 0, None, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    assert lib.mnl_eval(10, 4, 0, 1, 0, None, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    assert lib.mnl_eval(10, 4, 0, 0, 1, None, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    # misaligned pointer
+    bad = ctypes.c_void_p((1 << 20) + 8)
+    assert lib.mnl_eval(10, 4, 2, 0, 0, bad, None, None, fake, fake, fake, None, None, None) == M.MNL_ERR_ARG
+    it, ll = ctypes.c_int32(), ctypes.c_double()
+    # tol <= 0, max_iter < 0
+    assert lib.mnl_newton_fit(10, 4, 2, 0, 0, fake, None, None, fake, None, 0.0, 5, fake, ctypes.byref(it),
+                              ctypes.byref(ll), None) == M.MNL_ERR_ARG
+    assert lib.mnl_newton_fit(10, 4, 2, 0, 0, fake, None, None, fake, None, 1e-6, -1, fake, ctypes.byref(it),
+                              ctypes.byref(ll), None) == M.MNL_ERR_ARG
+    assert lib.mnl_eval_host(10, 1, 2, 0, 0, fake, None, None, fake, fake, fake, None, None) == M.MNL_ERR_ARG
+    assert lib.mnl_cholesky(0, fake, None) == M.MNL_ERR_ARG
+
+
+def test_library_is_sm100a_only():
+    so = open(M.LIB_PATH, "rb").read()
+    assert b"sm_100a" in so or b"compute_100a" in so
+
+
+def test_product_path_does_not_import_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1404_3177_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, fn
