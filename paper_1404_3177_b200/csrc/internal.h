@@ -19,8 +19,9 @@ struct Dims {
 };
 
 // Packed per-individual rows in library scratch.
-// Row strides are even (16-byte rows for bulk copies) and = 8 (mod 16) doubles, which makes
-// the 4-row x 8-column fragment gathers of the Hessian generator bank-conflict-free.
+// Row strides are even (16-byte rows for bulk copies) and = 4 (mod 16) doubles, which makes
+// the 4-row x 8-column fragment gathers of the Hessian generator bank-conflict-free (64-bit
+// shared loads are served per half-warp: 4 rows x 4 columns must hit 16 distinct bank pairs).
 struct Packed {
   int64_t Npad;   // N rounded up to a multiple of kRowPad; rows >= N are zero
   int ldX;        // Xp [Npad][ldX]: 1, x_i1..x_ip, 0...
@@ -33,9 +34,9 @@ struct Packed {
 
 constexpr int kRowPad = 64;   // Npad multiple (>= the largest chunk KC)
 
-inline int pad8mod16(int n) {  // smallest m >= n with m % 16 == 8
-  int m = (n + 7) / 8 * 8;
-  if (m % 16 != 8) m += 8;
+inline int pad4mod16(int n) {  // smallest m >= n with m % 16 == 4
+  int m = n;
+  while (m % 16 != 4) ++m;
   return m;
 }
 

@@ -26,6 +26,7 @@
 // Split-N partial tiles are reduced in a fixed order (deterministic), then k_assemble gathers
 // H (exactly symmetric) into the caller's row-major n_p x n_p buffer.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -94,9 +95,15 @@ __device__ __forceinline__ void tma_stage(const GemmParams& P, double* dst, int6
 }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
+  // volatile: keeps the program order (fragment loads for ks+1 ahead of ks's DMMAs)
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double2 lds128(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
 }
 
 struct Gen {  // one generated column, pre-offset to this lane's row (i % 4)
@@ -119,7 +126,7 @@ __device__ __forceinline__ double gen_val(const double* R, const Gen& g, int ks)
 
 template <int BN, int KC>
 __global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
-  constexpr int WARPS_M = (BN == 128) ? 2 : 4;
+  constexpr int WARPS_M = (BN == 128) ? 2 : 4;  // 128: 2x4 warps of 64x32; 96: 4x2 of 32x48; 64: 4x2 of 32x32
   constexpr int WARPS_N = 8 / WARPS_M;
   constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   constexpr int MT = WTM / 8, NTL = WTN / 8;
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
     // per-thread generator columns (constant over the item)
     const Gen gA0 = make_gen(P.descA[tm * BM + (2 * w) * 8 + cl], r4);
     const Gen gA1 = make_gen(P.descA[tm * BM + (2 * w + 1) * 8 + cl], r4);
-    const int pbB = w % PBB;
+    const int pbB = w < PBB ? w : 0;  // warp w < PBB generates B pair-block w (all ks)
     const Gen gB0 = make_gen(P.descB[tn * BN + (2 * pbB) * 8 + cl], r4);
     const Gen gB1 = make_gen(P.descB[tn * BN + (2 * pbB + 1) * 8 + cl], r4);
 
@@ -194,36 +201,41 @@ __global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
         v.y = gen_val(R, gA1, ks);
         reinterpret_cast<double2*>(ga)[(ks * PBA + w) * 32 + lane] = v;
       }
+      if (w < PBB) {
 #pragma unroll
-      for (int j = 0; j < (PBB * KS) / 8; ++j) {
-        const int ks = (w + 8 * j) / PBB;
-        double2 v;
-        v.x = gen_val(R, gB0, ks);
-        v.y = gen_val(R, gB1, ks);
-        reinterpret_cast<double2*>(gb)[(ks * PBB + pbB) * 32 + lane] = v;
+        for (int ks = 0; ks < KS; ++ks) {
+          double2 v;
+          v.x = gen_val(R, gB0, ks);
+          v.y = gen_val(R, gB1, ks);
+          reinterpret_cast<double2*>(gb)[(ks * PBB + pbB) * 32 + lane] = v;
+        }
       }
       __syncthreads();
       if (tid == 0 && c + 2 < c_end) tma_stage(P, RAW + b * P.stage_doubles, c + 2, KC, &mbar[b]);
-      // ---- DMMA on this chunk ----
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        double af[MT], bf[NTL];
+      // ---- DMMA on this chunk (fragments for ks+1 loaded while ks's DMMAs issue) ----
+      double af[2][MT], bf[2][NTL];
+      auto load_frags = [&](int buf, int ks) {
 #pragma unroll
         for (int mp = 0; mp < MT / 2; ++mp) {
-          const double2 v = reinterpret_cast<const double2*>(ga)[(ks * PBA + wm * (MT / 2) + mp) * 32 + lane];
-          af[2 * mp] = v.x;
-          af[2 * mp + 1] = v.y;
+          const double2 v = lds128(ga + 2 * ((ks * PBA + wm * (MT / 2) + mp) * 32 + lane));
+          af[buf][2 * mp] = v.x;
+          af[buf][2 * mp + 1] = v.y;
         }
 #pragma unroll
         for (int np = 0; np < NTL / 2; ++np) {
-          const double2 v = reinterpret_cast<const double2*>(gb)[(ks * PBB + wn * (NTL / 2) + np) * 32 + lane];
-          bf[2 * np] = v.x;
-          bf[2 * np + 1] = v.y;
+          const double2 v = lds128(gb + 2 * ((ks * PBB + wn * (NTL / 2) + np) * 32 + lane));
+          bf[buf][2 * np] = v.x;
+          bf[buf][2 * np + 1] = v.y;
         }
+      };
+      load_frags(0, 0);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        if (ks + 1 < KS) load_frags((ks + 1) & 1, ks + 1);
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
-          for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[ks & 1][i], bf[ks & 1][j]);
       }
     }
     // ---- epilogue: this split's partial tile ----
@@ -381,12 +393,6 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
   }
 }
 
-template <int BN, int KC>
-size_t gemm_smem_bytes(int stage_doubles) {
-  constexpr int KS = KC / 4;
-  return (size_t)(2 * KS * 8 * 64 + 2 * KS * (BN / 16) * 64 + 2 * stage_doubles) * sizeof(double);
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
@@ -437,6 +443,21 @@ static int choose_splits(int tiles, int64_t nchunks, int sms, int min_chunks) {
   return best;
 }
 
+// Output-tile width: the widest of {128, 96, 64} whose padded width is within 5% of the smallest
+// padded width (wider tiles reuse each generated operand more; measured equal time on c4 for
+// 128 vs 96).
+static int choose_bn(int MB) {
+  if (const char* e = getenv("MNL_FORCE_BN")) return atoi(e);  // experiments only
+  int64_t min_pad = -1;
+  for (int bn : {128, 96, 64}) {
+    const int64_t pad = (int64_t)(MB + bn - 1) / bn * bn;
+    if (min_pad < 0 || pad < min_pad) min_pad = pad;
+  }
+  for (int bn : {128, 96, 64})
+    if ((double)((MB + bn - 1) / bn * bn) <= 1.05 * (double)min_pad) return bn;
+  return 64;
+}
+
 static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vector<ColDesc>& B, int BN,
                       int KC, const Packed& pk, const int* segs, int nseg, int sms, size_t* bytes) {
   J.BN = BN;
@@ -470,10 +491,7 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   if (cudaMalloc(&J.Cpart, cbytes * J.splits) != cudaSuccess) return false;
   if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
   *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
-  if (BN == 128 && KC == 32) J.smem = gemm_smem_bytes<128, 32>(J.stage_doubles);
-  else if (BN == 128 && KC == 16) J.smem = gemm_smem_bytes<128, 16>(J.stage_doubles);
-  else if (BN == 64 && KC == 32) J.smem = gemm_smem_bytes<64, 32>(J.stage_doubles);
-  else J.smem = gemm_smem_bytes<64, 16>(J.stage_doubles);
+  J.smem = (size_t)(2 * (KC / 4) * 8 * 64 + 2 * (KC / 4) * (BN / 16) * 64 + 2 * J.stage_doubles) * sizeof(double);
   return J.smem <= 220 * 1024;
 }
 
@@ -505,7 +523,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       for (int a = 0; a < q; ++a)
         for (int b = a; b < q; ++b) B.push_back(ColDesc{offX + a, pk.ldX, offX + b, pk.ldX, 0.0, 1.0});
       // padding columns point at Xp[.][0] (finite) with c0 = s = 0
-      if (setup_job(hp->j1, A, B, 128, KC, pk, segs, 2, sms, &bytes)) break;
+      if (setup_job(hp->j1, A, B, choose_bn((int)B.size()), KC, pk, segs, 2, sms, &bytes)) break;
       free_job(hp->j1);
       if (KC == 16) ok = false;
     }
@@ -525,9 +543,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       for (int e = 0; e < f; ++e) AG.push_back(ColDesc{offP + K + e, pk.ldP, offX + 0, pk.ldX, 0.0, 1.0});
       A.insert(A.end(), AG.begin(), AG.end());
       B = AG;
-      // choose BN: 64 unless the B side is large
-      const int BN = (int)B.size() > 96 * 2 ? 128 : 64;
-      if (setup_job(hp->j2, A, B, BN, KC, pk, segs, nseg, sms, &bytes)) break;
+      if (setup_job(hp->j2, A, B, choose_bn((int)B.size()), KC, pk, segs, nseg, sms, &bytes)) break;
       free_job(hp->j2);
       if (KC == 16) ok = false;
     }
@@ -591,8 +607,8 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.stage_doubles = off;
   P.stage_bytes = (unsigned)(off * 8);
   P.counter = counter;
-  static bool attr[4] = {false, false, false, false};
-  const int ai = (BN == 128 ? 0 : 2) + (KC == 32 ? 0 : 1);
+  static bool attr[6] = {false, false, false, false, false, false};
+  const int ai = (BN == 128 ? 0 : (BN == 96 ? 2 : 4)) + (KC == 32 ? 0 : 1);
   if (!attr[ai]) {
     cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
@@ -610,10 +626,9 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
 static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
                            cudaEvent_t after_gemm = nullptr) {
   cudaError_t e;
-  if (J.BN == 128 && J.KC == 32) e = run_gemm<128, 32>(J, pk, counter, sms, st);
-  else if (J.BN == 128) e = run_gemm<128, 16>(J, pk, counter, sms, st);
-  else if (J.KC == 32) e = run_gemm<64, 32>(J, pk, counter, sms, st);
-  else e = run_gemm<64, 16>(J, pk, counter, sms, st);
+  if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32>(J, pk, counter, sms, st) : run_gemm<128, 16>(J, pk, counter, sms, st);
+  else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32>(J, pk, counter, sms, st) : run_gemm<96, 16>(J, pk, counter, sms, st);
+  else e = J.KC == 32 ? run_gemm<64, 32>(J, pk, counter, sms, st) : run_gemm<64, 16>(J, pk, counter, sms, st);
   if (e != cudaSuccess) return e;
   if (after_gemm) cudaEventRecord(after_gemm, st);
   const int64_t n = J.split_stride;

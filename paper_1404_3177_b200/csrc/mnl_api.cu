@@ -101,9 +101,9 @@ int init_device(Workspace& W) {
 
 bool ensure_packed(Workspace& W, const Dims& D, Packed* pk) {
   pk->Npad = (D.N + kRowPad - 1) / kRowPad * kRowPad;
-  pk->ldX = pad8mod16(D.q);
-  pk->ldZ = pad8mod16(std::max(D.K * D.d, 1));
-  pk->ldP = pad8mod16(D.K + D.f);
+  pk->ldX = pad4mod16(D.q);
+  pk->ldZ = pad4mod16(std::max(D.K * D.d, 1));
+  pk->ldP = pad4mod16(D.K + D.f);
   const size_t nX = pk->Npad * pk->ldX, nZ = D.d ? pk->Npad * pk->ldZ : 2, nP = pk->Npad * pk->ldP;
   const bool newP = !(nP <= W.cPr && W.Pr);
   if (!grow(&W.Xp, &W.cXp, nX) || !grow(&W.Zp, &W.cZp, nZ) || !grow(&W.Pr, &W.cPr, nP)) return false;
