@@ -82,7 +82,11 @@ void hess_last_times(HessPlan* hp, double out[4]);
 // ---- k_chol.cu -------------------------------------------------------------------------
 // In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.
 cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t st);
-// x = (L L^T)^{-1} b ; x may alias b; work: n doubles.
+// Factor A in place and solve (L L^T) x = b in the same pass (forward solve fused into the
+// panels, backward solve as one wavefront kernel). x may alias b.
+cudaError_t launch_cholesky_solve_fused(int n, double* A, int lda, int* info, const double* b, double* x,
+                                        cudaStream_t st);
+// x = (L L^T)^{-1} b ; x may alias b.
 cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, double* x,
                               cudaStream_t st);
 

@@ -273,62 +273,86 @@ __global__ void k_reduce_splits(double* __restrict__ dst, const double* __restri
   }
 }
 
-// J3: T_k = sum_i P_ik e_ik f_ik^T for one alternative k over a split of the individuals.
-// e = [x~_i (q; absent for k = 0), z_ik (d), y_ik (f)], f = [z_ik (d), y_ik (f)].
-constexpr int AR_TI = 32;
-__global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, int f, int splits,
-                                               int64_t nchunks, const double* __restrict__ Pr, int ldP,
+// J3: T_k = sum_i P_ik e_ik f_ik^T per alternative k, on DMMA.
+// e = [x~_i (q; absent for k = 0), z_ik (d), y_ik (f)] (E rows), f = [z_ik (d), y_ik (f)] (F cols).
+// A CTA's 8 warps take 8 consecutive alternatives over the same individuals (the x~ rows are shared
+// through L1); a warp owns a 64 x 32 panel of T_k (MT x NT 8x8 DMMA blocks) and loads its fragment
+// elements straight from the packed rows (A = P_ik e_ik, B = f_ik, inner dimension = individuals).
+// Item = (alternative group, e-panel, f-panel, split); split partials are reduced in fixed order.
+template <int MT, int NT>
+__global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, int f, int splits, int64_t Npad,
+                                               int n_ep, int n_fp, const double* __restrict__ Pr, int ldP,
                                                const double* __restrict__ Xp, int ldX,
                                                const double* __restrict__ Zp, int ldZ,
-                                               const double* __restrict__ Y, double* Tpart) {
-  extern __shared__ __align__(16) double sm[];
+                                               const double* __restrict__ Y, double* Tpart, int64_t tstride) {
   const int E = q + d + f, F = d + f;
-  double* Sv = sm;               // [AR_TI][E]  P_ik e_ik
-  double* Sh = Sv + AR_TI * E;   // [AR_TI][F]  f_ik
-  const int k = blockIdx.x % K, split = blockIdx.x / K;
-  const int64_t c_begin = split * nchunks / splits, c_end = (split + 1) * nchunks / splits;
-  const int tid = threadIdx.x;
-  const int n_ent = E * F;
-  const int64_t tstride = ((int64_t)K * n_ent + 1) / 2 * 2;
-  double* out = Tpart + split * tstride + (int64_t)k * n_ent;
-  for (int base = 0; base < n_ent; base += 256 * 8) {
-    double acc[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n_kg = (K + 7) / 8;
+  int item = blockIdx.x;
+  const int kg = item % n_kg; item /= n_kg;
+  const int ep = item % n_ep; item /= n_ep;
+  const int fp = item % n_fp; item /= n_fp;
+  const int split = item;
+  const int k = kg * 8 + w;
+  if (k >= K) return;
+  const int64_t nq = Npad / 4;
+  const int64_t q_begin = split * nq / splits, q_end = (split + 1) * nq / splits;
+  const int r4 = lane & 3, c8 = lane >> 2;
+  int ekind[MT], ecol[MT], fkind[NT], fcol[NT];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    for (int64_t c = c_begin; c < c_end; ++c) {
-      const int64_t i0 = c * AR_TI;
-      __syncthreads();
-      for (int e = tid; e < AR_TI * (E + F); e += 256) {
-        const int i = e / (E + F), r = e - i * (E + F);
-        const int64_t row = i0 + i;
-        double v = 0.0;
-        if (row < N) {
-          int rr = r < E ? r : r - E + q;  // Sh entries map to e-index q + (0..F)
-          if (rr < q) v = (k == 0) ? 0.0 : Xp[row * ldX + rr];
-          else if (rr < q + d) v = Zp[row * ldZ + k * d + (rr - q)];
-          else v = Y[(row * K + k) * f + (rr - q - d)];
-          if (r < E) v *= Pr[row * ldP + k];
-        }
-        if (r < E) Sv[i * E + r] = v;
-        else Sh[i * F + (r - E)] = v;
+  for (int mb = 0; mb < MT; ++mb) {
+    const int e = ep * MT * 8 + mb * 8 + c8;
+    if (e < q) { ekind[mb] = (k == 0) ? 3 : 0; ecol[mb] = e; }
+    else if (e < q + d) { ekind[mb] = 1; ecol[mb] = k * d + (e - q); }
+    else if (e < E) { ekind[mb] = 2; ecol[mb] = k * f + (e - q - d); }
+    else { ekind[mb] = 3; ecol[mb] = 0; }
+  }
+#pragma unroll
+  for (int nb = 0; nb < NT; ++nb) {
+    const int fi = fp * NT * 8 + nb * 8 + c8;
+    if (fi < d) { fkind[nb] = 1; fcol[nb] = k * d + fi; }
+    else if (fi < F) { fkind[nb] = 2; fcol[nb] = k * f + (fi - d); }
+    else { fkind[nb] = 3; fcol[nb] = 0; }
+  }
+  auto ld = [&](int kind, int col, int64_t i) -> double {
+    if (kind == 0) return __ldg(Xp + i * ldX + col);
+    if (kind == 1) return __ldg(Zp + i * ldZ + col);
+    if (kind == 2) return i < N ? __ldg(Y + i * (int64_t)K * f + col) : 0.0;
+    return 0.0;
+  };
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 2
+  for (int64_t qq = q_begin; qq < q_end; ++qq) {
+    const int64_t i = qq * 4 + r4;
+    const double pk = __ldg(Pr + i * ldP + k);
+    double av[MT], bv[NT];
+#pragma unroll
+    for (int mb = 0; mb < MT; ++mb) av[mb] = pk * ld(ekind[mb], ecol[mb], i);
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb) bv[nb] = ld(fkind[nb], fcol[nb], i);
+#pragma unroll
+    for (int mb = 0; mb < MT; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb)
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
+            : "d"(av[mb]), "d"(bv[nb]));
+  }
+  double* out = Tpart + split * tstride + (int64_t)k * E * F;
+#pragma unroll
+  for (int mb = 0; mb < MT; ++mb) {
+    const int e = ep * MT * 8 + mb * 8 + c8;
+#pragma unroll
+    for (int nb = 0; nb < NT; ++nb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int fi = fp * NT * 8 + nb * 8 + 2 * r4 + h;
+        if (e < E && fi < F) out[e * F + fi] = acc[mb][nb][h];
       }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int ent = base + tid + 256 * j;
-        if (ent < n_ent) {
-          const int r = ent / F, cc = ent - r * F;
-          double a = acc[j];
-          for (int i = 0; i < AR_TI; ++i) a = fma(Sv[i * E + r], Sh[i * F + cc], a);
-          acc[j] = a;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int ent = base + tid + 256 * j;
-      if (ent < n_ent) out[ent] = acc[j];
-    }
   }
 }
 
@@ -418,11 +442,9 @@ struct GemmJob {
 struct HessPlan {
   bool has_j2;
   GemmJob j1, j2;
-  int ar_splits;
-  int64_t ar_nchunks;
+  int ar_splits, ar_mt, ar_nt, ar_ep, ar_fp;
   double* Tpart = nullptr;
   double* T = nullptr;
-  size_t ar_smem;
   unsigned* counters = nullptr;  // [2]
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t bytes = 0;
@@ -548,15 +570,18 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       if (KC == 16) ok = false;
     }
     const int E = q + d + f, F = d + f;
-    hp->ar_nchunks = pk.Npad / AR_TI;
+    hp->ar_mt = (E + 7) / 8 >= 8 ? 8 : ((E + 7) / 8 > 4 ? 8 : ((E + 7) / 8 > 2 ? 4 : 2));
+    hp->ar_nt = (F + 7) / 8 > 2 ? 4 : 2;
+    hp->ar_ep = (E + hp->ar_mt * 8 - 1) / (hp->ar_mt * 8);
+    hp->ar_fp = (F + hp->ar_nt * 8 - 1) / (hp->ar_nt * 8);
+    const int base_items = (K + 7) / 8 * hp->ar_ep * hp->ar_fp;
     int S = 1;
-    while ((int64_t)K * S < 2 * sms && hp->ar_nchunks / (S * 2) >= 4) S *= 2;
+    while ((int64_t)base_items * S < 2 * sms && pk.Npad / 4 / (S * 2) >= 64) S *= 2;
     hp->ar_splits = S;
     const size_t tb = ((size_t)K * E * F + 1) / 2 * 2 * sizeof(double);
     if (cudaMalloc(&hp->Tpart, tb * S) != cudaSuccess) ok = false;
     if (cudaMalloc(&hp->T, tb) != cudaSuccess) ok = false;
     bytes += tb * (S + 1);
-    hp->ar_smem = (size_t)AR_TI * (E + F) * sizeof(double);
   }
   for (auto& e : hp->ev) cudaEventCreate(&e);
   if (cudaMalloc(&hp->counters, 2 * sizeof(unsigned)) != cudaSuccess) ok = false;
@@ -648,10 +673,21 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
     e = run_job(hp->j2, pk, hp->counters + 1, hp->sms, st);
     if (e != cudaSuccess) return e;
     const int E = D.q + D.d + D.f, F = D.d + D.f;
-    k_arrow<<<D.K * hp->ar_splits, 256, hp->ar_smem, st>>>(D.N, D.K, D.q, D.d, D.f, hp->ar_splits, hp->ar_nchunks,
-                                                           pk.Pr, pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y,
-                                                           hp->Tpart);
-    count_launch();
+    {
+      const int items = (D.K + 7) / 8 * hp->ar_ep * hp->ar_fp * hp->ar_splits;
+      const int64_t tstride = ((int64_t)D.K * E * F + 1) / 2 * 2;
+#define MNL_ARROW(MT_, NT_)                                                                                  \
+  k_arrow<MT_, NT_><<<items, 256, 0, st>>>(D.N, D.K, D.q, D.d, D.f, hp->ar_splits, pk.Npad, hp->ar_ep, hp->ar_fp, \
+                                           pk.Pr, pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y, hp->Tpart, tstride)
+      if (hp->ar_mt == 8 && hp->ar_nt == 4) MNL_ARROW(8, 4);
+      else if (hp->ar_mt == 8) MNL_ARROW(8, 2);
+      else if (hp->ar_mt == 4 && hp->ar_nt == 4) MNL_ARROW(4, 4);
+      else if (hp->ar_mt == 4) MNL_ARROW(4, 2);
+      else if (hp->ar_nt == 4) MNL_ARROW(2, 4);
+      else MNL_ARROW(2, 2);
+#undef MNL_ARROW
+      count_launch();
+    }
     const int64_t n = (int64_t)D.K * E * F;
     k_reduce_splits<<<(int)std::min<int64_t>((n / 2 + 256) / 256, 1024), 256, 0, st>>>(hp->T, hp->Tpart, n,
                                                                                        hp->ar_splits, (n + 1) / 2 * 2);

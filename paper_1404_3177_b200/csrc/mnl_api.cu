@@ -227,8 +227,10 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
     cudaEventRecord(ev[0], st);
     if (launch_hessian(hp, D, pk, Y, W.A, n, -1.0, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }  // A = -H
     cudaEventRecord(ev[1], st);
-    if (launch_cholesky(n, W.A, n, W.info, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
-    if (launch_chol_solve(n, W.A, n, W.grad, W.delta, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
+    if (launch_cholesky_solve_fused(n, W.A, n, W.info, W.grad, W.delta, st) != cudaSuccess) {
+      rc = MNL_ERR_CUDA;
+      break;
+    }
     cudaEventRecord(ev[2], st);
     int info = 0;
     cudaMemcpyAsync(&info, W.info, sizeof(int), cudaMemcpyDeviceToHost, st);
