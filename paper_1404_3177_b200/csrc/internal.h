@@ -46,7 +46,7 @@ void count_launch(int n = 1);
 // ---- k_eval.cu -------------------------------------------------------------------------
 // Per-CTA partials layout: [2 + n_p] doubles: l_sum, l_comp, grad[n_p].
 struct EvalPlan {
-  int grid, block, kpl;
+  int grid, block, kpl, cm;
   size_t smem;
   int n_part;  // 2 + n_p
 };

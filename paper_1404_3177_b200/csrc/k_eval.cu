@@ -10,11 +10,15 @@
 // and, for the Hessian pass, the probability rows Pr[i] = [P_i0..P_i,K-1, ybar_i] with
 // ybar_i = sum_k P_ik y_ik (the O(K) regrouping of the generic blocks).
 //
-// Layout: CTA = 8 warps, persistent over tiles of 32 individuals; a warp owns 4 individuals and
-// its lanes the alternatives k = lane + 32*kk.  The utility GEMM X~ B uses B = [beta_k] staged
-// transposed in shared memory; the beta-gradient X~^T R accumulates in registers per tile and
-// in CTA-owned shared memory across tiles.  CTA partials are reduced in a fixed order by
-// k_eval_finalize, so results are deterministic.
+// Layout: CTA = 8 warps, persistent over tiles of 64 individuals (X tiles prefetched with
+// cp.async, double-buffered).  The two dense contractions run on the FP64 tensor pipe
+// (mma.sync m8n8k4, SASS DMMA.8x8x4):
+//   phase B  U = X~ B   (warp w: individuals 8w..8w+7 x all alternatives; the C fragment gives
+//            each lane 2 alternatives per 8-block of one individual, so the row softmax is a
+//            local reduction plus two shuffles);
+//   phase C  G += X~^T R (the beta gradient; CTA-persistent accumulators in registers).
+// Phase D (only with Y or Z) folds the alpha/gamma gradients and ybar with lanes over
+// alternatives.  CTA partials are reduced in a fixed order by k_eval_finalize (deterministic).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -25,13 +29,13 @@ namespace mnl {
 
 namespace {
 
-constexpr int TI = 32;   // individuals per tile
 constexpr int NW = 8;    // warps per CTA
-constexpr int IPW = 4;   // individuals per warp per tile
+// individuals per tile: 8 warps x 8 rows, halved for K > 128 to bound shared memory
+__host__ __device__ constexpr int tile_rows(int kpl) { return kpl >= 8 ? 32 : 64; }
 
 struct EvalArgs {
   int64_t N;
-  int K, p, f, d, q, n_p, off_alpha, off_gamma;
+  int K, p, f, d, q, n_p, off_alpha, off_gamma, QP, XS;
   const double* X;
   const double* Y;
   const double* Z;
@@ -54,222 +58,344 @@ __device__ __forceinline__ void neu_add(double& s, double& c, double x) {
   s = t;
 }
 
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-template <int KPL>
-__global__ void __launch_bounds__(NW * 32) k_eval_kernel(const EvalArgs A) {
+template <int KPL, int CM_MAX>
+__global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   extern __shared__ __align__(16) double sm[];
-  constexpr int KP = 32 * KPL;
+  constexpr int KP = 32 * KPL, KPS = KP + 4;   // alternatives padded; smem row stride = 4 (mod 16)
+  constexpr int NBN = KP / 8;                   // 8-wide alternative blocks
+  constexpr int TI = tile_rows(KPL);
   const int K = A.K, q = A.q, d = A.d, f = A.f, p = A.p;
+  const int QP = A.QP, XS = A.XS;              // q padded to 4; X tile row stride (= 4 mod 16)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  double* Bs = sm;                        // [q][KP]   Bs[a][k] = beta_k[a], 0 for k = 0 / k >= K
-  double* Gs = Bs + q * KP;               // [q][KP]   beta-gradient accumulators (CTA-owned)
-  double* Xs = Gs + q * KP;               // [TI][q]   x~ rows of the tile
-  double* Rs = Xs + TI * q;               // [TI][KP]  residuals r_ik
-  double* Wa = Rs + TI * KP;              // [NW][KPL][d][32] alpha-gradient, lane-private
-  double* Wg = Wa + NW * KPL * d * 32;    // [NW][f][32]      gamma-gradient, lane-private
-  double* Cf = Wg + NW * f * 32;          // [K*d + f]        alpha_0..alpha_{K-1}, gamma
+  const int r4 = lane & 3, c8 = lane >> 2;
+  double* Bs = sm;                              // [QP][KPS]  Bs[a][k] = beta_k[a]
+  double* Xs = Bs + QP * KPS;                   // [2][TI][XS] x~ tiles (col 0 = 1)
+  double* Rs = Xs + 2 * TI * XS;                // [TI][KPS]  residuals
+  double* Ps = Rs + TI * KPS;                   // [TI][KPS]  probabilities (only with Y)
+  double* Wa = Ps + ((d + f) ? TI * KPS : 0);   // [NW][KPL][d][32] alpha-gradient, lane-private,
+                                                // then [NW][f][32] gamma-gradient (e >= 8)
+  double* Cf = Wa + NW * KPL * d * 32 + NW * f * 32;  // [K*d + f]  alpha, gamma
+  int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
 
-  for (int idx = tid; idx < q * KP; idx += blockDim.x) {
-    int a = idx / KP, k = idx - a * KP;
-    Bs[idx] = (k >= 1 && k < K) ? A.coef[(k - 1) * q + a] : 0.0;
-    Gs[idx] = 0.0;
+  for (int idx = tid; idx < QP * KPS; idx += blockDim.x) {
+    const int a = idx / KPS, k = idx - a * KPS;
+    Bs[idx] = (a < q && k >= 1 && k < K) ? A.coef[(k - 1) * q + a] : 0.0;
   }
+  for (int idx = tid; idx < 2 * TI * XS; idx += blockDim.x) Xs[idx] = ((idx % XS) == 0) ? 1.0 : 0.0;
   for (int idx = tid; idx < NW * KPL * d * 32 + NW * f * 32; idx += blockDim.x) Wa[idx] = 0.0;
   for (int idx = tid; idx < K * d + f; idx += blockDim.x) Cf[idx] = A.coef[A.off_alpha + idx];
   const double* alpha = Cf;
   const double* gamma = Cf + K * d;
 
-  double l_s = 0.0, l_c = 0.0;  // this warp's loglik (Neumaier), identical on all lanes
-  const int64_t ntiles = (A.N + TI - 1) / TI;
+  // phase-C warp grid over (m-blocks of a, n-blocks of k)
+  const int MB = QP / 8 + ((QP & 7) ? 1 : 0);
+  constexpr int WN = NBN < 8 ? NBN : 8;
+  constexpr int WM = 8 / WN;
+  const int cwm = w / WN, cwn = w % WN;
+  constexpr int CN = NBN / WN;                 // n-blocks per warp (CM_MAX m-blocks per warp)
+  double G[CM_MAX][CN][2];
+#pragma unroll
+  for (int i = 0; i < CM_MAX; ++i)
+#pragma unroll
+    for (int j = 0; j < CN; ++j) G[i][j][0] = G[i][j][1] = 0.0;
+  double gam[8];  // gamma-gradient lane partial (f <= 8 in registers, else phase D smem)
+#pragma unroll
+  for (int e = 0; e < 8; ++e) gam[e] = 0.0;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  double l_s = 0.0, l_c = 0.0;  // Neumaier loglik of this lane's rows (lanes with r4 == 0)
+  const int64_t ntiles = (A.N + TI - 1) / TI;
+  auto prefetch = [&](int64_t tile, int buf) {
     const int64_t i0 = tile * TI;
     const int nt = (int)(A.N - i0 < TI ? A.N - i0 : TI);
-    __syncthreads();  // previous tile's phase C done with Xs / Rs; setup above visible
-    for (int e = tid; e < TI * q; e += blockDim.x) {
-      int i = e / q, a = e - i * q;
-      double v = 0.0;
-      if (i < nt) v = (a == 0) ? 1.0 : A.X[(i0 + i) * p + (a - 1)];
-      Xs[e] = v;
+    double* dst = Xs + buf * TI * XS;
+    const double* src = A.X + i0 * p;
+    for (int e = tid; e < nt * p; e += blockDim.x) {
+      const int i = e / p, a = e - i * p;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(dst + i * XS + a + 1))),
+                   "l"(src + e)
+                   : "memory");
     }
-    __syncthreads();
+    for (int i = tid; i < nt; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(chs + buf * TI + i))),
+                   "l"(A.choice + i0 + i)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (tid == 0) {  // warm L2 with the tile's alternative-varying rows (contiguous blocks)
+      if (f) {
+        const char* y0 = reinterpret_cast<const char*>(A.Y + i0 * K * f);
+        unsigned bytes = (unsigned)((int64_t)nt * K * f * 8) & ~15u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(y0), "r"(bytes) : "memory");
+      }
+      if (d) {
+        const char* z0 = reinterpret_cast<const char*>(A.Z + i0 * K * d);
+        unsigned bytes = (unsigned)((int64_t)nt * K * d * 8) & ~15u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(z0), "r"(bytes) : "memory");
+      }
+    }
+  };
 
-    // ---- phase B: a1 + a2 + a3 (+ residuals, alpha/gamma gradients, P rows) ----
-    double u[IPW][KPL];
-#pragma unroll
-    for (int j = 0; j < IPW; ++j)
-#pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) u[j][kk] = 0.0;
-    for (int a = 0; a < q; ++a) {
-      double xv[IPW];
-#pragma unroll
-      for (int j = 0; j < IPW; ++j) xv[j] = Xs[(w * IPW + j) * q + a];
-#pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) {
-        double b = Bs[a * KP + lane + 32 * kk];
-#pragma unroll
-        for (int j = 0; j < IPW; ++j) u[j][kk] = fma(xv[j], b, u[j][kk]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < IPW; ++j) {
-      const int il = w * IPW + j;
-      double* Rrow = Rs + il * KP;
-      if (il >= nt) {  // ragged tail: no contribution
-        if (A.want_grad)
-#pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) Rrow[lane + 32 * kk] = 0.0;
-        continue;
-      }
-      const int64_t i = i0 + il;
+  int buf = 0;
+  if ((int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x, 0);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    const int64_t i0 = tile * TI;
+    const int nt = (int)(A.N - i0 < TI ? A.N - i0 : TI);
+    __syncthreads();  // everyone done with the previous tile (buffers, Rs, Ps)
+    if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x, buf ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const double* X_t = Xs + buf * TI * XS;
+    const int* ch_t = chs + buf * TI;
+
+    // ---------------- phase A2: corr[i][k] = z_ik.alpha_k + y_ik.gamma (lanes over alternatives) -----
+    // the warp's 8 individuals are processed together so their loads are in flight at once
+    if (d + f) {
+      const int ib = 8 * w;
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
-        if (k < K) {
-          double v = u[j][kk];
-          const double* zr = A.Z + (i * K + k) * d;
-          for (int c = 0; c < d; ++c) v = fma(zr[c], alpha[k * d + c], v);
-          const double* yr = A.Y + (i * K + k) * f;
-          for (int e = 0; e < f; ++e) v = fma(yr[e], gamma[e], v);
-          u[j][kk] = v;
-        } else {
-          u[j][kk] = -INFINITY;
+        if (k < K && ib < nt && ib < TI) {
+          double v[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) v[jj] = 0.0;
+          for (int c = 0; c < d; ++c) {
+            const double al = alpha[k * d + c];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (ib + jj < nt) v[jj] = fma(A.Z[((i0 + ib + jj) * K + k) * d + c], al, v[jj]);
+          }
+          for (int e = 0; e < f; ++e) {
+            const double ga = gamma[e];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (ib + jj < nt) v[jj] = fma(A.Y[((i0 + ib + jj) * K + k) * f + e], ga, v[jj]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) Ps[(ib + jj) * KPS + k] = v[jj];
         }
       }
-      double m = u[j][0];
-#pragma unroll
-      for (int kk = 1; kk < KPL; ++kk) m = fmax(m, u[j][kk]);
-      m = warp_max(m);
-      double ex[KPL], s = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) {
-        ex[kk] = (lane + 32 * kk < K) ? exp(u[j][kk] - m) : 0.0;
-        s += ex[kk];
-      }
-      s = warp_sum(s);
-      const double inv_s = 1.0 / s;
-      int y = A.choice[i];
-      if (y < 0 || y >= K) {
-        if (lane == 0) atomicOr(A.err, 1);
-        y = 0;
-      }
-      double uy_l = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < KPL; ++kk)
-        if (kk == (y >> 5)) uy_l = u[j][kk];
-      const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
-      neu_add(l_s, l_c, uy - (m + log(s)));
+      __syncthreads();
+    }
 
-      double P[KPL];
+    // ---------------- phase B: u = X~ B on DMMA, then softmax / loglik / residuals ----------------
+    const int il = (8 * w + c8) % TI;  // this lane's individual (row of the C fragment)
+    const bool in_b = 8 * w < TI;      // warps beyond the tile skip phase B
+    double u[NBN][2];
 #pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) P[kk] = ex[kk] * inv_s;
-      if (A.writeP) {
-        double* pr = A.Pr + i * A.ldP;
+    for (int nb = 0; nb < NBN; ++nb) u[nb][0] = u[nb][1] = 0.0;
+    for (int a0 = 0; a0 < QP; a0 += 4) {
+      const double av = X_t[il * XS + a0 + r4];
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk)
-          if (lane + 32 * kk < K) pr[lane + 32 * kk] = P[kk];
-        for (int e = 0; e < f; ++e) {
-          double v = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) {
-            const int k = lane + 32 * kk;
-            if (k < K) v = fma(P[kk], A.Y[(i * K + k) * f + e], v);
-          }
-          v = warp_sum(v);
-          if (lane == 0) pr[K + e] = v;
-        }
+      for (int nb = 0; nb < NBN; ++nb) {
+        const double bv = Bs[(a0 + r4) * KPS + nb * 8 + c8];
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(u[nb][0]), "+d"(u[nb][1])
+            : "d"(av), "d"(bv));
       }
-      if (A.want_grad) {
+    }
+    const bool valid = in_b && il < nt;
+    const int64_t i = i0 + il;
+    int y = valid ? ch_t[il] : 0;
+    if (valid && (y < 0 || y >= K)) {
+      atomicOr(A.err, 1);
+      y = 0;
+    }
+    // z.alpha + y.gamma corrections, mask padding alternatives
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) {
-          const int k = lane + 32 * kk;
-          const double r = (k < K) ? ((k == y ? 1.0 : 0.0) - P[kk]) : 0.0;
-          Rrow[k] = r;
-          if (k < K) {
-            const double* zr = A.Z + (i * K + k) * d;
-            for (int c = 0; c < d; ++c) Wa[((w * KPL + kk) * d + c) * 32 + lane] += zr[c] * r;
-          }
-        }
-        for (int e = 0; e < f; ++e) {
-          double v = 0.0;
+    for (int nb = 0; nb < NBN; ++nb)
 #pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) {
-            const int k = lane + 32 * kk;
-            if (k < K) v = fma(A.Y[(i * K + k) * f + e], (k == y ? 1.0 : 0.0) - P[kk], v);
+      for (int h = 0; h < 2; ++h) {
+        const int k = nb * 8 + 2 * r4 + h;
+        double v = u[nb][h];
+        if (k < K && valid && (d + f)) v += Ps[il * KPS + k];
+        u[nb][h] = (k < K) ? v : -INFINITY;
+      }
+    double m = -INFINITY;
+#pragma unroll
+    for (int nb = 0; nb < NBN; ++nb) m = fmax(m, fmax(u[nb][0], u[nb][1]));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    double ssum = 0.0, uy = 0.0;
+#pragma unroll
+    for (int nb = 0; nb < NBN; ++nb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = nb * 8 + 2 * r4 + h;
+        if (k == y) uy = u[nb][h];
+        const double e = (k < K) ? exp(u[nb][h] - m) : 0.0;
+        u[nb][h] = e;
+        ssum += e;
+      }
+    ssum += __shfl_xor_sync(0xffffffffu, ssum, 1);
+    ssum += __shfl_xor_sync(0xffffffffu, ssum, 2);
+    uy += __shfl_xor_sync(0xffffffffu, uy, 1);
+    uy += __shfl_xor_sync(0xffffffffu, uy, 2);
+    if (valid && r4 == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));
+    const double inv_s = 1.0 / ssum;
+    double* Rrow = Rs + il * KPS;
+    double* Prow = Ps + il * KPS;
+#pragma unroll
+    for (int nb = 0; nb < NBN; ++nb) {
+      const int k = nb * 8 + 2 * r4;
+      double2 P2, R2;
+      P2.x = valid ? u[nb][0] * inv_s : 0.0;
+      P2.y = valid ? u[nb][1] * inv_s : 0.0;
+      R2.x = valid ? ((k == y ? 1.0 : 0.0) - P2.x) : 0.0;
+      R2.y = valid ? ((k + 1 == y ? 1.0 : 0.0) - P2.y) : 0.0;
+      if (k >= K) { P2.x = 0.0; R2.x = 0.0; }
+      if (k + 1 >= K) { P2.y = 0.0; R2.y = 0.0; }
+      if (in_b) {
+        *reinterpret_cast<double2*>(Rrow + k) = R2;
+        if (f) *reinterpret_cast<double2*>(Prow + k) = P2;
+      }
+      if (A.writeP && valid) {
+        double* pr = A.Pr + i * A.ldP + k;
+        if (k + 1 < K) *reinterpret_cast<double2*>(pr) = P2;
+        else if (k < K) pr[0] = P2.x;
+      }
+    }
+    __syncthreads();  // Rs / Ps complete
+
+    // ---------------- phase C: beta gradient G[a][k] += sum_i x~_ia r_ik on DMMA ----------------
+    if (A.want_grad) {
+      for (int ks = 0; ks < TI / 4; ++ks) {
+        double bf[CN];
+#pragma unroll
+        for (int j = 0; j < CN; ++j) bf[j] = Rs[(4 * ks + r4) * KPS + (cwn + WN * j) * 8 + c8];
+#pragma unroll
+        for (int mi = 0; mi < CM_MAX; ++mi) {
+          const int mb = cwm + WM * mi;
+          if (mb < MB) {
+            const double af = X_t[(4 * ks + r4) * XS + mb * 8 + c8];
+#pragma unroll
+            for (int j = 0; j < CN; ++j)
+              asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                  : "+d"(G[mi][j][0]), "+d"(G[mi][j][1])
+                  : "d"(af), "d"(bf[j]));
           }
-          Wg[(w * f + e) * 32 + lane] += v;
         }
       }
     }
-    if (!A.want_grad) continue;
-    __syncthreads();
 
-    // ---- phase C: beta gradient  G[a][k] += sum_i x~_ia r_ik  (a4, X~^T R) ----
-    for (int ma0 = 0; ma0 * 8 < q; ma0 += 4) {
-      double acc[4][KPL];
+    // ---------------- phase D: alpha / gamma gradients and ybar (lanes over alternatives) ---------
+    // the warp's 8 individuals together (independent loads in flight)
+    if (d || f) {
+      const int ib = 8 * w;
+      if (ib < nt && ib < TI) {
+        if (A.want_grad && d) {
 #pragma unroll
-      for (int m4 = 0; m4 < 4; ++m4)
+          for (int kk = 0; kk < KPL; ++kk) {
+            const int k = lane + 32 * kk;
+            if (k < K) {
+              double r[8];
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) acc[m4][kk] = 0.0;
-      for (int i = 0; i < TI; ++i) {
-        double r[KPL];
+              for (int jj = 0; jj < 8; ++jj) r[jj] = (ib + jj < nt) ? Rs[(ib + jj) * KPS + k] : 0.0;
+              for (int c = 0; c < d; ++c) {
+                double acc = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) r[kk] = Rs[i * KP + lane + 32 * kk];
-#pragma unroll
-        for (int m4 = 0; m4 < 4; ++m4) {
-          const int a = w + 8 * (ma0 + m4);
-          const double x = (a < q) ? Xs[i * q + a] : 0.0;
-#pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) acc[m4][kk] = fma(x, r[kk], acc[m4][kk]);
+                for (int jj = 0; jj < 8; ++jj)
+                  if (ib + jj < nt) acc = fma(A.Z[((i0 + ib + jj) * K + k) * d + c], r[jj], acc);
+                Wa[((w * KPL + kk) * d + c) * 32 + lane] += acc;
+              }
+            }
+          }
         }
-      }
+        for (int e = 0; e < f; ++e) {
+          double yb[8], gg = 0.0;
 #pragma unroll
-      for (int m4 = 0; m4 < 4; ++m4) {
-        const int a = w + 8 * (ma0 + m4);
-        if (a < q)
+          for (int jj = 0; jj < 8; ++jj) yb[jj] = 0.0;
 #pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) Gs[a * KP + lane + 32 * kk] += acc[m4][kk];
+          for (int kk = 0; kk < KPL; ++kk) {
+            const int k = lane + 32 * kk;
+            if (k < K) {
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                if (ib + jj < nt) {
+                  const double yv = A.Y[((i0 + ib + jj) * K + k) * f + e];
+                  yb[jj] = fma(Ps[(ib + jj) * KPS + k], yv, yb[jj]);
+                  gg = fma(yv, Rs[(ib + jj) * KPS + k], gg);
+                }
+              }
+            }
+          }
+          if (A.want_grad) {
+            if (e < 8) {
+#pragma unroll
+              for (int t = 0; t < 8; ++t)
+                if (t == e) gam[t] += gg;
+            } else {
+              Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gg;
+            }
+          }
+          if (A.writeP) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const double v = warp_sum(yb[jj]);
+              if (lane == 0 && ib + jj < nt) A.Pr[(i0 + ib + jj) * A.ldP + K + e] = v;
+            }
+          }
+        }
       }
     }
   }
 
-  // ---- CTA partials (fixed order) ----
+  // ---------------- CTA partials (fixed order) ----------------
   __syncthreads();
   double* out = A.part + (size_t)blockIdx.x * A.n_part;
-  double* wl = Rs;  // reuse: per-warp loglik pairs
-  if (lane == 0) { wl[2 * w] = l_s; wl[2 * w + 1] = l_c; }
+  double* scratch = Rs;  // reuse
+  // loglik: lanes with r4 == 0 hold rows; combine in (warp, lane) order
+  scratch[2 * tid] = l_s;
+  scratch[2 * tid + 1] = l_c;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0, c = 0.0;
-    for (int ww = 0; ww < NW; ++ww) { neu_add(s, c, wl[2 * ww]); neu_add(s, c, wl[2 * ww + 1]); }
+    for (int t = 0; t < NW * 32; t += 4) { neu_add(s, c, scratch[2 * t]); neu_add(s, c, scratch[2 * t + 1]); }
     out[0] = s;
     out[1] = c;
   }
   if (!A.want_grad) return;
-  for (int idx = tid; idx < (K - 1) * q; idx += blockDim.x) {
-    int k = idx / q + 1, a = idx - (k - 1) * q;
-    out[2 + idx] = Gs[a * KP + k];
+  // beta gradient straight from the G fragments: G[a][k] -> out[2 + (k-1) q + a]
+#pragma unroll
+  for (int mi = 0; mi < CM_MAX; ++mi) {
+    const int mb = cwm + WM * mi;
+    if (mb < MB) {
+      const int a = mb * 8 + c8;
+#pragma unroll
+      for (int j = 0; j < CN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = (cwn + WN * j) * 8 + 2 * r4 + h;
+          if (a < q && k >= 1 && k < K) out[2 + (k - 1) * q + a] = G[mi][j][h];
+        }
+    }
   }
+  __syncthreads();
+  // gamma partials: registers (e < 8) -> smem, then fixed-order sums
+  double* gsc = Rs;  // [NW*32][8]
+  for (int e = 0; e < 8; ++e) gsc[tid * 8 + e] = gam[e];
+  __syncthreads();
   for (int idx = tid; idx < K * d; idx += blockDim.x) {
-    int k = idx / d, c = idx - k * d, kk = k >> 5, ln = k & 31;
+    const int k = idx / d, c = idx - k * d, kk = k >> 5, ln = k & 31;
     double v = 0.0;
     for (int ww = 0; ww < NW; ++ww) v += Wa[((ww * KPL + kk) * d + c) * 32 + ln];
     out[2 + A.off_alpha + idx] = v;
   }
   for (int e = tid; e < f; e += blockDim.x) {
     double v = 0.0;
-    for (int ww = 0; ww < NW; ++ww)
-      for (int ln = 0; ln < 32; ++ln) v += Wg[(ww * f + e) * 32 + ln];
+    if (e < 8) {
+      for (int t = 0; t < NW * 32; ++t) v += gsc[t * 8 + e];
+    } else {
+      for (int ww = 0; ww < NW; ++ww)
+        for (int ln = 0; ln < 32; ++ln) v += Wa[NW * KPL * d * 32 + (ww * f + e) * 32 + ln];
+    }
     out[2 + A.off_gamma + e] = v;
   }
 }
@@ -345,26 +471,30 @@ __global__ void k_axpy_pow2(int n, const double* theta, const double* delta, int
   if (r < n) out[r] = theta[r] + ldexp(delta[r], -j);  // a7: theta + delta / 2^j, exact scaling
 }
 
-template <int KPL>
+template <int KPL, int CM>
 cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  k_eval_kernel<KPL><<<plan.grid, plan.block, plan.smem, st>>>(a);
+  k_eval_kernel<KPL, CM><<<plan.grid, plan.block, plan.smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
 }  // namespace
 
+static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
+static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
+
 static size_t eval_smem(const Dims& D, int kpl) {
-  const int KP = 32 * kpl;
-  size_t n = 2 * (size_t)D.q * KP + (size_t)TI * D.q + (size_t)TI * KP + (size_t)NW * kpl * D.d * 32 +
-             (size_t)NW * D.f * 32 + (size_t)D.K * D.d + D.f;
+  const int KP = 32 * kpl, KPS = KP + 4, TI = tile_rows(kpl);
+  const size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
+                   ((D.d + D.f) ? (size_t)TI * KPS : 0) + (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32 +
+                   (size_t)D.K * D.d + D.f + 1 + TI;  // + 2*TI ints
   return n * sizeof(double);
 }
 
@@ -372,16 +502,20 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   int kpl = 1;
   while (32 * kpl < D.K) kpl *= 2;
   if (kpl > 8) return false;
+  // register budget: phase-C accumulators (cm x cn blocks) + the phase-B row (nbn blocks)
+  const int nbn = 4 * kpl, wn = nbn < 8 ? nbn : 8, wm = 8 / wn, cn = nbn / wn;
+  const int mb = (eval_qp(D) + 7) / 8;
+  int cm = 2;
+  while (cm < (mb + wm - 1) / wm) cm *= 2;
+  if (cm > 8 || 2 * cm * cn + 2 * nbn > 96) return false;
+  plan->cm = cm;
   size_t smem = eval_smem(D, kpl);
-  if (smem > 200 * 1024) return false;
+  if (smem > 220 * 1024) return false;
   plan->kpl = kpl;
   plan->smem = smem;
   plan->block = NW * 32;
-  int per_sm = (int)((227 * 1024) / (smem + 1024));
-  if (per_sm < 1) per_sm = 1;
-  if (per_sm > 4) per_sm = 4;
-  const int64_t ntiles = (D.N + TI - 1) / TI;
-  int64_t grid = (int64_t)sms * per_sm;
+  const int64_t ntiles = (D.N + tile_rows(kpl) - 1) / tile_rows(kpl);
+  int64_t grid = sms;
   if (grid > ntiles) grid = ntiles;
   plan->grid = (int)grid;
   plan->n_part = 2 + D.n_p;
@@ -395,17 +529,24 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
   EvalArgs a;
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
+  a.QP = eval_qp(D); a.XS = eval_xs(D);
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
   a.Pr = writeP ? pk->Pr : nullptr;
   a.ldP = writeP ? pk->ldP : 0;
   a.want_grad = want_grad; a.writeP = writeP;
   a.part = part; a.n_part = plan.n_part; a.err = err;
+#define MNL_EVAL_CASE(KPL_)                                   \
+  case KPL_:                                                  \
+    if (plan.cm == 2) return launch_k<KPL_, 2>(plan, a, st);  \
+    if (plan.cm == 4) return launch_k<KPL_, 4>(plan, a, st);  \
+    return launch_k<KPL_, 8>(plan, a, st);
   switch (plan.kpl) {
-    case 1: return launch_k<1>(plan, a, st);
-    case 2: return launch_k<2>(plan, a, st);
-    case 4: return launch_k<4>(plan, a, st);
-    case 8: return launch_k<8>(plan, a, st);
+    MNL_EVAL_CASE(1)
+    MNL_EVAL_CASE(2)
+    MNL_EVAL_CASE(4)
+    MNL_EVAL_CASE(8)
   }
+#undef MNL_EVAL_CASE
   return cudaErrorInvalidValue;
 }
 
