@@ -448,11 +448,16 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
 }
 
 __global__ void k_pack(int64_t N, int64_t Npad, int p, int Kd, const double* __restrict__ X,
-                       const double* __restrict__ Z, double* Xp, int ldX, double* Zp, int ldZ) {
-  const int64_t nx = Npad * ldX, nz = Zp ? Npad * ldZ : 0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx + nz;
+                       const double* __restrict__ Z, double* Xp, int ldX, double* Zp, int ldZ, double* Pr,
+                       int ldP) {
+  // Xp / Zp rows (zero padding rows and columns) and the zero padding rows of Pr (rows >= N are
+  // never written by pass 1; the Hessian kernels rely on them being exactly zero)
+  const int64_t nx = Npad * ldX, nz = Zp ? Npad * ldZ : 0, npr = (Npad - N) * ldP;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx + nz + npr;
        e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < nx) {
+    if (e >= nx + nz) {
+      Pr[N * ldP + (e - nx - nz)] = 0.0;
+    } else if (e < nx) {
       const int64_t i = e / ldX;
       const int a = (int)(e - i * ldX);
       double v = 0.0;
@@ -562,10 +567,10 @@ cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const doub
 
 cudaError_t launch_pack(const Dims& D, const Packed& pk, const double* X, const double* Z,
                         cudaStream_t st) {
-  int64_t total = pk.Npad * pk.ldX + (D.d ? pk.Npad * pk.ldZ : 0);
+  int64_t total = pk.Npad * pk.ldX + (D.d ? pk.Npad * pk.ldZ : 0) + (pk.Npad - D.N) * pk.ldP;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   k_pack<<<blocks, 256, 0, st>>>(D.N, pk.Npad, D.p, D.K * D.d, X, Z, pk.Xp, pk.ldX,
-                                 D.d ? pk.Zp : nullptr, pk.ldZ);
+                                 D.d ? pk.Zp : nullptr, pk.ldZ, pk.Pr, pk.ldP);
   count_launch();
   return cudaGetLastError();
 }

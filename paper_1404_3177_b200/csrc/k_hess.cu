@@ -298,49 +298,57 @@ __global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, i
   const int64_t nq = Npad / 4;
   const int64_t q_begin = split * nq / splits, q_end = (split + 1) * nq / splits;
   const int r4 = lane & 3, c8 = lane >> 2;
-  int ekind[MT], ecol[MT], fkind[NT], fcol[NT];
+  // per (lane, block) source: element (i, col) = src[i * str] * sc, no divergent branches
+  // (sc = 0 for padding / the x~ part of alternative 0; src then points at a valid zero-weight row)
+  const double* esrc[MT];
+  int64_t estr[MT];
+  double esc[MT];
+  const double* fsrc[NT];
+  int64_t fstr[NT];
 #pragma unroll
   for (int mb = 0; mb < MT; ++mb) {
     const int e = ep * MT * 8 + mb * 8 + c8;
-    if (e < q) { ekind[mb] = (k == 0) ? 3 : 0; ecol[mb] = e; }
-    else if (e < q + d) { ekind[mb] = 1; ecol[mb] = k * d + (e - q); }
-    else if (e < E) { ekind[mb] = 2; ecol[mb] = k * f + (e - q - d); }
-    else { ekind[mb] = 3; ecol[mb] = 0; }
+    esc[mb] = 1.0;
+    if (e < q) { esrc[mb] = Xp + e; estr[mb] = ldX; if (k == 0) esc[mb] = 0.0; }
+    else if (e < q + d) { esrc[mb] = Zp + k * d + (e - q); estr[mb] = ldZ; }
+    else if (e < E) { esrc[mb] = Y + (int64_t)k * f + (e - q - d); estr[mb] = (int64_t)K * f; }
+    else { esrc[mb] = Xp; estr[mb] = ldX; esc[mb] = 0.0; }
   }
 #pragma unroll
   for (int nb = 0; nb < NT; ++nb) {
     const int fi = fp * NT * 8 + nb * 8 + c8;
-    if (fi < d) { fkind[nb] = 1; fcol[nb] = k * d + fi; }
-    else if (fi < F) { fkind[nb] = 2; fcol[nb] = k * f + (fi - d); }
-    else { fkind[nb] = 3; fcol[nb] = 0; }
+    if (fi < d) { fsrc[nb] = Zp + k * d + fi; fstr[nb] = ldZ; }
+    else if (fi < F) { fsrc[nb] = Y + (int64_t)k * f + (fi - d); fstr[nb] = (int64_t)K * f; }
+    else { fsrc[nb] = Xp; fstr[nb] = 0; }  // finite filler; its A partner rows are multiplied by 0 below
   }
-  auto ld = [&](int kind, int col, int64_t i) -> double {
-    if (kind == 0) return __ldg(Xp + i * ldX + col);
-    if (kind == 1) return __ldg(Zp + i * ldZ + col);
-    if (kind == 2) return i < N ? __ldg(Y + i * (int64_t)K * f + col) : 0.0;
-    return 0.0;
-  };
   double acc[MT][NT][2];
 #pragma unroll
   for (int a = 0; a < MT; ++a)
 #pragma unroll
     for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 2
-  for (int64_t qq = q_begin; qq < q_end; ++qq) {
-    const int64_t i = qq * 4 + r4;
-    const double pk = __ldg(Pr + i * ldP + k);
-    double av[MT], bv[NT];
+  constexpr int U = 2;  // quads of individuals whose loads are issued together
+  for (int64_t qq0 = q_begin; qq0 < q_end; qq0 += U) {
+    double av[U][MT], bv[U][NT];
 #pragma unroll
-    for (int mb = 0; mb < MT; ++mb) av[mb] = pk * ld(ekind[mb], ecol[mb], i);
+    for (int u = 0; u < U; ++u) {
+      int64_t i = (qq0 + u) * 4 + r4;
+      const double w8 = (qq0 + u < q_end) ? 1.0 : 0.0;
+      const double pk = w8 * __ldg(Pr + i * ldP + k);  // 0 for padding rows (i >= N)
+      const int64_t ic = i < N ? i : N - 1;            // Y has only N rows
 #pragma unroll
-    for (int nb = 0; nb < NT; ++nb) bv[nb] = ld(fkind[nb], fcol[nb], i);
+      for (int mb = 0; mb < MT; ++mb) av[u][mb] = pk * esc[mb] * __ldg(esrc[mb] + ic * estr[mb]);
 #pragma unroll
-    for (int mb = 0; mb < MT; ++mb)
+      for (int nb = 0; nb < NT; ++nb) bv[u][nb] = __ldg(fsrc[nb] + ic * fstr[nb]);
+    }
 #pragma unroll
-      for (int nb = 0; nb < NT; ++nb)
-        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-            : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
-            : "d"(av[mb]), "d"(bv[nb]));
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int mb = 0; mb < MT; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NT; ++nb)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
+              : "d"(av[u][mb]), "d"(bv[u][nb]));
   }
   double* out = Tpart + split * tstride + (int64_t)k * E * F;
 #pragma unroll
@@ -570,7 +578,10 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       if (KC == 16) ok = false;
     }
     const int E = q + d + f, F = d + f;
-    hp->ar_mt = (E + 7) / 8 >= 8 ? 8 : ((E + 7) / 8 > 4 ? 8 : ((E + 7) / 8 > 2 ? 4 : 2));
+    {
+      const int mbs = (E + 7) / 8;
+      hp->ar_mt = mbs > 6 ? 8 : (mbs > 4 ? 6 : (mbs > 2 ? 4 : 2));
+    }
     hp->ar_nt = (F + 7) / 8 > 2 ? 4 : 2;
     hp->ar_ep = (E + hp->ar_mt * 8 - 1) / (hp->ar_mt * 8);
     hp->ar_fp = (F + hp->ar_nt * 8 - 1) / (hp->ar_nt * 8);
@@ -681,6 +692,8 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
                                            pk.Pr, pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y, hp->Tpart, tstride)
       if (hp->ar_mt == 8 && hp->ar_nt == 4) MNL_ARROW(8, 4);
       else if (hp->ar_mt == 8) MNL_ARROW(8, 2);
+      else if (hp->ar_mt == 6 && hp->ar_nt == 4) MNL_ARROW(6, 4);
+      else if (hp->ar_mt == 6) MNL_ARROW(6, 2);
       else if (hp->ar_mt == 4 && hp->ar_nt == 4) MNL_ARROW(4, 4);
       else if (hp->ar_mt == 4) MNL_ARROW(4, 2);
       else if (hp->ar_nt == 4) MNL_ARROW(2, 4);

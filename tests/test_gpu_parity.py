@@ -205,3 +205,16 @@ def test_fit_maxiter_and_zero_iter():
     assert r.status == M.MNL_MAXITER and r.iters == 2
     r0 = M.mnl_newton_fit(dp, tol=1e-14, max_iter=0)
     assert r0.status == M.MNL_MAXITER and r0.iters == 0 and float(r0.coef.abs().max()) == 0.0
+
+
+def test_scratch_reuse_large_then_small_ragged():
+    """Library scratch (probability rows, packed design rows) is reused across problem sizes; padding
+    rows must read as exact zeros after a larger problem has used the buffers."""
+    big = datagen.make("c5")
+    gpu_eval(device_problem(big), big.theta_true)
+    small = datagen.custom(37, 5, 3, 2, 2, seed=41, coef_sd=0.4)
+    D = oracle_data(small)
+    l_o, g_o, H_o = O.mnl_eval(D, small.theta_true)
+    l, g, H = gpu_eval(device_problem(small), small.theta_true)
+    check_lg(l, g, l_o, g_o)
+    assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
