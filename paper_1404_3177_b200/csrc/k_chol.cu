@@ -15,6 +15,7 @@
 // The matrix is row-major with leading dimension lda; only the lower triangle is referenced.
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "internal.h"
 
@@ -211,18 +212,28 @@ __global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, in
   }
 }
 
-// trailing update: lower tiles (ti >= tj) of A22 -= L21 L21^T
-__global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, int j0) {
+// trailing update: lower tiles (ti >= tj) of A22 -= L21 L21^T.
+// col_only = 1: only block-column 0 of the trailing matrix (the next panel, lookahead path);
+// col_only = 0: the lower triangle starting at tile (first, first).
+__global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, int j0, int col_only, int first) {
   extern __shared__ __align__(16) double dsm[];
   double(*Li)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
   double(*Lj)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + NB * LDS);
   const int jb = min(NB, n - j0);
   const int s0 = j0 + jb;
-  const int t = blockIdx.x;  // -> (ti, tj), ti >= tj, row-major over the lower triangle
-  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-  while (ti * (ti + 1) / 2 > t) --ti;
-  const int tj = t - ti * (ti + 1) / 2;
+  int ti, tj;
+  if (col_only) {
+    ti = blockIdx.x;
+    tj = 0;
+  } else {
+    const int t = blockIdx.x;  // -> (ti, tj), ti >= tj, row-major over the lower triangle
+    ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    tj = t - ti * (ti + 1) / 2;
+    ti += first;
+    tj += first;
+  }
   const int ri = s0 + ti * NB, rj = s0 + tj * NB;
   const int tid = threadIdx.x;
   for (int e = tid; e < NB * NB; e += 256) {
@@ -389,24 +400,74 @@ cudaError_t launch_wave(int n, const double* L, int lda, double* x, int upper, c
   return e;
 }
 
-// factorisation; with x != null also the forward solve x <- L^{-1} x
+struct Lookahead {
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t start = nullptr, done = nullptr;
+};
+Lookahead g_la;
+
+cudaEvent_t la_event(size_t i) {
+  while (g_la.ev.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    g_la.ev.push_back(e);
+  }
+  return g_la.ev[i];
+}
+
+// Factorisation with a one-panel lookahead; with x != null also the forward solve x <- L^{-1} x.
+// side stream: [A22 update of the next panel's block column] -> potrf(j+1) -> trsm(j+1)
+// main stream: the rest of panel j's trailing update, concurrently.
 cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
   set_attrs();
   if (!ensure_work(n)) return cudaErrorMemoryAllocation;
+  if (!g_la.side) {
+    int lo = 0, hi = 0;  // the panel chain is the critical path: give it the highest priority
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&g_la.side, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&g_la.start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g_la.done, cudaEventDisableTiming);
+  }
+  cudaStream_t sp = g_la.side;
+  const int np = (n + NB - 1) / NB;
   cudaMemsetAsync(info, 0, sizeof(int), st);
-  for (int j0 = 0; j0 < n; j0 += NB) {
-    const int jb = std::min(NB, n - j0);
-    double* Lj = g_cw.Linv + (size_t)(j0 / NB) * NB * NB;
-    k_potrf_inv<<<1, 256, 0, st>>>(n, A, lda, j0, Lj, info, x);
+  cudaEventRecord(g_la.start, st);
+  cudaStreamWaitEvent(sp, g_la.start, 0);
+  auto panel = [&](int j) {  // potrf + trsm of panel j on the side stream
+    const int j0 = j * NB, jb = std::min(NB, n - j0);
+    double* Lj = g_cw.Linv + (size_t)j * NB * NB;
+    k_potrf_inv<<<1, 256, 0, sp>>>(n, A, lda, j0, Lj, info, x);
     count_launch();
     const int rem = n - j0 - jb;
     if (rem > 0) {
-      const int mt = (rem + NB - 1) / NB;
-      k_trsm_gemm<<<mt, 256, kDyn, st>>>(n, A, lda, j0, Lj, x);
-      k_syrk_tiles<<<mt * (mt + 1) / 2, 256, kDyn, st>>>(n, A, lda, j0);
-      count_launch(2);
+      k_trsm_gemm<<<(rem + NB - 1) / NB, 256, kDyn, sp>>>(n, A, lda, j0, Lj, x);
+      count_launch();
     }
+  };
+  panel(0);
+  cudaEventRecord(la_event(2 * 0), sp);  // ev_p(0)
+  for (int j = 0; j + 1 < np; ++j) {
+    const int j0 = j * NB;
+    const int rem = n - j0 - NB;
+    const int mt = (rem + NB - 1) / NB;
+    // main: rest of panel j's trailing update (tiles with tj >= 1)
+    cudaStreamWaitEvent(st, la_event(2 * j), 0);
+    if (mt > 1) {
+      k_syrk_tiles<<<(mt - 1) * mt / 2, 256, kDyn, st>>>(n, A, lda, j0, 0, 1);
+      count_launch();
+    }
+    cudaEventRecord(la_event(2 * j + 1), st);  // ev_r(j)
+    // side: next panel's block column, then its factorisation
+    k_syrk_tiles<<<mt, 256, kDyn, sp>>>(n, A, lda, j0, 1, 0);
+    count_launch();
+    panel(j + 1);
+    cudaEventRecord(la_event(2 * (j + 1)), sp);  // ev_p(j+1)
+    // the next column update (side, iteration j+1) must follow this rest update (main)
+    cudaStreamWaitEvent(sp, la_event(2 * j + 1), 0);
   }
+  cudaEventRecord(g_la.done, sp);
+  cudaStreamWaitEvent(st, g_la.done, 0);
   g_cw.factor = A;
   g_cw.factor_n = n;
   return cudaGetLastError();
