@@ -124,16 +124,20 @@ __device__ __forceinline__ double gen_val(const double* R, const Gen& g, int ks)
   return R[g.p1 + ks * g.s1] * fma(g.s, R[g.p2 + ks * g.s2], g.c0);
 }
 
-template <int BN, int KC>
-__global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
-  constexpr int WARPS_M = (BN == 128) ? 2 : 4;  // 128: 2x4 warps of 64x32; 96: 4x2 of 32x48; 64: 4x2 of 32x32
-  constexpr int WARPS_N = 8 / WARPS_M;
+template <int BN, int KC, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmParams P) {
+  // 8 warps: 128 -> 2x4 warps of 64x32; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32.
+  // 4 warps (two CTAs per SM): 64 -> 2x2 of 64x32.
+  constexpr int WARPS_M = NWARP == 4 ? 2 : ((BN == 128) ? 2 : 4);
+  constexpr int WARPS_N = NWARP / WARPS_M;
   constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   constexpr int MT = WTM / 8, NTL = WTN / 8;
   constexpr int KS = KC / 4;
   constexpr int PBA = BM / 16, PBB = BN / 16;
   constexpr int GA_D = KS * PBA * 64, GB_D = KS * PBB * 64;  // doubles per buffer
-  static_assert(PBA == 8, "A generator assumes 8 pair-blocks (one per warp)");
+  constexpr int PA_W = PBA / NWARP;                   // A pair-blocks generated per warp
+  constexpr int PB_W = (PBB + NWARP - 1) / NWARP;     // B pair-blocks generated per warp
+  static_assert(PBA % NWARP == 0, "A pair-blocks must split evenly over the warps");
 
   extern __shared__ __align__(128) double sm[];
   double* GA = sm;                          // [2][KS][PBA][32][2]
@@ -167,12 +171,21 @@ __global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
     const int64_t c_begin = split * P.nchunks / P.splits;
     const int64_t c_end = (split + 1) * P.nchunks / P.splits;
 
-    // per-thread generator columns (constant over the item)
-    const Gen gA0 = make_gen(P.descA[tm * BM + (2 * w) * 8 + cl], r4);
-    const Gen gA1 = make_gen(P.descA[tm * BM + (2 * w + 1) * 8 + cl], r4);
-    const int pbB = w < PBB ? w : 0;  // warp w < PBB generates B pair-block w (all ks)
-    const Gen gB0 = make_gen(P.descB[tn * BN + (2 * pbB) * 8 + cl], r4);
-    const Gen gB1 = make_gen(P.descB[tn * BN + (2 * pbB + 1) * 8 + cl], r4);
+    // per-thread generator columns (constant over the item): warp w generates A pair-blocks
+    // w*PA_W .. and B pair-blocks w*PB_W .. (those < PBB), all ks
+    Gen gA[PA_W][2], gBv[PB_W][2];
+#pragma unroll
+    for (int j = 0; j < PA_W; ++j) {
+      const int pb = w * PA_W + j;
+      gA[j][0] = make_gen(P.descA[tm * BM + (2 * pb) * 8 + cl], r4);
+      gA[j][1] = make_gen(P.descA[tm * BM + (2 * pb + 1) * 8 + cl], r4);
+    }
+#pragma unroll
+    for (int j = 0; j < PB_W; ++j) {
+      const int pb = min(w * PB_W + j, PBB - 1);
+      gBv[j][0] = make_gen(P.descB[tn * BN + (2 * pb) * 8 + cl], r4);
+      gBv[j][1] = make_gen(P.descB[tn * BN + (2 * pb + 1) * 8 + cl], r4);
+    }
 
     if (tid == 0) {
       for (int64_t c = c_begin; c < c_end && c < c_begin + 2; ++c) {
@@ -195,19 +208,25 @@ __global__ void __launch_bounds__(NT, 1) k_gen_gemm(const GemmParams P) {
       double* gb = GB + b * GB_D;
       // ---- generate operand fragments (fragment-native layout, one double2 per lane) ----
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        double2 v;
-        v.x = gen_val(R, gA0, ks);
-        v.y = gen_val(R, gA1, ks);
-        reinterpret_cast<double2*>(ga)[(ks * PBA + w) * 32 + lane] = v;
-      }
-      if (w < PBB) {
+      for (int j = 0; j < PA_W; ++j)
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           double2 v;
-          v.x = gen_val(R, gB0, ks);
-          v.y = gen_val(R, gB1, ks);
-          reinterpret_cast<double2*>(gb)[(ks * PBB + pbB) * 32 + lane] = v;
+          v.x = gen_val(R, gA[j][0], ks);
+          v.y = gen_val(R, gA[j][1], ks);
+          reinterpret_cast<double2*>(ga)[(ks * PBA + w * PA_W + j) * 32 + lane] = v;
+        }
+#pragma unroll
+      for (int j = 0; j < PB_W; ++j) {
+        const int pb = w * PB_W + j;
+        if (pb < PBB) {
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            double2 v;
+            v.x = gen_val(R, gBv[j][0], ks);
+            v.y = gen_val(R, gBv[j][1], ks);
+            reinterpret_cast<double2*>(gb)[(ks * PBB + pb) * 32 + lane] = v;
+          }
         }
       }
       __syncthreads();
@@ -432,7 +451,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
 // ------------------------------------------------------------------------------------------
 
 struct GemmJob {
-  int BN, KC;
+  int BN, KC, nwarp = 8;
   int MA, MB, tilesM, tilesN, splits;
   int64_t nchunks;
   ColDesc* dA = nullptr;  // device
@@ -492,12 +511,13 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
                       int KC, const Packed& pk, const int* segs, int nseg, int sms, size_t* bytes) {
   J.BN = BN;
   J.KC = KC;
+  J.nwarp = (BN == 64 && getenv("MNL_J1_NWARP4")) ? 4 : 8;  // experiments: two 4-warp CTAs per SM
   J.MA = (int)A.size();
   J.MB = (int)B.size();
   J.tilesM = (J.MA + BM - 1) / BM;
   J.tilesN = (J.MB + BN - 1) / BN;
   J.nchunks = pk.Npad / KC;
-  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms, 4);
+  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms * (8 / J.nwarp), 4);
   J.ldc = J.tilesN * BN;
   J.split_stride = (int64_t)J.tilesM * BM * J.ldc;
   J.nseg = nseg;
@@ -522,7 +542,7 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
   *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
   J.smem = (size_t)(2 * (KC / 4) * 8 * 64 + 2 * (KC / 4) * (BN / 16) * 64 + 2 * J.stage_doubles) * sizeof(double);
-  return J.smem <= 220 * 1024;
+  return J.smem <= (J.nwarp == 4 ? 112 * 1024 : 220 * 1024);
 }
 
 static void free_job(GemmJob& J) {
@@ -619,7 +639,7 @@ void hess_plan_destroy(HessPlan* hp) {
 
 size_t hess_plan_bytes(const HessPlan* hp) { return hp ? hp->bytes : 0; }
 
-template <int BN, int KC>
+template <int BN, int KC, int NWARP>
 static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st) {
   GemmParams P;
   P.descA = J.dA;
@@ -643,18 +663,17 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.stage_doubles = off;
   P.stage_bytes = (unsigned)(off * 8);
   P.counter = counter;
-  static bool attr[6] = {false, false, false, false, false, false};
-  const int ai = (BN == 128 ? 0 : (BN == 96 ? 2 : 4)) + (KC == 32 ? 0 : 1);
-  if (!attr[ai]) {
-    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
     if (e != cudaSuccess) return e;
-    attr[ai] = true;
+    attr = true;
   }
   const int items = J.tilesM * J.tilesN * J.splits;
-  const int grid = std::min(items, sms);
+  const int grid = std::min(items, sms * (8 / NWARP));
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
-  k_gen_gemm<BN, KC><<<grid, NT, J.smem, st>>>(P);
+  k_gen_gemm<BN, KC, NWARP><<<grid, NWARP * 32, J.smem, st>>>(P);
   count_launch();
   return cudaGetLastError();
 }
@@ -662,9 +681,10 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
 static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
                            cudaEvent_t after_gemm = nullptr) {
   cudaError_t e;
-  if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32>(J, pk, counter, sms, st) : run_gemm<128, 16>(J, pk, counter, sms, st);
-  else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32>(J, pk, counter, sms, st) : run_gemm<96, 16>(J, pk, counter, sms, st);
-  else e = J.KC == 32 ? run_gemm<64, 32>(J, pk, counter, sms, st) : run_gemm<64, 16>(J, pk, counter, sms, st);
+  if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4>(J, pk, counter, sms, st) : run_gemm<64, 16, 4>(J, pk, counter, sms, st);
+  else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8>(J, pk, counter, sms, st) : run_gemm<128, 16, 8>(J, pk, counter, sms, st);
+  else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8>(J, pk, counter, sms, st) : run_gemm<96, 16, 8>(J, pk, counter, sms, st);
+  else e = J.KC == 32 ? run_gemm<64, 32, 8>(J, pk, counter, sms, st) : run_gemm<64, 16, 8>(J, pk, counter, sms, st);
   if (e != cudaSuccess) return e;
   if (after_gemm) cudaEventRecord(after_gemm, st);
   const int64_t n = J.split_stride;

@@ -218,3 +218,22 @@ def test_scratch_reuse_large_then_small_ragged():
     l, g, H = gpu_eval(device_problem(small), small.theta_true)
     check_lg(l, g, l_o, g_o)
     assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+
+
+def test_fit_singular_design_reports_not_spd():
+    """A column of zeros makes -H exactly singular; the fit must stop with
+    MNL_ERR_NOT_SPD (the paper advises relaxing tolerances), not return garbage."""
+    prob = datagen.custom(300, 3, 2, 0, 0, seed=43)
+    prob.X[:, 1] = 0.0
+    dp = device_problem(prob)
+    r = M.mnl_newton_fit(dp, tol=1e-8, raise_on_error=False)
+    assert r.status == M.MNL_ERR_NOT_SPD
+
+
+def test_fit_from_host_buffers_matches_device():
+    prob = datagen.make("c1")
+    dp = device_problem(prob)
+    r = M.mnl_newton_fit(dp, tol=1e-8)
+    coef, iters, ll, rc = M.mnl_newton_fit_host(prob.X, prob.Y, prob.Z, prob.choice, prob.spec.K, tol=1e-8)
+    assert rc == M.MNL_OK and iters == r.iters
+    assert np.array_equal(coef, r.coef.cpu().numpy()) and ll == r.loglik
