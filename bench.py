@@ -11,7 +11,9 @@ Workload: BASELINE.json configs[3] ("c4", N=500000, K=100, p=50, n_p=5049), the 
 config the metric is quoted on; inputs are synthetic (datagen, seed 0), resident in HBM and larger
 than L2 (X 200 MB, probability rows 416 MB), so no L2 flush is needed between steps.
 
---gpus N > 1: replicas only (each rank runs its own full problem).
+--gpus N > 1: data-parallel over individuals (paper_1404_3177_b200/distributed.py): rank r owns a
+contiguous slice of the c4 individuals, one NCCL all-reduce of (l, g, H) per evaluation, every rank
+factors the same -H (strong scaling: the total work is fixed).
 --impl reference: the CPU oracle (oracle/) as it stands, timed on this host's cores on a bounded
 sample of the same workload (the only other place bench.py executes oracle/).
 """
@@ -139,14 +141,131 @@ def hess_flops(spec):
     return dict(j1=j1, j2=j2, arrow=ar, f_min=j1 + j2 + ar, f_paper=F_H)
 
 
+def run_dp(args):
+    """N > 1: data-parallel Newton step over the ranks' slices (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1404_3177_b200 as M
+    from paper_1404_3177_b200 import distributed as DP
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    M.load()
+    prob = datagen.make(args.config, seed=args.seed)
+    spec = prob.spec
+    lo, hi = DP.shard_range(spec.N, ws, rank)
+    X = torch.from_numpy(np.ascontiguousarray(prob.X[lo:hi])).to(dev)
+    Y = torch.from_numpy(np.ascontiguousarray(prob.Y[lo:hi])).to(dev) if spec.f else None
+    Z = torch.from_numpy(np.ascontiguousarray(prob.Z[lo:hi])).to(dev) if spec.d else None
+    ch = torch.from_numpy(prob.choice[lo:hi].astype(np.int32)).to(dev)
+    dp = M.problem(X, Y, Z, ch, K=spec.K)
+    launches = [0]
+    ev_inner = DP.cuda_evaluator(dp)
+
+    def evaluate(theta, g, h):
+        r = ev_inner(theta, g, h)
+        launches[0] += M.last_launch_count()
+        return r
+
+    def solve(A, g):
+        A = A.contiguous()
+        rc = M.mnl_cholesky(A)
+        launches[0] += M.last_launch_count()
+        if rc != M.MNL_OK:
+            return rc, None
+        x = M.mnl_cholesky_solve(A, g.contiguous())
+        launches[0] += M.last_launch_count()
+        return M.MNL_OK, x
+
+    def all_reduce(t):
+        dist.all_reduce(t)
+
+    theta0 = torch.zeros(spec.n_params, dtype=torch.float64, device=dev)
+
+    def step():
+        return DP.newton_fit_dp(evaluate, all_reduce, solve, theta0, tol=1e-300, max_iter=1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches[0] = 0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    hts = M.last_hessian_times()  # the last Hessian of the last step (this rank's slice)
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: each rank copies its slice from pinned host memory every step, result back to the host
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    hX, hch = pin(prob.X[lo:hi]), pin(prob.choice[lo:hi].astype(np.int32))
+    hY = pin(prob.Y[lo:hi]) if spec.f else None
+    hZ = pin(prob.Z[lo:hi]) if spec.d else None
+    n_e2e = max(1, min(args.steps, 3))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        X.copy_(hX, non_blocking=True)
+        ch.copy_(hch, non_blocking=True)
+        if hY is not None:
+            Y.copy_(hY, non_blocking=True)
+        if hZ is not None:
+            Z.copy_(hZ, non_blocking=True)
+        f = step()
+        f.coef.cpu()
+    torch.cuda.synchronize()
+    te = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    result = None
+    if rank == 0:
+        fl = hess_flops(spec)
+        peak, peak_src = fp64_peak_tflops()
+        j1_rank = fl["j1"] * (hi - lo) / spec.N
+        roof = {"kernel": "k_gen_gemm (J1) on rank 0's slice", "bound": "tensor",
+                "achieved": j1_rank / (hts["j1_gemm"] / 1e3) / 1e12 if hts["j1_gemm"] else None,
+                "peak": peak, "peak_source": peak_src, "unit": "TFLOP/s", "traffic": None,
+                "algorithmic_flops_per_launch": j1_rank, "avg_launch_ms": hts["j1_gemm"]}
+        roof["frac"] = roof["achieved"] / peak if roof["achieved"] else None
+        bi = hX.numel() * 8 + hch.numel() * 4 + (hY.numel() * 8 if hY is not None else 0) + \
+            (hZ.numel() * 8 if hZ is not None else 0)
+        result = {
+            "metric": METRIC, "value": args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen seed %d)" % args.seed,
+            "config": {"workload": f"{args.config}: N={spec.N} K={spec.K} p={spec.p} f={spec.f} d={spec.d} "
+                                   f"n_p={spec.n_params}, one Newton iteration from theta=0 per step",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"data-parallel over individuals, {ws} ranks, NCCL all-reduce of (l, g, H)"},
+            "s_per_newton_iter": ms / args.steps / 1e3,
+            "roofline": roof,
+            "gpu_launches": int(launches[0]),
+            "clocks": clk.summary(),
+            "e2e": {"value": 1.0 / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(bi),
+                    "d2h_bytes_per_step": int(spec.n_params * 8), "steps": n_e2e, "per_rank_bytes": True},
+        }
+    dist.barrier()
+    dist.destroy_process_group()
+    return result, prob
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_1404_3177_b200 as M
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl")
+    if ws > 1 or os.environ.get("BENCH_FORCE_DP"):
+        return run_dp(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     M.load()
@@ -324,7 +443,7 @@ def main():
     res, prob = run_ours(args)
     if res is None:
         return
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and res.get("n_gpus", 1) == 1 and "data-parallel" not in res["config"]["parallelism"]:
         res["cpu_baseline"] = cpu_baseline(prob, args.oracle_sample)
     print(json.dumps(res), flush=True)
 
