@@ -124,7 +124,9 @@ __device__ __forceinline__ double gen_val(const double* R, const Gen& g, int ks)
   return R[g.p1 + ks * g.s1] * fma(g.s, R[g.p2 + ks * g.s2], g.c0);
 }
 
-template <int BN, int KC, int NWARP>
+// AGEN: A columns use the general form R1 * (c0 + s R2) (J1's weights P_k (delta_kl - P_l));
+// otherwise, and always for B, the descriptors are plain products R1 * R2 (c0 = 0, s = 1).
+template <int BN, int KC, int NWARP, bool AGEN>
 __global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmParams P) {
   // 8 warps: 128 -> 2x4 warps of 64x32; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32.
   // 4 warps (two CTAs per SM): 64 -> 2x2 of 64x32.
@@ -207,25 +209,55 @@ __global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmPa
       double* ga = GA + b * GA_D;
       double* gb = GB + b * GB_D;
       // ---- generate operand fragments (fragment-native layout, one double2 per lane) ----
+      // in batches of GB k-slices: all shared-memory loads of a batch first, then the FP64 ops,
+      // then the stores (the accumulators leave ~60 registers free here; latency ~ 1 round trip)
+      constexpr int GBT = KS < 8 ? KS : 8;
 #pragma unroll
       for (int j = 0; j < PA_W; ++j)
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          double2 v;
-          v.x = gen_val(R, gA[j][0], ks);
-          v.y = gen_val(R, gA[j][1], ks);
-          reinterpret_cast<double2*>(ga)[(ks * PBA + w * PA_W + j) * 32 + lane] = v;
+        for (int kb = 0; kb < KS; kb += GBT) {
+          double a1[GBT][2], a2[GBT][2];
+#pragma unroll
+          for (int t = 0; t < GBT; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              a1[t][h] = R[gA[j][h].p1 + (kb + t) * gA[j][h].s1];
+              a2[t][h] = R[gA[j][h].p2 + (kb + t) * gA[j][h].s2];
+            }
+#pragma unroll
+          for (int t = 0; t < GBT; ++t) {
+            double2 v;
+            if constexpr (AGEN) {
+              v.x = a1[t][0] * fma(gA[j][0].s, a2[t][0], gA[j][0].c0);
+              v.y = a1[t][1] * fma(gA[j][1].s, a2[t][1], gA[j][1].c0);
+            } else {
+              v.x = a1[t][0] * a2[t][0];
+              v.y = a1[t][1] * a2[t][1];
+            }
+            reinterpret_cast<double2*>(ga)[((kb + t) * PBA + w * PA_W + j) * 32 + lane] = v;
+          }
         }
 #pragma unroll
       for (int j = 0; j < PB_W; ++j) {
         const int pb = w * PB_W + j;
         if (pb < PBB) {
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            double2 v;
-            v.x = gen_val(R, gBv[j][0], ks);
-            v.y = gen_val(R, gBv[j][1], ks);
-            reinterpret_cast<double2*>(gb)[(ks * PBB + pb) * 32 + lane] = v;
+          for (int kb = 0; kb < KS; kb += GBT) {
+            double b1[GBT][2], b2[GBT][2];
+#pragma unroll
+            for (int t = 0; t < GBT; ++t)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                b1[t][h] = R[gBv[j][h].p1 + (kb + t) * gBv[j][h].s1];
+                b2[t][h] = R[gBv[j][h].p2 + (kb + t) * gBv[j][h].s2];
+              }
+#pragma unroll
+            for (int t = 0; t < GBT; ++t) {
+              double2 v;
+              v.x = b1[t][0] * b2[t][0];
+              v.y = b1[t][1] * b2[t][1];
+              reinterpret_cast<double2*>(gb)[((kb + t) * PBB + pb) * 32 + lane] = v;
+            }
           }
         }
       }
@@ -452,6 +484,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
 
 struct GemmJob {
   int BN, KC, nwarp = 8;
+  bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
   int64_t nchunks;
   ColDesc* dA = nullptr;  // device
@@ -593,6 +626,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       for (int e = 0; e < f; ++e) AG.push_back(ColDesc{offP + K + e, pk.ldP, offX + 0, pk.ldX, 0.0, 1.0});
       A.insert(A.end(), AG.begin(), AG.end());
       B = AG;
+      hp->j2.agen = false;
       if (setup_job(hp->j2, A, B, choose_bn((int)B.size()), KC, pk, segs, nseg, sms, &bytes)) break;
       free_job(hp->j2);
       if (KC == 16) ok = false;
@@ -639,7 +673,7 @@ void hess_plan_destroy(HessPlan* hp) {
 
 size_t hess_plan_bytes(const HessPlan* hp) { return hp ? hp->bytes : 0; }
 
-template <int BN, int KC, int NWARP>
+template <int BN, int KC, int NWARP, bool AGEN>
 static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st) {
   GemmParams P;
   P.descA = J.dA;
@@ -665,7 +699,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.counter = counter;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP, AGEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -673,7 +707,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   const int items = J.tilesM * J.tilesN * J.splits;
   const int grid = std::min(items, sms * (8 / NWARP));
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
-  k_gen_gemm<BN, KC, NWARP><<<grid, NWARP * 32, J.smem, st>>>(P);
+  k_gen_gemm<BN, KC, NWARP, AGEN><<<grid, NWARP * 32, J.smem, st>>>(P);
   count_launch();
   return cudaGetLastError();
 }
@@ -681,10 +715,16 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
 static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
                            cudaEvent_t after_gemm = nullptr) {
   cudaError_t e;
-  if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4>(J, pk, counter, sms, st) : run_gemm<64, 16, 4>(J, pk, counter, sms, st);
-  else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8>(J, pk, counter, sms, st) : run_gemm<128, 16, 8>(J, pk, counter, sms, st);
-  else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8>(J, pk, counter, sms, st) : run_gemm<96, 16, 8>(J, pk, counter, sms, st);
-  else e = J.KC == 32 ? run_gemm<64, 32, 8>(J, pk, counter, sms, st) : run_gemm<64, 16, 8>(J, pk, counter, sms, st);
+  if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
+    if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 4, true>(J, pk, counter, sms, st);
+    else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true>(J, pk, counter, sms, st);
+    else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true>(J, pk, counter, sms, st);
+    else e = J.KC == 32 ? run_gemm<64, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true>(J, pk, counter, sms, st);
+  } else {  // J2: U^T U, plain products
+    if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, false>(J, pk, counter, sms, st);
+    else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, false>(J, pk, counter, sms, st);
+    else e = J.KC == 32 ? run_gemm<64, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, false>(J, pk, counter, sms, st);
+  }
   if (e != cudaSuccess) return e;
   if (after_gemm) cudaEventRecord(after_gemm, st);
   const int64_t n = J.split_stride;
