@@ -30,12 +30,13 @@ namespace mnl {
 namespace {
 
 constexpr int NW = 8;    // warps per CTA
-// individuals per tile: 8 warps x 8 rows, halved for K > 128 to bound shared memory
-__host__ __device__ constexpr int tile_rows(int kpl) { return kpl >= 8 ? 32 : 64; }
+// individuals per tile: 8 warps x 8 rows, halved for K > 128 or with alternative-varying data
+// (whose per-warp row staging needs the shared memory)
+__host__ __device__ constexpr int tile_rows(int kpl, bool yz) { return (kpl >= 8 && yz) ? 16 : ((kpl >= 8 || yz) ? 32 : 64); }
 
 struct EvalArgs {
   int64_t N;
-  int K, p, f, d, q, n_p, off_alpha, off_gamma, QP, XS;
+  int K, p, f, d, q, n_p, off_alpha, off_gamma, QP, XS, TI, SCR;
   const double* X;
   const double* Y;
   const double* Z;
@@ -58,10 +59,143 @@ __device__ __forceinline__ void neu_add(double& s, double& c, double x) {
   s = t;
 }
 
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Phase E (only with Y or Z): per individual, lanes over alternatives. The individual's Y and Z rows
+// are staged in this warp's smem slot by cp.async (the next individual's while this one computes):
+// corr = z.alpha + y.gamma, softmax, loglik, P (global Pr) and r (Rs), ybar, gamma/alpha gradients.
+__device__ __forceinline__ void stage_rows(const EvalArgs& A, double* slot, int64_t gi, int lane) {
+  const int ny = A.K * A.f, nz = A.K * A.d;
+  const double* ysrc = A.Y + gi * ny;
+  const double* zsrc = A.Z + gi * nz;
+  for (int t = lane; t < ny; t += 32)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(slot + t))), "l"(ysrc + t) : "memory");
+  for (int t = lane; t < nz; t += 32)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(slot + ny + t))), "l"(zsrc + t) : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int KPL>
+__device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, double* Rs, const int* ch_t, double* scr,
+                                        const double* alpha, const double* gamma, double* Wa, double (&gam)[8],
+                                        double& l_s, double& l_c, int64_t i0, int nt, int KPS, int w, int lane) {
+  const int K = A.K, d = A.d, f = A.f;
+  const int rows = (A.TI + NW - 1) / NW;  // individuals per warp per tile
+  const int ib = w * rows;
+  const int n_mine = min(rows, nt - ib);
+  for (int ii = ib + max(n_mine, 0); ii < ib + rows; ++ii)  // ragged tail: zero residual rows
+    for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
+  if (n_mine <= 0) return;
+  stage_rows(A, scr, i0 + ib, lane);
+  for (int jj = 0; jj < n_mine; ++jj) {
+    const int ii = ib + jj;
+    const int64_t gi = i0 + ii;
+    double* cur = scr + (jj & 1) * A.SCR;
+    if (jj + 1 < n_mine) {
+      stage_rows(A, scr + ((jj + 1) & 1) * A.SCR, gi + 1, lane);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const double* Ys = cur;
+    const double* Zs = cur + K * f;
+    double u[KPL];
+    double m = -INFINITY;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const int k = lane + 32 * kk;
+      double v = -INFINITY;
+      if (k < K) {
+        v = Us[ii * KPS + k];
+        for (int c = 0; c < d; ++c) v = fma(Zs[k * d + c], alpha[k * d + c], v);
+        for (int e = 0; e < f; ++e) v = fma(Ys[k * f + e], gamma[e], v);
+      }
+      u[kk] = v;
+      m = fmax(m, v);
+    }
+    m = warp_max(m);
+    double ssum = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const double e = (lane + 32 * kk < K) ? exp(u[kk] - m) : 0.0;
+      ssum += e;
+      u[kk] = e;
+    }
+    ssum = warp_sum(ssum);
+    int y = ch_t[ii];
+    if (y < 0 || y >= K) {
+      if (lane == 0) atomicOr(A.err, 1);
+      y = 0;
+    }
+    // u at the chosen alternative: recompute it (cheap) on the owning lane
+    double uy_l = 0.0;
+    if ((y & 31) == lane) {
+      const int k = y;
+      double v = Us[ii * KPS + k];
+      for (int c = 0; c < d; ++c) v = fma(Zs[k * d + c], alpha[k * d + c], v);
+      for (int e = 0; e < f; ++e) v = fma(Ys[k * f + e], gamma[e], v);
+      uy_l = v;
+    }
+    const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
+    if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
+    const double inv_s = 1.0 / ssum;
+    double r[KPL];
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const int k = lane + 32 * kk;
+      const double P = u[kk] * inv_s;
+      u[kk] = P;
+      r[kk] = (k < K) ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
+      if (k < KPS) Rs[ii * KPS + k] = r[kk];
+      if (A.writeP && k < K) A.Pr[gi * A.ldP + k] = P;
+    }
+    for (int e = 0; e < f; ++e) {
+      double yb = 0.0, gg = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        if (k < K) {
+          const double yv = Ys[k * f + e];
+          yb = fma(u[kk], yv, yb);
+          gg = fma(yv, r[kk], gg);
+        }
+      }
+      if (A.want_grad) {
+        if (e < 8) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t == e) gam[t] += gg;
+        } else {
+          Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gg;
+        }
+      }
+      if (A.writeP) {
+        yb = warp_sum(yb);
+        if (lane == 0) A.Pr[gi * A.ldP + K + e] = yb;
+      }
+    }
+    if (A.want_grad && d) {
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        if (k < K)
+          for (int c = 0; c < d; ++c) Wa[((w * KPL + kk) * d + c) * 32 + lane] += Zs[k * d + c] * r[kk];
+      }
+    }
+    __syncwarp();  // done with this slot before it is refilled
+  }
 }
 
 template <int KPL, int CM_MAX>
@@ -69,7 +203,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   extern __shared__ __align__(16) double sm[];
   constexpr int KP = 32 * KPL, KPS = KP + 4;   // alternatives padded; smem row stride = 4 (mod 16)
   constexpr int NBN = KP / 8;                   // 8-wide alternative blocks
-  constexpr int TI = tile_rows(KPL);
+  const int TI = A.TI;
   const int K = A.K, q = A.q, d = A.d, f = A.f, p = A.p;
   const int QP = A.QP, XS = A.XS;              // q padded to 4; X tile row stride (= 4 mod 16)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -82,6 +216,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
                                                 // then [NW][f][32] gamma-gradient (e >= 8)
   double* Cf = Wa + NW * KPL * d * 32 + NW * f * 32;  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
+  double* Scr = Cf + K * d + f + 1 + TI;                  // [NW][2][SCR] Y|Z rows of one individual
+  if ((reinterpret_cast<uintptr_t>(Scr) & 15u) != 0) Scr += 1;
 
   for (int idx = tid; idx < QP * KPS; idx += blockDim.x) {
     const int a = idx / KPS, k = idx - a * KPS;
@@ -155,36 +291,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     const double* X_t = Xs + buf * TI * XS;
     const int* ch_t = chs + buf * TI;
 
-    // ---------------- phase A2: corr[i][k] = z_ik.alpha_k + y_ik.gamma (lanes over alternatives) -----
-    // the warp's 8 individuals are processed together so their loads are in flight at once
-    if (d + f) {
-      const int ib = 8 * w;
-#pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) {
-        const int k = lane + 32 * kk;
-        if (k < K && ib < nt && ib < TI) {
-          double v[8];
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) v[jj] = 0.0;
-          for (int c = 0; c < d; ++c) {
-            const double al = alpha[k * d + c];
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (ib + jj < nt) v[jj] = fma(A.Z[((i0 + ib + jj) * K + k) * d + c], al, v[jj]);
-          }
-          for (int e = 0; e < f; ++e) {
-            const double ga = gamma[e];
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (ib + jj < nt) v[jj] = fma(A.Y[((i0 + ib + jj) * K + k) * f + e], ga, v[jj]);
-          }
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) Ps[(ib + jj) * KPS + k] = v[jj];
-        }
-      }
-      __syncthreads();
-    }
-
     // ---------------- phase B: u = X~ B on DMMA, then softmax / loglik / residuals ----------------
     const int il = (8 * w + c8) % TI;  // this lane's individual (row of the C fragment)
     const bool in_b = 8 * w < TI;      // warps beyond the tile skip phase B
@@ -203,20 +309,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     }
     const bool valid = in_b && il < nt;
     const int64_t i = i0 + il;
+    if (d + f) {
+      // ---- alternative-varying data present: stash u, then phase E (lanes over alternatives) ----
+      if (in_b) {
+#pragma unroll
+        for (int nb = 0; nb < NBN; ++nb)
+          *reinterpret_cast<double2*>(Ps + il * KPS + nb * 8 + 2 * r4) = make_double2(u[nb][0], u[nb][1]);
+      }
+      __syncthreads();
+      phase_e<KPL>(A, Ps, Rs, ch_t, Scr + w * 2 * A.SCR, alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+    } else {
     int y = valid ? ch_t[il] : 0;
     if (valid && (y < 0 || y >= K)) {
       atomicOr(A.err, 1);
       y = 0;
     }
-    // z.alpha + y.gamma corrections, mask padding alternatives
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int k = nb * 8 + 2 * r4 + h;
-        double v = u[nb][h];
-        if (k < K && valid && (d + f)) v += Ps[il * KPS + k];
-        u[nb][h] = (k < K) ? v : -INFINITY;
+        if (k >= K) u[nb][h] = -INFINITY;
       }
     double m = -INFINITY;
 #pragma unroll
@@ -241,7 +354,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     if (valid && r4 == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));
     const double inv_s = 1.0 / ssum;
     double* Rrow = Rs + il * KPS;
-    double* Prow = Ps + il * KPS;
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb) {
       const int k = nb * 8 + 2 * r4;
@@ -252,17 +364,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
       R2.y = valid ? ((k + 1 == y ? 1.0 : 0.0) - P2.y) : 0.0;
       if (k >= K) { P2.x = 0.0; R2.x = 0.0; }
       if (k + 1 >= K) { P2.y = 0.0; R2.y = 0.0; }
-      if (in_b) {
-        *reinterpret_cast<double2*>(Rrow + k) = R2;
-        if (f) *reinterpret_cast<double2*>(Prow + k) = P2;
-      }
+      if (in_b) *reinterpret_cast<double2*>(Rrow + k) = R2;
       if (A.writeP && valid) {
         double* pr = A.Pr + i * A.ldP + k;
         if (k + 1 < K) *reinterpret_cast<double2*>(pr) = P2;
         else if (k < K) pr[0] = P2.x;
       }
     }
-    __syncthreads();  // Rs / Ps complete
+    }
+    __syncthreads();  // Rs complete
 
     // ---------------- phase C: beta gradient G[a][k] += sum_i x~_ia r_ik on DMMA ----------------
     if (A.want_grad) {
@@ -285,66 +395,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
       }
     }
 
-    // ---------------- phase D: alpha / gamma gradients and ybar (lanes over alternatives) ---------
-    // the warp's 8 individuals together (independent loads in flight)
-    if (d || f) {
-      const int ib = 8 * w;
-      if (ib < nt && ib < TI) {
-        if (A.want_grad && d) {
-#pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) {
-            const int k = lane + 32 * kk;
-            if (k < K) {
-              double r[8];
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) r[jj] = (ib + jj < nt) ? Rs[(ib + jj) * KPS + k] : 0.0;
-              for (int c = 0; c < d; ++c) {
-                double acc = 0.0;
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                  if (ib + jj < nt) acc = fma(A.Z[((i0 + ib + jj) * K + k) * d + c], r[jj], acc);
-                Wa[((w * KPL + kk) * d + c) * 32 + lane] += acc;
-              }
-            }
-          }
-        }
-        for (int e = 0; e < f; ++e) {
-          double yb[8], gg = 0.0;
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) yb[jj] = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) {
-            const int k = lane + 32 * kk;
-            if (k < K) {
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                if (ib + jj < nt) {
-                  const double yv = A.Y[((i0 + ib + jj) * K + k) * f + e];
-                  yb[jj] = fma(Ps[(ib + jj) * KPS + k], yv, yb[jj]);
-                  gg = fma(yv, Rs[(ib + jj) * KPS + k], gg);
-                }
-              }
-            }
-          }
-          if (A.want_grad) {
-            if (e < 8) {
-#pragma unroll
-              for (int t = 0; t < 8; ++t)
-                if (t == e) gam[t] += gg;
-            } else {
-              Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gg;
-            }
-          }
-          if (A.writeP) {
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const double v = warp_sum(yb[jj]);
-              if (lane == 0 && ib + jj < nt) A.Pr[(i0 + ib + jj) * A.ldP + K + e] = v;
-            }
-          }
-        }
-      }
-    }
   }
 
   // ---------------- CTA partials (fixed order) ----------------
@@ -495,11 +545,17 @@ cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
 static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
+static int eval_scr(const Dims& D) {  // per-warp row staging: [2][Y row | Z row], 16-byte padded
+  const int n = D.K * D.f + D.K * D.d;
+  return (D.d + D.f) ? (n + 1) / 2 * 2 + 2 : 0;
+}
+
 static size_t eval_smem(const Dims& D, int kpl) {
-  const int KP = 32 * kpl, KPS = KP + 4, TI = tile_rows(kpl);
+  const int KP = 32 * kpl, KPS = KP + 4, TI = tile_rows(kpl, (D.d + D.f) > 0);
   const size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
                    ((D.d + D.f) ? (size_t)TI * KPS : 0) + (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32 +
-                   (size_t)D.K * D.d + D.f + 1 + TI;  // + 2*TI ints
+                   (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
+                   (size_t)NW * 2 * eval_scr(D);
   return n * sizeof(double);
 }
 
@@ -519,7 +575,8 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   plan->kpl = kpl;
   plan->smem = smem;
   plan->block = NW * 32;
-  const int64_t ntiles = (D.N + tile_rows(kpl) - 1) / tile_rows(kpl);
+  const int ti = tile_rows(kpl, (D.d + D.f) > 0);
+  const int64_t ntiles = (D.N + ti - 1) / ti;
   int64_t grid = sms;
   if (grid > ntiles) grid = ntiles;
   plan->grid = (int)grid;
@@ -535,6 +592,7 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = eval_qp(D); a.XS = eval_xs(D);
+  a.TI = tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = eval_scr(D);
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
   a.Pr = writeP ? pk->Pr : nullptr;
   a.ldP = writeP ? pk->ldP : 0;
