@@ -161,29 +161,45 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
       if (k < KPS) Rs[ii * KPS + k] = r[kk];
       if (A.writeP && k < K) A.Pr[gi * A.ldP + k] = P;
     }
-    for (int e = 0; e < f; ++e) {
-      double yb = 0.0, gg = 0.0;
+    // ybar_e = sum_k P_k y_ke and the gamma gradient, 8 components at a time; the cross-lane sums
+    // of ybar go through shared memory (red[8][33]): lane 4e'+j adds 8 of the 32 partials, then
+    // two shuffles - instead of a 5-step shuffle reduction per component
+    double* red = scr + 2 * A.SCR;  // [8][33] per warp
+    for (int e0 = 0; e0 < f; e0 += 8) {
+      double yb[8];
 #pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) {
-        const int k = lane + 32 * kk;
-        if (k < K) {
-          const double yv = Ys[k * f + e];
-          yb = fma(u[kk], yv, yb);
-          gg = fma(yv, r[kk], gg);
-        }
-      }
-      if (A.want_grad) {
-        if (e < 8) {
+      for (int t = 0; t < 8; ++t) {
+        const int e = e0 + t;
+        double ybt = 0.0, gg = 0.0;
+        if (e < f) {
 #pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if (t == e) gam[t] += gg;
-        } else {
-          Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gg;
+          for (int kk = 0; kk < KPL; ++kk) {
+            const int k = lane + 32 * kk;
+            if (k < K) {
+              const double yv = Ys[k * f + e];
+              ybt = fma(u[kk], yv, ybt);
+              gg = fma(yv, r[kk], gg);
+            }
+          }
+          if (A.want_grad) {
+            if (e < 8) gam[t] += gg;  // e0 == 0 here
+            else Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gg;
+          }
         }
+        yb[t] = ybt;
       }
       if (A.writeP) {
-        yb = warp_sum(yb);
-        if (lane == 0) A.Pr[gi * A.ldP + K + e] = yb;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) red[t * 33 + lane] = yb[t];
+        __syncwarp();
+        const int t = lane >> 2, j = lane & 3;
+        double sacc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sacc += red[t * 33 + j * 8 + q];
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+        if (j == 0 && e0 + t < f) A.Pr[gi * A.ldP + K + e0 + t] = sacc;
+        __syncwarp();
       }
     }
     if (A.want_grad && d) {
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
           *reinterpret_cast<double2*>(Ps + il * KPS + nb * 8 + 2 * r4) = make_double2(u[nb][0], u[nb][1]);
       }
       __syncthreads();
-      phase_e<KPL>(A, Ps, Rs, ch_t, Scr + w * 2 * A.SCR, alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+      phase_e<KPL>(A, Ps, Rs, ch_t, Scr + w * (2 * A.SCR + 8 * 33 + 2), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
     } else {
     int y = valid ? ch_t[il] : 0;
     if (valid && (y < 0 || y >= K)) {
@@ -531,7 +547,7 @@ cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024);
+                                         227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -547,7 +563,7 @@ static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
 static int eval_scr(const Dims& D) {  // per-warp row staging: [2][Y row | Z row], 16-byte padded
   const int n = D.K * D.f + D.K * D.d;
-  return (D.d + D.f) ? (n + 1) / 2 * 2 + 2 : 0;
+  return (D.d + D.f) ? (n + 1) / 2 * 2 + 2 : 0;  // per slot; plus the [8][33] reduction area
 }
 
 static size_t eval_smem(const Dims& D, int kpl) {
@@ -555,7 +571,7 @@ static size_t eval_smem(const Dims& D, int kpl) {
   const size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
                    ((D.d + D.f) ? (size_t)TI * KPS : 0) + (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32 +
                    (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
-                   (size_t)NW * 2 * eval_scr(D);
+                   (size_t)NW * (2 * eval_scr(D) + ((D.d + D.f) ? 8 * 33 + 2 : 0));
   return n * sizeof(double);
 }
 
@@ -571,7 +587,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   if (cm > 8 || 2 * cm * cn + 2 * nbn > 96) return false;
   plan->cm = cm;
   size_t smem = eval_smem(D, kpl);
-  if (smem > 220 * 1024) return false;
+  if (smem > 227 * 1024) return false;  // sm_100a opt-in maximum (232448 bytes)
   plan->kpl = kpl;
   plan->smem = smem;
   plan->block = NW * 32;
