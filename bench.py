@@ -231,10 +231,11 @@ def run_dp(args):
         fl = hess_flops(spec)
         peak, peak_src = fp64_peak_tflops()
         j1_rank = fl["j1"] * (hi - lo) / spec.N
-        roof = {"kernel": "k_gen_gemm (J1) on rank 0's slice", "bound": "tensor",
-                "achieved": j1_rank / (hts["j1_gemm"] / 1e3) / 1e12 if hts["j1_gemm"] else None,
+        j1_ms = hts["j1_gemm"] + hts["j1_tail"]
+        roof = {"kernel": "k_gen_gemm (J1 + tail) on rank 0's slice", "bound": "tensor",
+                "achieved": j1_rank / (j1_ms / 1e3) / 1e12 if j1_ms else None,
                 "peak": peak, "peak_source": peak_src, "unit": "TFLOP/s", "traffic": None,
-                "algorithmic_flops_per_launch": j1_rank, "avg_launch_ms": hts["j1_gemm"]}
+                "algorithmic_flops_per_launch": j1_rank, "avg_launch_ms": j1_ms}
         roof["frac"] = roof["achieved"] / peak if roof["achieved"] else None
         bi = hX.numel() * 8 + hch.numel() * 4 + (hY.numel() * 8 if hY is not None else 0) + \
             (hZ.numel() * 8 if hZ is not None else 0)
@@ -352,7 +353,7 @@ def run_ours(args):
                        "parallelism": "replicas" if ws > 1 else "single-gpu"},
             "s_per_newton_iter": ms_step / 1e3,
             "hessian_ms": float(np.mean(hess_ms)), "cholesky_solve_ms": float(np.mean(chol_ms)),
-            "roofline": {"kernel": "k_gen_gemm<128,32> (beta-beta pairs x vech DMMA GEMM, J1)",
+            "roofline": {"kernel": "k_gen_gemm (J1: beta-beta pairs x vech DMMA GEMM; 128-column tiles + narrow tail launch)",
                          "bound": "tensor", "achieved": achieved, "peak": peak, "peak_source": peak_src,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_flops_per_launch": fl["j1"], "avg_launch_ms": gemm_avg,

@@ -106,7 +106,7 @@ typedef struct {
   double chol_ms;           /* device time in Cholesky factor + solves */
   double eval_ms;           /* device time in log-likelihood / gradient passes */
   double total_ms;          /* wall time of the call */
-  double gemm_ms;           /* device time of the beta-beta DMMA GEMM kernel (J1), summed */
+  double gemm_ms;           /* device time of the beta-beta DMMA GEMMs (J1 + tail), summed */
   int32_t halvings_per_iter[64];  /* first 64 iterations */
 } mnl_fit_stats;
 
@@ -135,9 +135,11 @@ int mnl_cholesky(int32_t n, double* A, void* stream);
 int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, void* stream);
 
 /* Device times (ms, CUDA events on the call's stream) of the last Hessian assembly:
- * out[0] beta-beta DMMA GEMM kernel (J1), out[1] its split-N reduction, out[2] the Z/Y blocks
- * (J2 GEMM + reduction + same-alternative terms), out[3] the symmetric assembly. */
-int mnl_last_hessian_times(double out[4]);
+ * out[0] beta-beta DMMA GEMM over whole 128-column tiles (J1), out[1] its split-N reduction,
+ * out[2] the narrow tail GEMM of the remaining vech columns (J1b; 0 if none), out[3] its reduction,
+ * out[4] the Z/Y blocks (J2 GEMM + reduction + same-alternative terms),
+ * out[5] the symmetric assembly. */
+int mnl_last_hessian_times(double out[6]);
 
 /* Kernel launches made by the last call on this thread (for the bench's gpu_launches). */
 int64_t mnl_last_launch_count(void);

@@ -77,7 +77,7 @@ size_t hess_plan_bytes(const HessPlan*);
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y,
                            double* out, int ld_out, double sign, cudaStream_t st);
 // Phase times of the last launch_hessian (valid once the stream has passed it).
-void hess_last_times(HessPlan* hp, double out[4]);
+void hess_last_times(HessPlan* hp, double out[6]);
 
 // ---- k_chol.cu -------------------------------------------------------------------------
 // In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.

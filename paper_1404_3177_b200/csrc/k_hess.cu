@@ -42,7 +42,6 @@ struct ColDesc {
 namespace {
 
 constexpr int BM = 128;
-constexpr int NT = 256;
 
 struct GemmParams {
   const ColDesc* descA;
@@ -119,9 +118,6 @@ __device__ __forceinline__ Gen make_gen(const ColDesc& d, int r4) {
   g.c0 = d.c0;
   g.s = d.s;
   return g;
-}
-__device__ __forceinline__ double gen_val(const double* R, const Gen& g, int ks) {
-  return R[g.p1 + ks * g.s1] * fma(g.s, R[g.p2 + ks * g.s2], g.c0);
 }
 
 // AGEN: A columns use the general form R1 * (c0 + s R2) (J1's weights P_k (delta_kl - P_l));
@@ -417,8 +413,10 @@ __global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, i
 
 struct AsmArgs {
   int K, q, d, f, n_beta, off_gamma, n_p;
-  const double* C1;  // [pairs_pad][ld1]  (reduced)
+  const double* C1;  // [pairs_pad][ld1]  (reduced) vech columns [0, n1a)
   int ld1;
+  const double* C1b; // [pairs_pad][ld1b] vech columns [n1a, ...)
+  int ld1b, n1a;
   const double* C2;  // [n_p_pad][ld2]    (reduced)
   int ld2;
   const double* T;   // [K][E][F]         (reduced)
@@ -442,7 +440,9 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
     if (r < A.n_beta && c < A.n_beta) {
       int k1 = r / q, a1 = r - k1 * q, k2 = c / q, a2 = c - k2 * q;  // 0-based k-1
       const int kl = min(k1, k2), kh = max(k1, k2), al = min(a1, a2), ah = max(a1, a2);
-      negH = A.C1[tri_index(kl, kh, M) * A.ld1 + tri_index(al, ah, q)];
+      const int64_t pr = tri_index(kl, kh, M);
+      const int v = (int)tri_index(al, ah, q);
+      negH = v < A.n1a ? A.C1[pr * A.ld1 + v] : A.C1b[pr * A.ld1b + (v - A.n1a)];
     } else {
       const int lo = min(r, c), hi = max(r, c);
       double u = A.C2[(int64_t)lo * A.ld2 + (hi - A.n_beta)];
@@ -501,12 +501,14 @@ struct GemmJob {
 
 struct HessPlan {
   bool has_j2;
-  GemmJob j1, j2;
+  GemmJob j1, j1b, j2;  // j1b: the vech columns beyond the last whole 128-column tile of j1
+  bool has_j1b = false;
+  int n1a = 0;          // vech columns computed by j1
   int ar_splits, ar_mt, ar_nt, ar_ep, ar_fp;
   double* Tpart = nullptr;
   double* T = nullptr;
   unsigned* counters = nullptr;  // [2]
-  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t bytes = 0;
   int sms;
 };
@@ -606,8 +608,18 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       for (int a = 0; a < q; ++a)
         for (int b = a; b < q; ++b) B.push_back(ColDesc{offX + a, pk.ldX, offX + b, pk.ldX, 0.0, 1.0});
       // padding columns point at Xp[.][0] (finite) with c0 = s = 0
-      if (setup_job(hp->j1, A, B, choose_bn((int)B.size()), KC, pk, segs, 2, sms, &bytes)) break;
+      // Split the vech columns: whole 128-column tiles in j1, a narrow remainder job j1b (its own
+      // 64/96/128 width) instead of padding the last tile (c4: 1326 = 10 x 128 + 46).
+      const int nv = (int)B.size(), rem = nv % 128;
+      const bool split = nv > 128 && rem > 0 && rem <= 96;
+      hp->n1a = split ? nv - rem : nv;
+      std::vector<ColDesc> Ba(B.begin(), B.begin() + hp->n1a), Bb(B.begin() + hp->n1a, B.end());
+      bool good = setup_job(hp->j1, A, Ba, split ? 128 : choose_bn(nv), KC, pk, segs, 2, sms, &bytes);
+      hp->has_j1b = split;
+      if (good && split) good = setup_job(hp->j1b, A, Bb, choose_bn(rem), KC, pk, segs, 2, sms, &bytes);
+      if (good) break;
       free_job(hp->j1);
+      free_job(hp->j1b);
       if (KC == 16) ok = false;
     }
   }
@@ -662,6 +674,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
 void hess_plan_destroy(HessPlan* hp) {
   if (!hp) return;
   free_job(hp->j1);
+  free_job(hp->j1b);
   free_job(hp->j2);
   cudaFree(hp->Tpart);
   cudaFree(hp->T);
@@ -740,6 +753,13 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
   cudaError_t e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
   if (e != cudaSuccess) return e;
   cudaEventRecord(hp->ev[2], st);
+  if (hp->has_j1b) {
+    e = run_job(hp->j1b, pk, hp->counters, hp->sms, st, hp->ev[3]);
+    if (e != cudaSuccess) return e;
+  } else {
+    cudaEventRecord(hp->ev[3], st);
+  }
+  cudaEventRecord(hp->ev[4], st);
   if (hp->has_j2) {
     e = run_job(hp->j2, pk, hp->counters + 1, hp->sms, st);
     if (e != cudaSuccess) return e;
@@ -767,11 +787,12 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  cudaEventRecord(hp->ev[3], st);
+  cudaEventRecord(hp->ev[5], st);
   AsmArgs A;
   A.K = D.K; A.q = D.q; A.d = D.d; A.f = D.f;
   A.n_beta = D.n_beta; A.off_gamma = D.off_gamma; A.n_p = D.n_p;
   A.C1 = hp->j1.Cred; A.ld1 = hp->j1.ldc;
+  A.C1b = hp->has_j1b ? hp->j1b.Cred : nullptr; A.ld1b = hp->has_j1b ? hp->j1b.ldc : 0; A.n1a = hp->n1a;
   A.C2 = hp->has_j2 ? hp->j2.Cred : nullptr; A.ld2 = hp->has_j2 ? hp->j2.ldc : 0;
   A.T = hp->T;
   A.out = out; A.ld_out = ld_out; A.sign = sign;
@@ -779,12 +800,14 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   k_assemble<<<blocks, 256, 0, st>>>(A);
   count_launch();
-  cudaEventRecord(hp->ev[4], st);
+  cudaEventRecord(hp->ev[6], st);
   return cudaGetLastError();
 }
 
-void hess_last_times(HessPlan* hp, double out[4]) {
-  for (int i = 0; i < 4; ++i) {
+void hess_last_times(HessPlan* hp, double out[6]) {
+  // [0] J1 GEMM (128-column tiles), [1] its split reduction, [2] J1 tail GEMM (narrow tile),
+  // [3] its reduction, [4] Z/Y blocks (J2 + same-alternative), [5] assembly
+  for (int i = 0; i < 6; ++i) {
     float ms = 0.f;
     if (!hp || cudaEventElapsedTime(&ms, hp->ev[i], hp->ev[i + 1]) != cudaSuccess) ms = 0.f;
     out[i] = ms;
