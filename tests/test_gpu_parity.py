@@ -187,7 +187,7 @@ def test_fit_parity_random_start_with_halvings():
                           loglik=f.loglik), tol=1e-8, coef0=start)
 
 
-@pytest.mark.parametrize("cfg", ["c3", "c5"])
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
 def test_fit_parity_golden(cfg):
     path = os.path.join(GOLDEN, f"{cfg}_fit.json")
     if not os.path.exists(path):
