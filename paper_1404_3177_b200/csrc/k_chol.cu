@@ -26,89 +26,171 @@ constexpr int NB = 64;
 constexpr int LDS = NB + 4;  // 68 = 4 (mod 16) doubles: conflict-free 8x4 fragment gathers
 constexpr int LDR = NB + 1;  // row-per-thread access patterns
 
-// k_potrf_inv: right-looking Cholesky of the jb x jb diagonal block fused with X = L^{-1}, held in
-// REGISTERS: thread t owns row r = t / 4 and the columns q + 4k (q = t % 4, k < 16) of both S and X.
-// Step c: the owner of S[c][c] publishes the pivot; column c of L and row c of X are scaled by
-// 1/sqrt(pivot) by their owners and broadcast through shared memory (double-buffered by step
-// parity); every thread then updates its own elements:
-//   S[r][cc] -= L[r][c] L[cc][c]  (c < cc <= r),   X[r][j] -= L[r][c] X[c][j]  (r > c, j <= c).
-// Two barriers per step and no shared-memory read-modify-write.  With x != null it also applies
-// the forward-solve piece y_j = Linv b_j (b_j already holds every earlier panel's update).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// k_potrf_inv: Cholesky of the jb x jb diagonal block fused with X = L^{-1}, blocked by 16:
+// for each 16-column sub-panel: (1) one warp factors the 16 x 16 diagonal block in registers with
+// shuffles (lanes 0-15: rows of L, lanes 16-31: rows of its inverse), (2) L21 = A21 X11^T,
+// (3) A22 -= L21 L21^T on DMMA by all warps; finally the off-diagonal blocks of X are
+// X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj. With x != null it also applies the forward-solve piece
+// y_j = Linv b_j (b_j already holds every earlier panel's update).
+constexpr int SB = 16;
+// One step of the in-warp 16 x 16 Cholesky + inverse (compile-time C so that every register index
+// is static; lanes 0-15 hold rows of L, lanes 16-31 rows of L^{-1}).
+template <int C>
+__device__ __forceinline__ void chol16_step(double (&d)[16], bool isS, int r, bool& bad_any) {
+  const double piv = __shfl_sync(0xffffffffu, d[C], C);
+  const bool bad = !(piv > 0.0) || !isfinite(piv);
+  bad_any |= bad;
+  const double rd = bad ? 1.0 : rsqrt(piv);
+  if (isS) {
+    if (r == C) d[C] = bad ? 1.0 : piv * rd;
+    else if (r > C) d[C] *= rd;
+  } else if (r == C) {
+#pragma unroll
+    for (int j = 0; j <= C; ++j) d[j] *= rd;
+  }
+#pragma unroll
+  for (int cc = C + 1; cc < 16; ++cc) {
+    const double lcc = __shfl_sync(0xffffffffu, d[C], cc);
+    if (isS && r >= cc) d[cc] = fma(-d[C], lcc, d[cc]);
+  }
+  const double lrc = __shfl_sync(0xffffffffu, d[C], r);  // L[r][C] from S-lane r
+#pragma unroll
+  for (int j = 0; j <= C; ++j) {
+    const double xcj = __shfl_sync(0xffffffffu, d[j], 16 + C);
+    if (!isS && r > C) d[j] = fma(-lrc, xcj, d[j]);
+  }
+  if constexpr (C + 1 < 16) chol16_step<C + 1>(d, isS, r, bad_any);
+}
+
 __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, int j0, double* Linv, int* info,
                                                    double* x) {
-  __shared__ double colbuf[2][NB], rowbuf[2][NB], bv[NB];
-  __shared__ double piv_s;
+  extern __shared__ __align__(16) double dsm[];
+  double(*S)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm);
+  double(*X)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + NB * LDR);
+  __shared__ double T[NB][SB + 1];
+  __shared__ double bv[NB];
   const int jb = min(NB, n - j0);
-  const int tid = threadIdx.x, r = tid >> 2, q = tid & 3;
-  double Sr[16], Xr[16];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  {  // all 16 loads of a thread in flight at once (clamped addresses, masked values)
+    double v[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int cc = q + 4 * k;
-    Sr[k] = (r < jb && cc <= r) ? A[(int64_t)(j0 + r) * lda + j0 + cc] : 0.0;
-    Xr[k] = (cc == r) ? 1.0 : 0.0;
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      const int rr = r < jb ? r : jb - 1, ccl = c < jb ? c : jb - 1;
+      v[m] = __ldg(A + (int64_t)(j0 + rr) * lda + j0 + ccl);
+    }
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      // rows / columns beyond jb: identity (keeps the blocked steps well defined; never written back)
+      S[r][c] = (r < jb && c <= r) ? v[m] : (r == c ? 1.0 : 0.0);
+      X[r][c] = 0.0;
+    }
   }
   if (x && tid < NB) bv[tid] = tid < jb ? x[j0 + tid] : 0.0;
+  __syncthreads();
   bool bad_any = false;
-  for (int c = 0; c < jb; ++c) {
-    const int par = c & 1, kc = c >> 2;
-    const bool col_owner = (q == (c & 3));
-    if (col_owner && r == c) {
-      double v = 0.0;
+  for (int c0 = 0; c0 < NB; c0 += SB) {
+    // (1) warp 0: 16 x 16 diagonal block and its inverse, in registers
+    if (w == 0) {
+      const bool isS = lane < SB;
+      const int r = lane & (SB - 1);
+      double d[SB];
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (k == kc) v = Sr[k];
-      piv_s = v;
-    }
-    __syncthreads();
-    const double piv = piv_s;
-    const bool bad = !(piv > 0.0) || !isfinite(piv);
-    bad_any |= bad;
-    const double rd = bad ? 1.0 : rsqrt(piv);
-    if (col_owner && r >= c && r < jb) {
+      for (int j = 0; j < SB; ++j) d[j] = isS ? (j <= r ? S[c0 + r][c0 + j] : 0.0) : (j == r ? 1.0 : 0.0);
+      chol16_step<0>(d, isS, r, bad_any);
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (k == kc) {
-          Sr[k] = (r == c) ? (bad ? 1.0 : piv * rd) : Sr[k] * rd;
-          colbuf[par][r] = Sr[k];
-        }
-    }
-    if (r == c) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int j = q + 4 * k;
-        if (j <= c) {
-          Xr[k] *= rd;
-          rowbuf[par][j] = Xr[k];
+      for (int j = 0; j < SB; ++j) {
+        if (isS) {
+          if (j <= r) S[c0 + r][c0 + j] = d[j];
+        } else {
+          X[c0 + r][c0 + j] = (j <= r) ? d[j] : 0.0;
         }
       }
     }
     __syncthreads();
-    if (r > c && r < jb) {
-      const double lrc = colbuf[par][r];
+    const int r0 = c0 + SB, R = NB - r0;
+    if (R > 0) {
+      // (2) L21 = A21 X11^T  (rows r0.., 16 columns), via registers then in place
+      double l21[3];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int cc = q + 4 * k;
-        if (cc > c && cc <= r) Sr[k] = fma(-lrc, colbuf[par][cc], Sr[k]);
-        if (cc <= c) Xr[k] = fma(-lrc, rowbuf[par][cc], Xr[k]);
+      for (int m = 0; m < 3; ++m) {
+        const int e = tid + 256 * m;
+        l21[m] = 0.0;
+        if (e < R * SB) {
+          const int i = r0 + e / SB, j = e % SB;
+          double acc = 0.0;
+          for (int t = 0; t <= j; ++t) acc = fma(S[i][c0 + t], X[c0 + j][c0 + t], acc);
+          l21[m] = acc;
+        }
       }
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int e = tid + 256 * m;
+        if (e < R * SB) S[r0 + e / SB][c0 + e % SB] = l21[m];
+      }
+      __syncthreads();
+      // (3) A22 -= L21 L21^T on DMMA: 8x8 blocks (mb >= nb) of the R x R trailing matrix
+      const int MBk = R / 8;
+      const int lr = lane >> 2, lk = lane & 3;
+      for (int blk = w; blk < MBk * (MBk + 1) / 2; blk += 8) {
+        int mb = (int)((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
+        while ((mb + 1) * (mb + 2) / 2 <= blk) ++mb;
+        while (mb * (mb + 1) / 2 > blk) --mb;
+        const int nb = blk - mb * (mb + 1) / 2;
+        double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < SB; k0 += 4) {
+          const double a = S[r0 + mb * 8 + lr][c0 + k0 + lk];
+          const double b = S[r0 + nb * 8 + lr][c0 + k0 + lk];
+          dmma(c0v, c1v, a, b);
+        }
+        const int rr = r0 + mb * 8 + lr, cc = r0 + nb * 8 + 2 * lk;
+        if (cc <= rr) S[rr][cc] -= c0v;
+        if (cc + 1 <= rr) S[rr][cc + 1] -= c1v;
+      }
+      __syncthreads();
     }
   }
   if (tid == 0 && bad_any) atomicCAS(info, 0, j0 + 1);
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int cc = q + 4 * k;
-    if (r < jb && cc <= r) A[(int64_t)(j0 + r) * lda + j0 + cc] = Sr[k];
-    Linv[r * NB + cc] = (r < jb && cc <= r) ? Xr[k] : 0.0;  // [NB][NB], zero outside the triangle
+  // (4) off-diagonal blocks of X = L^{-1}: X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj, block rows in order
+  for (int bi = 1; bi < NB / SB; ++bi) {
+    const int i0 = bi * SB;
+    // T[j-cols] = sum_k L_ik X_kj for all j < i0 (16 x i0), then X_i,<i0 = -X_ii T
+    for (int e = tid; e < SB * i0; e += 256) {
+      const int ii = e / i0, jj = e % i0;
+      double acc = 0.0;
+      for (int t = (jj / SB) * SB; t < i0; ++t) acc = fma(S[i0 + ii][t], X[t][jj], acc);
+      T[jj][ii] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < SB * i0; e += 256) {
+      const int ii = e / i0, jj = e % i0;
+      double acc = 0.0;
+      for (int t = 0; t <= ii; ++t) acc = fma(X[i0 + ii][i0 + t], T[jj][t], acc);
+      X[i0 + ii][jj] = -acc;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < NB * NB; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    if (r < jb && c <= r) A[(int64_t)(j0 + r) * lda + j0 + c] = S[r][c];
+    Linv[e] = (r < jb && c <= r) ? X[r][c] : 0.0;  // [NB][NB], zero outside the triangle
   }
   if (x) {
-    __syncthreads();
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (q + 4 * k <= r) s = fma(Xr[k], bv[q + 4 * k], s);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (q == 0 && r < jb) x[j0 + r] = s;
+    const int r = tid >> 2, q = tid & 3;
+    double sacc = 0.0;
+    for (int t = q; t <= r; t += 4) sacc = fma(X[r][t], bv[t], sacc);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    if (q == 0 && r < jb) x[j0 + r] = sacc;
   }
 }
 
@@ -141,11 +223,6 @@ __global__ void __launch_bounds__(256) k_trtri_blocks(int n, const double* A, in
   }
 }
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
 
 // out[64x64] = X[64x64] * Y[64x64]^T from two smem tiles (row-major, LDS); 8 warps of 16x32
 __device__ __forceinline__ void tile_xyT(const double (*Xs)[LDS], const double (*Ys)[LDS], double acc[2][4][2]) {
@@ -384,6 +461,7 @@ void set_attrs() {
     cudaFuncSetAttribute(k_trsm_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
     cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
     cudaFuncSetAttribute(k_trtri_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
+    cudaFuncSetAttribute(k_potrf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
     attr = true;
   }
 }
@@ -437,7 +515,7 @@ cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t
   auto panel = [&](int j) {  // potrf + trsm of panel j on the side stream
     const int j0 = j * NB, jb = std::min(NB, n - j0);
     double* Lj = g_cw.Linv + (size_t)j * NB * NB;
-    k_potrf_inv<<<1, 256, 0, sp>>>(n, A, lda, j0, Lj, info, x);
+    k_potrf_inv<<<1, 256, kDynR, sp>>>(n, A, lda, j0, Lj, info, x);
     count_launch();
     const int rem = n - j0 - jb;
     if (rem > 0) {
