@@ -123,19 +123,24 @@ __device__ __forceinline__ Gen make_gen(const ColDesc& d, int r4) {
 // AGEN: A columns use the general form R1 * (c0 + s R2) (J1's weights P_k (delta_kl - P_l));
 // otherwise, and always for B, the descriptors are plain products R1 * R2 (c0 = 0, s = 1).
 template <int BN, int KC, int NWARP, bool AGEN>
-__global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmParams P) {
+__global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen_gemm(const GemmParams P) {
   // 8 warps: 128 -> 2x4 warps of 64x32; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32.
-  // 4 warps (two CTAs per SM): 64 -> 2x2 of 64x32.
-  constexpr int WARPS_M = NWARP == 4 ? 2 : ((BN == 128) ? 2 : 4);
+  // 4 warps (two CTAs per SM): 64 -> 2x2 of 64x32.  16 warps: 128 -> 4x4 of 32x32.
+  constexpr int WARPS_M = NWARP == 4 ? 2 : (NWARP == 16 ? 4 : ((BN == 128) ? 2 : 4));
   constexpr int WARPS_N = NWARP / WARPS_M;
   constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   constexpr int MT = WTM / 8, NTL = WTN / 8;
   constexpr int KS = KC / 4;
   constexpr int PBA = BM / 16, PBB = BN / 16;
   constexpr int GA_D = KS * PBA * 64, GB_D = KS * PBB * 64;  // doubles per buffer
-  constexpr int PA_W = PBA / NWARP;                   // A pair-blocks generated per warp
-  constexpr int PB_W = (PBB + NWARP - 1) / NWARP;     // B pair-blocks generated per warp
-  static_assert(PBA % NWARP == 0, "A pair-blocks must split evenly over the warps");
+  // generator work split: warp w handles pair-blocks of group wg (PA_W of A, PB_W of B) for the
+  // k-slices of half kh (16 warps: two warps share a pair-block, one k-half each)
+  constexpr int KSPLIT = NWARP > 8 ? NWARP / 8 : 1;
+  constexpr int NWG = NWARP / KSPLIT;                 // warps per k-slice group
+  constexpr int KSW = KS / KSPLIT;                    // k-slices per warp
+  constexpr int PA_W = PBA / NWG;                     // A pair-blocks generated per warp
+  constexpr int PB_W = (PBB + NWG - 1) / NWG;         // B pair-blocks generated per warp
+  static_assert(PBA % NWG == 0, "A pair-blocks must split evenly over the warps");
 
   extern __shared__ __align__(128) double sm[];
   double* GA = sm;                          // [2][KS][PBA][32][2]
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmPa
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wm = w / WARPS_N, wn = w % WARPS_N;
   const int r4 = lane & 3, cl = lane >> 2;
+  const int wg = w % NWG, kh = w / NWG;
 
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
@@ -174,13 +180,13 @@ __global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmPa
     Gen gA[PA_W][2], gBv[PB_W][2];
 #pragma unroll
     for (int j = 0; j < PA_W; ++j) {
-      const int pb = w * PA_W + j;
+      const int pb = wg * PA_W + j;
       gA[j][0] = make_gen(P.descA[tm * BM + (2 * pb) * 8 + cl], r4);
       gA[j][1] = make_gen(P.descA[tm * BM + (2 * pb + 1) * 8 + cl], r4);
     }
 #pragma unroll
     for (int j = 0; j < PB_W; ++j) {
-      const int pb = min(w * PB_W + j, PBB - 1);
+      const int pb = min(wg * PB_W + j, PBB - 1);
       gBv[j][0] = make_gen(P.descB[tn * BN + (2 * pb) * 8 + cl], r4);
       gBv[j][1] = make_gen(P.descB[tn * BN + (2 * pb + 1) * 8 + cl], r4);
     }
@@ -207,11 +213,12 @@ __global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmPa
       // ---- generate operand fragments (fragment-native layout, one double2 per lane) ----
       // in batches of GB k-slices: all shared-memory loads of a batch first, then the FP64 ops,
       // then the stores (the accumulators leave ~60 registers free here; latency ~ 1 round trip)
-      constexpr int GBT = KS < 8 ? KS : 8;
+      constexpr int GBT = KSW < 8 ? KSW : 8;
+      const int ks0 = kh * KSW;
 #pragma unroll
       for (int j = 0; j < PA_W; ++j)
 #pragma unroll
-        for (int kb = 0; kb < KS; kb += GBT) {
+        for (int kb = ks0; kb < ks0 + KSW; kb += GBT) {
           double a1[GBT][2], a2[GBT][2];
 #pragma unroll
           for (int t = 0; t < GBT; ++t)
@@ -230,15 +237,15 @@ __global__ void __launch_bounds__(NWARP * 32, 8 / NWARP) k_gen_gemm(const GemmPa
               v.x = a1[t][0] * a2[t][0];
               v.y = a1[t][1] * a2[t][1];
             }
-            reinterpret_cast<double2*>(ga)[((kb + t) * PBA + w * PA_W + j) * 32 + lane] = v;
+            reinterpret_cast<double2*>(ga)[((kb + t) * PBA + wg * PA_W + j) * 32 + lane] = v;
           }
         }
 #pragma unroll
       for (int j = 0; j < PB_W; ++j) {
-        const int pb = w * PB_W + j;
+        const int pb = wg * PB_W + j;
         if (pb < PBB) {
 #pragma unroll
-          for (int kb = 0; kb < KS; kb += GBT) {
+          for (int kb = ks0; kb < ks0 + KSW; kb += GBT) {
             double b1[GBT][2], b2[GBT][2];
 #pragma unroll
             for (int t = 0; t < GBT; ++t)
@@ -547,12 +554,13 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   J.BN = BN;
   J.KC = KC;
   J.nwarp = (BN == 64 && getenv("MNL_J1_NWARP4")) ? 4 : 8;  // experiments: two 4-warp CTAs per SM
+  if (BN == 128 && J.agen && getenv("MNL_J1_NWARP16")) J.nwarp = 16;  // experiments: 16 warps, 32x32 tiles
   J.MA = (int)A.size();
   J.MB = (int)B.size();
   J.tilesM = (J.MA + BM - 1) / BM;
   J.tilesN = (J.MB + BN - 1) / BN;
   J.nchunks = pk.Npad / KC;
-  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms * (8 / J.nwarp), 4);
+  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms * (J.nwarp < 8 ? 8 / J.nwarp : 1), 4);
   J.ldc = J.tilesN * BN;
   J.split_stride = (int64_t)J.tilesM * BM * J.ldc;
   J.nseg = nseg;
@@ -718,7 +726,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
     attr = true;
   }
   const int items = J.tilesM * J.tilesN * J.splits;
-  const int grid = std::min(items, sms * (8 / NWARP));
+  const int grid = std::min(items, sms * (NWARP < 8 ? 8 / NWARP : 1));
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
   k_gen_gemm<BN, KC, NWARP, AGEN><<<grid, NWARP * 32, J.smem, st>>>(P);
   count_launch();
@@ -730,6 +738,7 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
   cudaError_t e;
   if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
     if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 4, true>(J, pk, counter, sms, st);
+    else if (J.nwarp == 16) e = J.KC == 32 ? run_gemm<128, 32, 16, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 16, true>(J, pk, counter, sms, st);
     else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true>(J, pk, counter, sms, st);
     else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true>(J, pk, counter, sms, st);
     else e = J.KC == 32 ? run_gemm<64, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true>(J, pk, counter, sms, st);
