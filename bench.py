@@ -422,6 +422,32 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def full_fit_extra(cfg: str, seed: int):
+    """North-star context numbers in the same run: the full Newton fit of `cfg` to ||g|| < 1e-6
+    (BASELINE.json configs[4] is the fit config), median of 3 after a warm-up fit."""
+    import torch
+    import paper_1404_3177_b200 as M
+    prob = datagen.make(cfg, seed=seed)
+    s = prob.spec
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dp = M.problem(torch.from_numpy(prob.X).to(dev), torch.from_numpy(prob.Y).to(dev) if s.f else None,
+                   torch.from_numpy(prob.Z).to(dev) if s.d else None,
+                   torch.from_numpy(prob.choice.astype(np.int32)).to(dev), K=s.K)
+    M.mnl_newton_fit(dp, tol=1e-6)
+    runs = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f = M.mnl_newton_fit(dp, tol=1e-6)
+        runs.append((time.perf_counter() - t0, f))
+    t, f = sorted(runs, key=lambda r: r[0])[1]
+    return {"config": f"{cfg}: N={s.N} K={s.K} p={s.p} f={s.f} d={s.d} n_p={s.n_params}", "fit_s": t,
+            "iters": f.iters, "halvings": f.stats["halvings"], "s_per_newton_iter": t / max(1, f.iters),
+            "hessian_ms_per_iter": f.stats["hess_ms"] / max(1, f.iters),
+            "hessian_evals_per_s": 1e3 * max(1, f.iters) / f.stats["hess_ms"], "status": f.status,
+            "grad_norm": f.stats["grad_norm"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,6 +459,7 @@ def main():
     ap.add_argument("--oracle-sample", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -444,7 +471,10 @@ def main():
     res, prob = run_ours(args)
     if res is None:
         return
-    if not args.no_cpu_baseline and res.get("n_gpus", 1) == 1 and "data-parallel" not in res["config"]["parallelism"]:
+    single = res.get("n_gpus", 1) == 1 and "data-parallel" not in res["config"]["parallelism"]
+    if single and not args.no_extra and args.config != "c5":
+        res["extra_full_fit"] = full_fit_extra("c5", args.seed)
+    if not args.no_cpu_baseline and single:
         res["cpu_baseline"] = cpu_baseline(prob, args.oracle_sample)
     print(json.dumps(res), flush=True)
 
