@@ -57,6 +57,7 @@ struct GemmParams {
   int seg_off[3];
   int stage_doubles;
   unsigned stage_bytes;
+  int nraw;  // raw stages: 2 (prefetch two chunks ahead) or 1 (refill after the generate phase)
   unsigned* counter;
 };
 
@@ -192,8 +193,8 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
     }
 
     if (tid == 0) {
-      for (int64_t c = c_begin; c < c_end && c < c_begin + 2; ++c) {
-        const unsigned b = (gc + (unsigned)(c - c_begin)) & 1u;
+      for (int64_t c = c_begin; c < c_end && c < c_begin + P.nraw; ++c) {
+        const unsigned b = P.nraw == 2 ? ((gc + (unsigned)(c - c_begin)) & 1u) : 0u;
         tma_stage(P, RAW + b * P.stage_doubles, c, KC, &mbar[b]);
       }
     }
@@ -206,8 +207,9 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
 
     for (int64_t c = c_begin; c < c_end; ++c, ++gc) {
       const unsigned b = gc & 1u;
-      mbar_wait(&mbar[b], (gc >> 1) & 1u);
-      const double* R = RAW + b * P.stage_doubles;
+      const unsigned rb = P.nraw == 2 ? b : 0u;
+      mbar_wait(&mbar[rb], P.nraw == 2 ? ((gc >> 1) & 1u) : (gc & 1u));
+      const double* R = RAW + rb * P.stage_doubles;
       double* ga = GA + b * GA_D;
       double* gb = GB + b * GB_D;
       // ---- generate operand fragments (fragment-native layout, one double2 per lane) ----
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
         }
       }
       __syncthreads();
-      if (tid == 0 && c + 2 < c_end) tma_stage(P, RAW + b * P.stage_doubles, c + 2, KC, &mbar[b]);
+      if (tid == 0 && c + P.nraw < c_end) tma_stage(P, RAW + rb * P.stage_doubles, c + P.nraw, KC, &mbar[rb]);
       // ---- DMMA on this chunk (fragments for ks+1 loaded while ks's DMMAs issue) ----
       double af[2][MT], bf[2][NTL];
       auto load_frags = [&](int buf, int ks) {
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
 // ------------------------------------------------------------------------------------------
 
 struct GemmJob {
-  int BN, KC, nwarp = 8;
+  int BN, KC, nwarp = 8, nraw = 2;
   bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
   int64_t nchunks;
@@ -584,8 +586,14 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   if (cudaMalloc(&J.Cpart, cbytes * J.splits) != cudaSuccess) return false;
   if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
   *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
-  J.smem = (size_t)(2 * (KC / 4) * 8 * 64 + 2 * (KC / 4) * (BN / 16) * 64 + 2 * J.stage_doubles) * sizeof(double);
-  return J.smem <= (J.nwarp == 4 ? 112 * 1024 : 220 * 1024);
+  const size_t lim = J.nwarp == 4 ? 112 * 1024 : 220 * 1024;
+  for (J.nraw = 2; J.nraw >= 1; --J.nraw) {  // prefer two raw stages; one if the stage is large
+    J.smem = (size_t)(2 * (KC / 4) * 8 * 64 + 2 * (KC / 4) * (BN / 16) * 64 + J.nraw * J.stage_doubles) *
+             sizeof(double);
+    if (J.smem <= lim) return true;
+  }
+  J.nraw = 1;
+  return false;
 }
 
 static void free_job(GemmJob& J) {
@@ -717,6 +725,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   }
   P.stage_doubles = off;
   P.stage_bytes = (unsigned)(off * 8);
+  P.nraw = J.nraw;
   P.counter = counter;
   static bool attr = false;
   if (!attr) {
