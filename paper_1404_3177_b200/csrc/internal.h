@@ -76,6 +76,8 @@ size_t hess_plan_bytes(const HessPlan*);
 // sign = -1 writes -H (the Newton system matrix). out: [n_p][ld_out].
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y,
                            double* out, int ld_out, double sign, cudaStream_t st);
+// Call after re-packing the design rows (Xp / Zp): invalidates data the plan derived from them.
+void hess_plan_design_changed(HessPlan* hp);
 // Phase times of the last launch_hessian (valid once the stream has passed it).
 void hess_last_times(HessPlan* hp, double out[6]);
 

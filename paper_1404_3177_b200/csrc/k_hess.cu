@@ -58,6 +58,7 @@ struct GemmParams {
   int stage_doubles;
   unsigned stage_bytes;
   int nraw;  // raw stages: 2 (prefetch two chunks ahead) or 1 (refill after the generate phase)
+  const double* bfrag;  // BPRE: B operand precomputed in fragment-native order [tilesN][nchunks][GB_D]
   unsigned* counter;
 };
 
@@ -123,7 +124,9 @@ __device__ __forceinline__ Gen make_gen(const ColDesc& d, int r4) {
 
 // AGEN: A columns use the general form R1 * (c0 + s R2) (J1's weights P_k (delta_kl - P_l));
 // otherwise, and always for B, the descriptors are plain products R1 * R2 (c0 = 0, s = 1).
-template <int BN, int KC, int NWARP, bool AGEN>
+// BPRE: the B operand does not depend on the probabilities (J1's vech x~ x~^T), so it is precomputed
+// once per design in fragment-native order and fetched per chunk by one bulk copy (no generation).
+template <int BN, int KC, int NWARP, bool AGEN, bool BPRE = false>
 __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen_gemm(const GemmParams P) {
   // 8 warps: 128 -> 2x4 warps of 64x32; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32.
   // 4 warps (two CTAs per SM): 64 -> 2x2 of 64x32.  16 warps: 128 -> 4x4 of 32x32.
@@ -148,16 +151,28 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
   double* GB = GA + 2 * GA_D;               // [2][KS][PBB][32][2]
   double* RAW = GB + 2 * GB_D;              // [2][stage_doubles]
   __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t bfull[2];
   __shared__ int s_item;
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wm = w / WARPS_N, wn = w % WARPS_N;
   const int r4 = lane & 3, cl = lane >> 2;
   const int wg = w % NWG, kh = w / NWG;
+  auto b_copy = [&](int tn_, int64_t c_, unsigned buf) {  // BPRE: fetch chunk c_'s B fragments
+    const unsigned bar = smem_u32(&bfull[buf]);
+    constexpr unsigned bytes = GB_D * 8;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    const double* src = P.bfrag + ((int64_t)tn_ * P.nchunks + c_) * GB_D;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(GB + buf * GB_D)), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
 
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&bfull[0], 1);
+    mbar_init(&bfull[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -197,6 +212,7 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
         const unsigned b = P.nraw == 2 ? ((gc + (unsigned)(c - c_begin)) & 1u) : 0u;
         tma_stage(P, RAW + b * P.stage_doubles, c, KC, &mbar[b]);
       }
+      if constexpr (BPRE) b_copy(tn, c_begin, gc & 1u);
     }
 
     double acc[MT][NTL][2];
@@ -209,6 +225,7 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
       const unsigned b = gc & 1u;
       const unsigned rb = P.nraw == 2 ? b : 0u;
       mbar_wait(&mbar[rb], P.nraw == 2 ? ((gc >> 1) & 1u) : (gc & 1u));
+      if constexpr (BPRE) mbar_wait(&bfull[b], (gc >> 1) & 1u);
       const double* R = RAW + rb * P.stage_doubles;
       double* ga = GA + b * GA_D;
       double* gb = GB + b * GB_D;
@@ -243,7 +260,7 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
           }
         }
 #pragma unroll
-      for (int j = 0; j < PB_W; ++j) {
+      for (int j = 0; j < (BPRE ? 0 : PB_W); ++j) {
         const int pb = wg * PB_W + j;
         if (pb < PBB) {
 #pragma unroll
@@ -268,6 +285,8 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
       }
       __syncthreads();
       if (tid == 0 && c + P.nraw < c_end) tma_stage(P, RAW + rb * P.stage_doubles, c + P.nraw, KC, &mbar[rb]);
+      if constexpr (BPRE)
+        if (tid == 0 && c + 1 < c_end) b_copy(tn, c + 1, b ^ 1u);  // its buffer was freed by DMMA(c-1)
       // ---- DMMA on this chunk (fragments for ks+1 loaded while ks's DMMAs issue) ----
       double af[2][MT], bf[2][NTL];
       auto load_frags = [&](int buf, int ks) {
@@ -305,6 +324,26 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
         *reinterpret_cast<double2*>(Cb + row * P.ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
     }
+  }
+}
+
+// BPRE: J1's B operand (x~_a x~_b for the tile's vech columns) in the kernel's fragment-native order:
+// out[(tn * nchunks + c) * GB_D + ((ks * PBB + pb) * 32 + lane) * 2 + h] =
+//   Xp[i][a(col)] * Xp[i][b(col)],  col = tn * BN + (2 pb + h) * 8 + lane / 4,  i = c * KC + 4 ks + lane % 4
+__global__ void k_bfrag(double* __restrict__ out, int64_t total, int BN, int KC, int64_t nchunks,
+                        const int* __restrict__ va, const int* __restrict__ vb, const double* __restrict__ Xp, int ldX) {
+  const int PBB = BN / 16, KS = KC / 4;
+  const int64_t GB_D = (int64_t)KS * PBB * 64;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = e / GB_D;
+    const int r = (int)(e - blk * GB_D);
+    const int h = r & 1, lane = (r >> 1) & 31, pb = (r >> 6) % PBB, ks = (r >> 6) / PBB;
+    const int tn = (int)(blk / nchunks);
+    const int64_t c = blk - (int64_t)tn * nchunks;
+    const int col = tn * BN + (2 * pb + h) * 8 + (lane >> 2);
+    const int64_t i = c * KC + 4 * ks + (lane & 3);
+    const int a = va[col], b = vb[col];
+    out[e] = (a >= 0) ? Xp[i * ldX + a] * Xp[i * ldX + b] : 0.0;
   }
 }
 
@@ -493,6 +532,9 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
 
 struct GemmJob {
   int BN, KC, nwarp = 8, nraw = 2;
+  bool bpre = false;        // B operand precomputed (k_bfrag) instead of generated
+  double* bfrag = nullptr;  // [tilesN][nchunks][GB_D]
+  int *va = nullptr, *vb = nullptr;  // per B column: vech (a, b), -1 for padding
   bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
   int64_t nchunks;
@@ -510,6 +552,7 @@ struct GemmJob {
 
 struct HessPlan {
   bool has_j2;
+  bool bvalid = false;  // J1's precomputed B fragments match the packed design rows
   GemmJob j1, j1b, j2;  // j1b: the vech columns beyond the last whole 128-column tile of j1
   bool has_j1b = false;
   int n1a = 0;          // vech columns computed by j1
@@ -599,6 +642,12 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
 static void free_job(GemmJob& J) {
   cudaFree(J.dA);
   cudaFree(J.dB);
+  cudaFree(J.bfrag);
+  cudaFree(J.va);
+  cudaFree(J.vb);
+  J.bfrag = nullptr;
+  J.va = J.vb = nullptr;
+  J.bpre = false;
   cudaFree(J.Cpart);
   cudaFree(J.Cred);
   J.dA = J.dB = nullptr;
@@ -630,7 +679,33 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       const bool split = nv > 128 && rem > 0 && rem <= 96;
       hp->n1a = split ? nv - rem : nv;
       std::vector<ColDesc> Ba(B.begin(), B.begin() + hp->n1a), Bb(B.begin() + hp->n1a, B.end());
-      bool good = setup_job(hp->j1, A, Ba, split ? 128 : choose_bn(nv), KC, pk, segs, 2, sms, &bytes);
+      // B of the main job precomputed once per design if it fits comfortably in HBM
+      const int bn1 = split ? 128 : choose_bn(nv);
+      const size_t bfrag_bytes = (size_t)((hp->n1a + bn1 - 1) / bn1) * bn1 * (size_t)pk.Npad * sizeof(double);
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const bool want_bpre = getenv("MNL_NO_BPRE") == nullptr && bfrag_bytes <= (size_t)32 << 30 &&
+                             bfrag_bytes + ((size_t)4 << 30) < free_b;
+      const int segs_p[1] = {0};
+      hp->j1.bpre = want_bpre;
+      bool good = setup_job(hp->j1, A, Ba, bn1, KC, pk, want_bpre ? segs_p : segs, want_bpre ? 1 : 2, sms, &bytes);
+      if (good && want_bpre) {
+        GemmJob& J = hp->j1;
+        const size_t ncol = (size_t)J.tilesN * J.BN;
+        std::vector<int> va(ncol, -1), vb(ncol, -1);
+        for (int a = 0, col = 0; a < q; ++a)
+          for (int b = a; b < q; ++b, ++col)
+            if (col < hp->n1a) { va[col] = a; vb[col] = b; }
+        const size_t nfr = (size_t)J.tilesN * J.nchunks * ((KC / 4) * (J.BN / 16) * 64);
+        good = cudaMalloc(&J.bfrag, nfr * sizeof(double)) == cudaSuccess &&
+               cudaMalloc(&J.va, ncol * sizeof(int)) == cudaSuccess &&
+               cudaMalloc(&J.vb, ncol * sizeof(int)) == cudaSuccess;
+        if (good) {
+          cudaMemcpy(J.va, va.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
+          cudaMemcpy(J.vb, vb.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
+          bytes += nfr * sizeof(double);
+        }
+      }
       hp->has_j1b = split;
       if (good && split) good = setup_job(hp->j1b, A, Bb, choose_bn(rem), KC, pk, segs, 2, sms, &bytes);
       if (good) break;
@@ -702,7 +777,7 @@ void hess_plan_destroy(HessPlan* hp) {
 
 size_t hess_plan_bytes(const HessPlan* hp) { return hp ? hp->bytes : 0; }
 
-template <int BN, int KC, int NWARP, bool AGEN>
+template <int BN, int KC, int NWARP, bool AGEN, bool BPRE = false>
 static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st) {
   GemmParams P;
   P.descA = J.dA;
@@ -726,10 +801,11 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.stage_doubles = off;
   P.stage_bytes = (unsigned)(off * 8);
   P.nraw = J.nraw;
+  P.bfrag = J.bfrag;
   P.counter = counter;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP, AGEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP, AGEN, BPRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -737,7 +813,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   const int items = J.tilesM * J.tilesN * J.splits;
   const int grid = std::min(items, sms * (NWARP < 8 ? 8 / NWARP : 1));
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
-  k_gen_gemm<BN, KC, NWARP, AGEN><<<grid, NWARP * 32, J.smem, st>>>(P);
+  k_gen_gemm<BN, KC, NWARP, AGEN, BPRE><<<grid, NWARP * 32, J.smem, st>>>(P);
   count_launch();
   return cudaGetLastError();
 }
@@ -748,8 +824,11 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
   if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
     if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 4, true>(J, pk, counter, sms, st);
     else if (J.nwarp == 16) e = J.KC == 32 ? run_gemm<128, 32, 16, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 16, true>(J, pk, counter, sms, st);
+    else if (J.BN == 128 && J.bpre) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true>(J, pk, counter, sms, st);
+    else if (J.BN == 96 && J.bpre) e = J.KC == 32 ? run_gemm<96, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true>(J, pk, counter, sms, st);
+    else if (J.bpre) e = J.KC == 32 ? run_gemm<64, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true, true>(J, pk, counter, sms, st);
     else e = J.KC == 32 ? run_gemm<64, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true>(J, pk, counter, sms, st);
   } else {  // J2: U^T U, plain products
     if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, false>(J, pk, counter, sms, st);
@@ -767,6 +846,13 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
 
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y, double* out,
                            int ld_out, double sign, cudaStream_t st) {
+  if (hp->j1.bpre && !hp->bvalid) {  // once per design (the packed rows changed)
+    const GemmJob& J = hp->j1;
+    const int64_t total = (int64_t)J.tilesN * J.nchunks * ((J.KC / 4) * (J.BN / 16) * 64);
+    k_bfrag<<<148 * 8, 256, 0, st>>>(J.bfrag, total, J.BN, J.KC, J.nchunks, J.va, J.vb, pk.Xp, pk.ldX);
+    count_launch();
+    hp->bvalid = true;
+  }
   cudaEventRecord(hp->ev[0], st);
   cudaError_t e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
   if (e != cudaSuccess) return e;
@@ -820,6 +906,10 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
   count_launch();
   cudaEventRecord(hp->ev[6], st);
   return cudaGetLastError();
+}
+
+void hess_plan_design_changed(HessPlan* hp) {
+  if (hp) hp->bvalid = false;
 }
 
 void hess_last_times(HessPlan* hp, double out[6]) {

@@ -164,6 +164,7 @@ int eval_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const doubl
   if (want_h) {
     if (!ensure_packed(W, D, &pk)) return MNL_ERR_CUDA;
     if (launch_pack(D, pk, X, Z, st) != cudaSuccess) return MNL_ERR_CUDA;
+    if (W.hp) hess_plan_design_changed(W.hp);
   }
   double* g = grad;
   double scal[3];
@@ -207,6 +208,7 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
   HessPlan* hp = get_hess_plan(W, D, pk);
   if (!hp) return MNL_ERR_CUDA;
   if (launch_pack(D, pk, X, Z, st) != cudaSuccess) return MNL_ERR_CUDA;
+  hess_plan_design_changed(hp);
   if (coef0) cudaMemcpyAsync(W.theta, coef0, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
   else cudaMemsetAsync(W.theta, 0, n * sizeof(double), st);
 
