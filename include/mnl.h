@@ -138,8 +138,9 @@ int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, v
  * out[0] beta-beta DMMA GEMM over whole 128-column tiles (J1), out[1] its split-N reduction,
  * out[2] the narrow tail GEMM of the remaining vech columns (J1b; 0 if none), out[3] its reduction,
  * out[4] the Z/Y blocks (J2 GEMM + reduction + same-alternative terms),
- * out[5] the symmetric assembly. */
-int mnl_last_hessian_times(double out[6]);
+ * out[5] the symmetric assembly, out[6] the J1 operand materialisation that precedes out[0]
+ * (weights every evaluation, design products once per packed design; 0 when generated in-kernel). */
+int mnl_last_hessian_times(double out[7]);
 
 /* Kernel launches made by the last call on this thread (for the bench's gpu_launches). */
 int64_t mnl_last_launch_count(void);

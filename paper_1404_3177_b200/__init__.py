@@ -106,10 +106,10 @@ def last_launch_count() -> int:
 
 def last_hessian_times() -> dict:
     """Device ms of the last Hessian assembly phases (CUDA events inside the library)."""
-    out = (ctypes.c_double * 6)()
+    out = (ctypes.c_double * 7)()
     load().mnl_last_hessian_times(out)
     return dict(j1_gemm=out[0], j1_reduce=out[1], j1_tail=out[2], j1_tail_reduce=out[3], j2_and_arrow=out[4],
-                assemble=out[5])
+                assemble=out[5], j1_operands=out[6])
 
 
 def release() -> None:

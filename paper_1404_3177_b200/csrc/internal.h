@@ -79,7 +79,7 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
 // Call after re-packing the design rows (Xp / Zp): invalidates data the plan derived from them.
 void hess_plan_design_changed(HessPlan* hp);
 // Phase times of the last launch_hessian (valid once the stream has passed it).
-void hess_last_times(HessPlan* hp, double out[6]);
+void hess_last_times(HessPlan* hp, double out[7]);
 
 // ---- k_chol.cu -------------------------------------------------------------------------
 // In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.

@@ -327,23 +327,192 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
   }
 }
 
-// BPRE: J1's B operand (x~_a x~_b for the tile's vech columns) in the kernel's fragment-native order:
+// BPRE: J1's B operand (x~_a x~_b for the tile's vech columns) in the kernels' fragment-native
+// order, one CTA per chunk of KC individuals (design rows staged once, all tn blocks written):
 // out[(tn * nchunks + c) * GB_D + ((ks * PBB + pb) * 32 + lane) * 2 + h] =
 //   Xp[i][a(col)] * Xp[i][b(col)],  col = tn * BN + (2 pb + h) * 8 + lane / 4,  i = c * KC + 4 ks + lane % 4
-__global__ void k_bfrag(double* __restrict__ out, int64_t total, int BN, int KC, int64_t nchunks,
-                        const int* __restrict__ va, const int* __restrict__ vb, const double* __restrict__ Xp, int ldX) {
-  const int PBB = BN / 16, KS = KC / 4;
-  const int64_t GB_D = (int64_t)KS * PBB * 64;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = e / GB_D;
-    const int r = (int)(e - blk * GB_D);
-    const int h = r & 1, lane = (r >> 1) & 31, pb = (r >> 6) % PBB, ks = (r >> 6) / PBB;
-    const int tn = (int)(blk / nchunks);
-    const int64_t c = blk - (int64_t)tn * nchunks;
-    const int col = tn * BN + (2 * pb + h) * 8 + (lane >> 2);
-    const int64_t i = c * KC + 4 * ks + (lane & 3);
-    const int a = va[col], b = vb[col];
-    out[e] = (a >= 0) ? Xp[i * ldX + a] * Xp[i * ldX + b] : 0.0;
+__global__ void __launch_bounds__(256) k_bfrag(double* __restrict__ out, int tilesN, int BN, int KC, int64_t nchunks,
+                                               const int* __restrict__ va, const int* __restrict__ vb,
+                                               const double* __restrict__ Xp, int ldX) {
+  extern __shared__ __align__(16) double xs[];  // [KC][ldX]
+  const int64_t c = blockIdx.x;
+  const int nrow = KC * ldX;
+  const double* src = Xp + c * (int64_t)nrow;
+  for (int e = threadIdx.x; e < nrow; e += blockDim.x) xs[e] = src[e];
+  __syncthreads();
+  const int PBB = BN / 16, KS = KC / 4, GB_D = KS * PBB * 64;
+  for (int tn = 0; tn < tilesN; ++tn) {
+    double2* dst = reinterpret_cast<double2*>(out + ((int64_t)tn * nchunks + c) * GB_D);
+    for (int v = threadIdx.x; v < GB_D / 2; v += blockDim.x) {
+      const int lane = v & 31, pb = (v >> 5) % PBB, ks = (v >> 5) / PBB;
+      const int i = 4 * ks + (lane & 3);
+      const int c0 = tn * BN + 2 * pb * 8 + (lane >> 2), c1 = c0 + 8;
+      const int a0 = va[c0], b0 = vb[c0], a1 = va[c1], b1 = vb[c1];
+      double2 o;
+      o.x = a0 < 0 ? 0.0 : xs[i * ldX + a0] * xs[i * ldX + b0];
+      o.y = a1 < 0 ? 0.0 : xs[i * ldX + a1] * xs[i * ldX + b1];
+      dst[v] = o;
+    }
+  }
+}
+
+// APRE: J1's A operand (the weights P_k (delta_kl - P_l) of pair row (k, l)) in the kernels'
+// fragment-native order, one CTA per chunk of KC individuals (its probability rows staged once,
+// then every tm block of the chunk written with 16-byte coalesced stores):
+// out[(tm * nchunks + c) * GA_D + ((ks * PBA + pb) * 32 + lane) * 2 + h] = P_ik (delta_kl - P_il),
+//   row = tm * 128 + (2 pb + h) * 8 + lane / 4 -> (k, l) = (ka[row], la[row]),  i = c * KC + 4 ks + lane % 4
+__global__ void __launch_bounds__(256) k_afrag(double* __restrict__ out, int tilesM, int KC, int64_t nchunks,
+                                               const int* __restrict__ ka, const int* __restrict__ la,
+                                               const double* __restrict__ Pr, int ldP) {
+  extern __shared__ __align__(16) double rs[];  // [KC][ldP]
+  const int64_t c = blockIdx.x;
+  const int nrow = KC * ldP;
+  const double* src = Pr + c * (int64_t)nrow;
+  for (int e = threadIdx.x; e < nrow; e += blockDim.x) rs[e] = src[e];
+  __syncthreads();
+  constexpr int PBA = BM / 16;
+  const int KS = KC / 4, GA_D = KS * PBA * 64;
+  for (int tm = 0; tm < tilesM; ++tm) {
+    double2* dst = reinterpret_cast<double2*>(out + ((int64_t)tm * nchunks + c) * GA_D);
+    for (int v = threadIdx.x; v < GA_D / 2; v += blockDim.x) {
+      const int lane = v & 31, pb = (v >> 5) % PBA, ks = (v >> 5) / PBA;
+      const int i = 4 * ks + (lane & 3);
+      double2 o;
+      const int r0 = tm * BM + 2 * pb * 8 + (lane >> 2), r1 = r0 + 8;
+      const int k0 = ka[r0], l0 = la[r0], k1 = ka[r1], l1 = la[r1];
+      o.x = k0 < 0 ? 0.0 : rs[i * ldP + k0] * ((k0 == l0 ? 1.0 : 0.0) - rs[i * ldP + l0]);
+      o.y = k1 < 0 ? 0.0 : rs[i * ldP + k1] * ((k1 == l1 ? 1.0 : 0.0) - rs[i * ldP + l1]);
+      dst[v] = o;
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Pipelined DMMA GEMM over precomputed fragment-native operands (J1 when both A and B are
+// materialised): warp NWARP is the producer (one lane: dynamic item fetch, then per chunk one
+// 32 KB bulk copy of A and of B into an S-stage ring guarded by full/empty mbarriers); warps
+// 0..NWARP-1 only load fragments and issue DMMA. No CTA-wide barrier inside the loop: a stage is
+// refilled as soon as the NWARP consumer warps have released it. Item metadata travels with the
+// stage (written before the producer's release-arrive, read after the consumers' acquire-wait).
+template <int BN, int KC, int S>
+__global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P, const double* __restrict__ afrag) {
+  constexpr int NWARP = 8;
+  constexpr int WARPS_M = (BN == 128) ? 2 : 4, WARPS_N = NWARP / WARPS_M;
+  constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  constexpr int MT = WTM / 8, NTL = WTN / 8;
+  constexpr int KS = KC / 4, PBA = BM / 16, PBB = BN / 16;
+  constexpr int GA_D = KS * PBA * 64, GB_D = KS * PBB * 64;
+  extern __shared__ __align__(128) double sm[];  // [S][GA_D + GB_D]
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  __shared__ int meta_item[S], meta_flags[S];
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int tiles = P.tilesM * P.tilesN, total = tiles * P.splits;
+
+  if (w == NWARP) {  // producer
+    if (lane != 0) return;
+    unsigned s = 0, ph = 0;
+    for (;;) {
+      const int item = (int)atomicAdd(P.counter, 1u);
+      if (item >= total) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        meta_item[s] = -1;
+        mbar_arrive(&full[s]);
+        return;
+      }
+      const int split = item / tiles, t = item - split * tiles;
+      const int tm = t / P.tilesN, tn = t - tm * P.tilesN;
+      const int64_t cb = split * P.nchunks / P.splits, ce = (split + 1) * P.nchunks / P.splits;
+      for (int64_t c = cb; c < ce; ++c) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        meta_item[s] = item;
+        meta_flags[s] = (c == cb ? 1 : 0) | (c + 1 == ce ? 2 : 0);
+        double* st = sm + s * (GA_D + GB_D);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                     "r"((unsigned)((GA_D + GB_D) * 8))
+                     : "memory");
+        bulk_g2s(st, afrag + ((int64_t)tm * P.nchunks + c) * GA_D, GA_D * 8, &full[s]);
+        bulk_g2s(st + GA_D, P.bfrag + ((int64_t)tn * P.nchunks + c) * GB_D, GB_D * 8, &full[s]);
+        if (++s == S) { s = 0; ph ^= 1u; }
+      }
+    }
+  }
+
+  // consumers
+  const int wm = w / WARPS_N, wn = w % WARPS_N;
+  const int r4 = lane & 3, cl = lane >> 2;
+  double acc[MT][NTL][2];
+  unsigned s = 0, ph = 0;
+  for (;;) {
+    mbar_wait(&full[s], ph);
+    const int item = meta_item[s], fl = meta_flags[s];
+    if (item < 0) break;
+    if (fl & 1) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    const double* ga = sm + s * (GA_D + GB_D);
+    const double* gb = ga + GA_D;
+    double af[2][MT], bf[2][NTL];
+    auto load_frags = [&](int buf, int ks) {
+#pragma unroll
+      for (int mp = 0; mp < MT / 2; ++mp) {
+        const double2 v = lds128(ga + 2 * ((ks * PBA + wm * (MT / 2) + mp) * 32 + lane));
+        af[buf][2 * mp] = v.x;
+        af[buf][2 * mp + 1] = v.y;
+      }
+#pragma unroll
+      for (int np = 0; np < NTL / 2; ++np) {
+        const double2 v = lds128(gb + 2 * ((ks * PBB + wn * (NTL / 2) + np) * 32 + lane));
+        bf[buf][2 * np] = v.x;
+        bf[buf][2 * np + 1] = v.y;
+      }
+    };
+    load_frags(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (ks + 1 < KS) load_frags((ks + 1) & 1, ks + 1);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[ks & 1][i], bf[ks & 1][j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) { s = 0; ph ^= 1u; }
+    if (fl & 2) {  // this split's partial tile
+      const int split = item / tiles, t = item - split * tiles;
+      const int tm = t / P.tilesN, tn = t - tm * P.tilesN;
+      double* Cb = P.C + split * P.split_stride;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int64_t row = (int64_t)tm * BM + wm * WTM + i * 8 + cl;
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+          const int col = tn * BN + wn * WTN + j * 8 + 2 * r4;
+          *reinterpret_cast<double2*>(Cb + row * P.ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+      }
+    }
   }
 }
 
@@ -535,6 +704,10 @@ struct GemmJob {
   bool bpre = false;        // B operand precomputed (k_bfrag) instead of generated
   double* bfrag = nullptr;  // [tilesN][nchunks][GB_D]
   int *va = nullptr, *vb = nullptr;  // per B column: vech (a, b), -1 for padding
+  bool apre = false;        // A operand materialised per evaluation (k_afrag) -> k_pipe_gemm
+  bool own_afrag = false;   // false: afrag borrowed from j1 (the tail job)
+  double* afrag = nullptr;  // [tilesM][nchunks][GA_D]
+  int *ka = nullptr, *la = nullptr;  // per A row: pair (k, l), -1 for padding
   bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
   int64_t nchunks;
@@ -560,7 +733,7 @@ struct HessPlan {
   double* Tpart = nullptr;
   double* T = nullptr;
   unsigned* counters = nullptr;  // [2]
-  cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // [7]: before operand prep
   size_t bytes = 0;
   int sms;
 };
@@ -645,13 +818,66 @@ static void free_job(GemmJob& J) {
   cudaFree(J.bfrag);
   cudaFree(J.va);
   cudaFree(J.vb);
-  J.bfrag = nullptr;
-  J.va = J.vb = nullptr;
-  J.bpre = false;
+  if (J.own_afrag) {
+    cudaFree(J.afrag);
+    cudaFree(J.ka);
+    cudaFree(J.la);
+  }
+  J.own_afrag = false;
+  J.bfrag = J.afrag = nullptr;
+  J.va = J.vb = J.ka = J.la = nullptr;
+  J.bpre = J.apre = false;
   cudaFree(J.Cpart);
   cudaFree(J.Cred);
   J.dA = J.dB = nullptr;
   J.Cpart = J.Cred = nullptr;
+}
+
+// Precomputed B fragments of vech columns [col0, col0 + ncols) of the (a <= b) enumeration.
+static bool alloc_bfrag(GemmJob& J, int col0, int ncols, int q, size_t* bytes) {
+  const size_t ncol = (size_t)J.tilesN * J.BN;
+  std::vector<int> va(ncol, -1), vb(ncol, -1);
+  for (int a = 0, v = 0; a < q; ++a)
+    for (int b = a; b < q; ++b, ++v)
+      if (v >= col0 && v < col0 + ncols) { va[v - col0] = a; vb[v - col0] = b; }
+  const size_t nfr = (size_t)J.tilesN * J.nchunks * ((J.KC / 4) * (J.BN / 16) * 64);
+  bool ok = cudaMalloc(&J.bfrag, nfr * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&J.va, ncol * sizeof(int)) == cudaSuccess && cudaMalloc(&J.vb, ncol * sizeof(int)) == cudaSuccess;
+  if (ok) {
+    cudaMemcpy(J.va, va.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(J.vb, vb.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
+    *bytes += nfr * sizeof(double);
+  } else {
+    cudaGetLastError();
+    cudaFree(J.bfrag); cudaFree(J.va); cudaFree(J.vb);
+    J.bfrag = nullptr; J.va = J.vb = nullptr;
+  }
+  return ok;
+}
+
+// Materialised A fragments (pair weights) if they fit with 4 GB to spare; otherwise A stays generated.
+static void alloc_afrag(GemmJob& J, int K, const Packed& pk, size_t* bytes) {
+  const size_t afrag_bytes = (size_t)J.tilesM * BM * (size_t)pk.Npad * sizeof(double);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  if (afrag_bytes > ((size_t)48 << 30) || afrag_bytes + ((size_t)4 << 30) >= free_b) return;
+  const size_t nrow = (size_t)J.tilesM * BM;
+  std::vector<int> ka(nrow, -1), la(nrow, -1);
+  size_t r = 0;
+  for (int k = 1; k < K; ++k)
+    for (int l = k; l < K; ++l, ++r) { ka[r] = k; la[r] = l; }
+  J.apre = cudaMalloc(&J.afrag, afrag_bytes) == cudaSuccess && cudaMalloc(&J.ka, nrow * sizeof(int)) == cudaSuccess &&
+           cudaMalloc(&J.la, nrow * sizeof(int)) == cudaSuccess;
+  if (J.apre) {
+    J.own_afrag = true;
+    cudaMemcpy(J.ka, ka.data(), nrow * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(J.la, la.data(), nrow * sizeof(int), cudaMemcpyHostToDevice);
+    *bytes += afrag_bytes;
+  } else {
+    cudaGetLastError();
+    cudaFree(J.afrag); cudaFree(J.ka); cudaFree(J.la);
+    J.afrag = nullptr; J.ka = J.la = nullptr;
+  }
 }
 
 HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
@@ -689,25 +915,27 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       const int segs_p[1] = {0};
       hp->j1.bpre = want_bpre;
       bool good = setup_job(hp->j1, A, Ba, bn1, KC, pk, want_bpre ? segs_p : segs, want_bpre ? 1 : 2, sms, &bytes);
-      if (good && want_bpre) {
-        GemmJob& J = hp->j1;
-        const size_t ncol = (size_t)J.tilesN * J.BN;
-        std::vector<int> va(ncol, -1), vb(ncol, -1);
-        for (int a = 0, col = 0; a < q; ++a)
-          for (int b = a; b < q; ++b, ++col)
-            if (col < hp->n1a) { va[col] = a; vb[col] = b; }
-        const size_t nfr = (size_t)J.tilesN * J.nchunks * ((KC / 4) * (J.BN / 16) * 64);
-        good = cudaMalloc(&J.bfrag, nfr * sizeof(double)) == cudaSuccess &&
-               cudaMalloc(&J.va, ncol * sizeof(int)) == cudaSuccess &&
-               cudaMalloc(&J.vb, ncol * sizeof(int)) == cudaSuccess;
-        if (good) {
-          cudaMemcpy(J.va, va.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
-          cudaMemcpy(J.vb, vb.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
-          bytes += nfr * sizeof(double);
+      if (good && want_bpre) good = alloc_bfrag(hp->j1, 0, hp->n1a, q, &bytes);
+      // A materialised too (pure pipelined GEMM) when the per-evaluation write of N x 128*tilesM
+      // doubles is small next to the GEMM (~23/vech of it at the measured rates) and fits in HBM
+      if (good && want_bpre && getenv("MNL_NO_APRE") == nullptr && hp->j1.BN == 128 && KC == 32 && hp->n1a >= 512)
+        alloc_afrag(hp->j1, K, pk, &bytes);
+      hp->has_j1b = split;
+      if (good && split) {
+        const int bnt = choose_bn(rem);
+        const bool tail_pipe = hp->j1.apre && bnt == 64;  // the tail reuses j1's materialised weights
+        hp->j1b.bpre = tail_pipe;
+        good = setup_job(hp->j1b, A, Bb, bnt, KC, pk, tail_pipe ? segs_p : segs, tail_pipe ? 1 : 2, sms, &bytes);
+        if (good && tail_pipe) {
+          if (alloc_bfrag(hp->j1b, hp->n1a, nv - hp->n1a, q, &bytes)) {
+            hp->j1b.apre = true;
+            hp->j1b.afrag = hp->j1.afrag;  // borrowed (same pairs, tilesM and chunks)
+          } else {
+            free_job(hp->j1b);
+            good = setup_job(hp->j1b, A, Bb, bnt, KC, pk, segs, 2, sms, &bytes);
+          }
         }
       }
-      hp->has_j1b = split;
-      if (good && split) good = setup_job(hp->j1b, A, Bb, choose_bn(rem), KC, pk, segs, 2, sms, &bytes);
       if (good) break;
       free_job(hp->j1);
       free_job(hp->j1b);
@@ -818,10 +1046,39 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   return cudaGetLastError();
 }
 
+template <int BN>
+static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaStream_t st) {
+  constexpr int KC = 32, S = BN == 128 ? 3 : 4;
+  constexpr size_t smem = (size_t)S * (KC / 4) * (BM / 16 + BN / 16) * 64 * sizeof(double);
+  GemmParams P{};
+  P.tilesM = J.tilesM;
+  P.tilesN = J.tilesN;
+  P.splits = J.splits;
+  P.nchunks = J.nchunks;
+  P.C = J.Cpart;
+  P.ldc = J.ldc;
+  P.split_stride = J.split_stride;
+  P.bfrag = J.bfrag;
+  P.counter = counter;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_pipe_gemm<BN, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = J.tilesM * J.tilesN * J.splits;
+  cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+  k_pipe_gemm<BN, KC, S><<<std::min(items, sms), 8 * 32 + 32, smem, st>>>(P, J.afrag);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
                            cudaEvent_t after_gemm = nullptr) {
   cudaError_t e;
-  if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
+  if (J.apre) {
+    e = J.BN == 128 ? run_pipe<128>(J, counter, sms, st) : run_pipe<64>(J, counter, sms, st);
+  } else if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
     if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 4, true>(J, pk, counter, sms, st);
     else if (J.nwarp == 16) e = J.KC == 32 ? run_gemm<128, 32, 16, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 16, true>(J, pk, counter, sms, st);
     else if (J.BN == 128 && J.bpre) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
@@ -846,12 +1103,27 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
 
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y, double* out,
                            int ld_out, double sign, cudaStream_t st) {
+  cudaEventRecord(hp->ev[7], st);
   if (hp->j1.bpre && !hp->bvalid) {  // once per design (the packed rows changed)
     const GemmJob& J = hp->j1;
     const int64_t total = (int64_t)J.tilesN * J.nchunks * ((J.KC / 4) * (J.BN / 16) * 64);
-    k_bfrag<<<148 * 8, 256, 0, st>>>(J.bfrag, total, J.BN, J.KC, J.nchunks, J.va, J.vb, pk.Xp, pk.ldX);
+    (void)total;
+    k_bfrag<<<(unsigned)J.nchunks, 256, (size_t)J.KC * pk.ldX * sizeof(double), st>>>(J.bfrag, J.tilesN, J.BN, J.KC,
+                                                                                     J.nchunks, J.va, J.vb, pk.Xp, pk.ldX);
     count_launch();
+    if (hp->has_j1b && hp->j1b.bpre) {
+      const GemmJob& T = hp->j1b;
+      k_bfrag<<<(unsigned)T.nchunks, 256, (size_t)T.KC * pk.ldX * sizeof(double), st>>>(T.bfrag, T.tilesN, T.BN, T.KC,
+                                                                                       T.nchunks, T.va, T.vb, pk.Xp, pk.ldX);
+      count_launch();
+    }
     hp->bvalid = true;
+  }
+  if (hp->j1.apre) {  // every evaluation (the weights depend on the probabilities)
+    const GemmJob& J = hp->j1;
+    k_afrag<<<(unsigned)J.nchunks, 256, (size_t)J.KC * pk.ldP * sizeof(double), st>>>(J.afrag, J.tilesM, J.KC, J.nchunks,
+                                                                                     J.ka, J.la, pk.Pr, pk.ldP);
+    count_launch();
   }
   cudaEventRecord(hp->ev[0], st);
   cudaError_t e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
@@ -912,12 +1184,15 @@ void hess_plan_design_changed(HessPlan* hp) {
   if (hp) hp->bvalid = false;
 }
 
-void hess_last_times(HessPlan* hp, double out[6]) {
+void hess_last_times(HessPlan* hp, double out[7]) {
   // [0] J1 GEMM (128-column tiles), [1] its split reduction, [2] J1 tail GEMM (narrow tile),
-  // [3] its reduction, [4] Z/Y blocks (J2 + same-alternative), [5] assembly
-  for (int i = 0; i < 6; ++i) {
+  // [3] its reduction, [4] Z/Y blocks (J2 + same-alternative), [5] assembly,
+  // [6] operand materialisation before J1 (k_afrag every evaluation, k_bfrag once per design)
+  for (int i = 0; i < 7; ++i) {
     float ms = 0.f;
-    if (!hp || cudaEventElapsedTime(&ms, hp->ev[i], hp->ev[i + 1]) != cudaSuccess) ms = 0.f;
+    if (!hp) { out[i] = 0.0; continue; }
+    cudaEvent_t a = i < 6 ? hp->ev[i] : hp->ev[7], b = i < 6 ? hp->ev[i + 1] : hp->ev[0];
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) ms = 0.f;
     out[i] = ms;
   }
 }

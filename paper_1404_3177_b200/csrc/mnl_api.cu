@@ -240,7 +240,7 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
     S.hess_ms += elapsed(ev[0], ev[1]);
     S.chol_ms += elapsed(ev[1], ev[2]);
     {
-      double ht[6];
+      double ht[7];
       hess_last_times(hp, ht);
       S.gemm_ms += ht[0] + ht[2];  // the beta-beta GEMM: whole tiles + narrow tail
     }
@@ -311,7 +311,7 @@ const char* mnl_status_string(int code) {
 
 int64_t mnl_last_launch_count(void) { return g_launches; }
 
-int mnl_last_hessian_times(double out[6]) {
+int mnl_last_hessian_times(double out[7]) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!out) return MNL_ERR_ARG;
   hess_last_times(g_ws.hp, out);

@@ -57,7 +57,7 @@ def gpu_row(cfg, reps=5):
         torch.cuda.synchronize()
         ev.append(e0.elapsed_time(e1))
         t = M.last_hessian_times()
-        hs.append(t["j1_gemm"] + t["j1_reduce"] + t["j1_tail"] + t["j1_tail_reduce"] + t["j2_and_arrow"] + t["assemble"])
+        hs.append(t["j1_gemm"] + t["j1_reduce"] + t["j1_tail"] + t["j1_tail_reduce"] + t["j2_and_arrow"] + t["assemble"] + t["j1_operands"])
     p1, hs, ev = [statistics.median(x[2:]) for x in (p1, hs, ev)]
     M.mnl_newton_fit(dp, tol=1e-6)  # warm-up
     fits = []
