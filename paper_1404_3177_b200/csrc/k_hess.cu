@@ -327,62 +327,69 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
   }
 }
 
-// BPRE: J1's B operand (x~_a x~_b for the tile's vech columns) in the kernels' fragment-native
-// order, one CTA per chunk of KC individuals (design rows staged once, all tn blocks written):
-// out[(tn * nchunks + c) * GB_D + ((ks * PBB + pb) * 32 + lane) * 2 + h] =
-//   Xp[i][a(col)] * Xp[i][b(col)],  col = tn * BN + (2 pb + h) * 8 + lane / 4,  i = c * KC + 4 ks + lane % 4
-__global__ void __launch_bounds__(256) k_bfrag(double* __restrict__ out, int tilesN, int BN, int KC, int64_t nchunks,
-                                               const int* __restrict__ va, const int* __restrict__ vb,
-                                               const double* __restrict__ Xp, int ldX) {
-  extern __shared__ __align__(16) double xs[];  // [KC][ldX]
-  const int64_t c = blockIdx.x;
-  const int nrow = KC * ldX;
-  const double* src = Xp + c * (int64_t)nrow;
-  for (int e = threadIdx.x; e < nrow; e += blockDim.x) xs[e] = src[e];
-  __syncthreads();
-  const int PBB = BN / 16, KS = KC / 4, GB_D = KS * PBB * 64;
-  for (int tn = 0; tn < tilesN; ++tn) {
-    double2* dst = reinterpret_cast<double2*>(out + ((int64_t)tn * nchunks + c) * GB_D);
-    for (int v = threadIdx.x; v < GB_D / 2; v += blockDim.x) {
-      const int lane = v & 31, pb = (v >> 5) % PBB, ks = (v >> 5) / PBB;
-      const int i = 4 * ks + (lane & 3);
-      const int c0 = tn * BN + 2 * pb * 8 + (lane >> 2), c1 = c0 + 8;
-      const int a0 = va[c0], b0 = vb[c0], a1 = va[c1], b1 = vb[c1];
-      double2 o;
-      o.x = a0 < 0 ? 0.0 : xs[i * ldX + a0] * xs[i * ldX + b0];
-      o.y = a1 < 0 ? 0.0 : xs[i * ldX + a1] * xs[i * ldX + b1];
-      dst[v] = o;
-    }
-  }
+// Operand materialisation: the generated columns of one GEMM operand written once to HBM in the
+// GEMM kernels' fragment-native order, one CTA per chunk of KC individuals (the chunk's rows of the
+// descriptor segments staged once in shared memory, then every tile of the operand written with
+// 16-byte coalesced stores). Same arithmetic as the in-kernel generator (k_gen_gemm):
+// out[(t * nchunks + c) * GD + ((ks * PB + pb) * 32 + lane) * 2 + h] = R[o1] * fma(s, R[o2], c0) of
+//   column t * BT + (2 pb + h) * 8 + lane / 4 at individual c * KC + 4 ks + lane % 4   (GD = KS * PB * 64).
+struct FragArgs {
+  const ColDesc* desc;
+  double* out;
+  int tiles, BT, KC;
+  int64_t nchunks;
+  int nseg;
+  const double* seg_ptr[3];
+  int seg_ld[3];
+  int seg_off[3];
+  int nh;  // CTAs per chunk (1, or 2 when the chunk's rows need > 48 KB of shared memory)
+};
+
+// offset into a KC-row stage -> offset into the KC/2-row stage (segment bases halve; the in-row
+// column offset stays)
+__device__ __forceinline__ int rebase(const FragArgs& F, int o) {
+  int sg = 0;
+#pragma unroll
+  for (int t = 1; t < 3; ++t)
+    if (t < F.nseg && o >= F.seg_off[t]) sg = t;
+  const int base = sg == 0 ? F.seg_off[0] : (sg == 1 ? F.seg_off[1] : F.seg_off[2]);
+  return base / F.nh + (o - base);
 }
 
-// APRE: J1's A operand (the weights P_k (delta_kl - P_l) of pair row (k, l)) in the kernels'
-// fragment-native order, one CTA per chunk of KC individuals (its probability rows staged once,
-// then every tm block of the chunk written with 16-byte coalesced stores):
-// out[(tm * nchunks + c) * GA_D + ((ks * PBA + pb) * 32 + lane) * 2 + h] = P_ik (delta_kl - P_il),
-//   row = tm * 128 + (2 pb + h) * 8 + lane / 4 -> (k, l) = (ka[row], la[row]),  i = c * KC + 4 ks + lane % 4
-__global__ void __launch_bounds__(256) k_afrag(double* __restrict__ out, int tilesM, int KC, int64_t nchunks,
-                                               const int* __restrict__ ka, const int* __restrict__ la,
-                                               const double* __restrict__ Pr, int ldP) {
-  extern __shared__ __align__(16) double rs[];  // [KC][ldP]
-  const int64_t c = blockIdx.x;
-  const int nrow = KC * ldP;
-  const double* src = Pr + c * (int64_t)nrow;
-  for (int e = threadIdx.x; e < nrow; e += blockDim.x) rs[e] = src[e];
+__global__ void __launch_bounds__(256) k_frag(const FragArgs F) {
+  // CTA = (chunk c, part h < nh): rows c * KC + h * KC / nh + [0, KC / nh), k-slices [h KS/nh, (h+1) KS/nh)
+  extern __shared__ __align__(16) double rs[];
+  const int64_t c = blockIdx.x / F.nh;
+  const int h = blockIdx.x - (int)c * F.nh, RH = F.KC / F.nh;
+#pragma unroll
+  for (int sg = 0; sg < 3; ++sg) {
+    if (sg >= F.nseg) break;
+    const int n2 = RH * F.seg_ld[sg] / 2;  // leading dimensions are even
+    const double2* src =
+        reinterpret_cast<const double2*>(F.seg_ptr[sg] + (c * F.KC + h * RH) * (int64_t)F.seg_ld[sg]);
+    double2* dst = reinterpret_cast<double2*>(rs + F.seg_off[sg] / F.nh);  // seg_off: offsets for KC rows
+    for (int e = threadIdx.x; e < n2; e += blockDim.x) dst[e] = src[e];
+  }
   __syncthreads();
-  constexpr int PBA = BM / 16;
-  const int KS = KC / 4, GA_D = KS * PBA * 64;
-  for (int tm = 0; tm < tilesM; ++tm) {
-    double2* dst = reinterpret_cast<double2*>(out + ((int64_t)tm * nchunks + c) * GA_D);
-    for (int v = threadIdx.x; v < GA_D / 2; v += blockDim.x) {
-      const int lane = v & 31, pb = (v >> 5) % PBA, ks = (v >> 5) / PBA;
-      const int i = 4 * ks + (lane & 3);
+  // one thread per (tile, pair-block, lane): its two columns' descriptors stay in registers over
+  // the k-slices; for each k-slice a warp stores 512 contiguous bytes. Descriptor offsets assume
+  // KC staged rows per segment (seg_off = KC * preceding lds): rebase to the half-size stage.
+  const int PB = F.BT / 16, KS = F.KC / 4, W = PB * 32;
+  for (int w = threadIdx.x; w < F.tiles * W; w += blockDim.x) {
+    const int t = w / W, r = w - t * W, lane = r & 31;
+    const int col = t * F.BT + (r >> 5) * 16 + (lane >> 2);
+    ColDesc d0 = F.desc[col], d1 = F.desc[col + 8];
+    d0.o1 = rebase(F, d0.o1); d0.o2 = rebase(F, d0.o2);
+    d1.o1 = rebase(F, d1.o1); d1.o2 = rebase(F, d1.o2);
+    const int i0 = lane & 3;
+    double2* dst = reinterpret_cast<double2*>(F.out + ((int64_t)t * F.nchunks + c) * (KS * W * 2)) + r;
+#pragma unroll 4
+    for (int kq = 0; kq < KS / F.nh; ++kq) {
+      const int i = 4 * kq + i0, ks = h * (KS / F.nh) + kq;
       double2 o;
-      const int r0 = tm * BM + 2 * pb * 8 + (lane >> 2), r1 = r0 + 8;
-      const int k0 = ka[r0], l0 = la[r0], k1 = ka[r1], l1 = la[r1];
-      o.x = k0 < 0 ? 0.0 : rs[i * ldP + k0] * ((k0 == l0 ? 1.0 : 0.0) - rs[i * ldP + l0]);
-      o.y = k1 < 0 ? 0.0 : rs[i * ldP + k1] * ((k1 == l1 ? 1.0 : 0.0) - rs[i * ldP + l1]);
-      dst[v] = o;
+      o.x = rs[d0.o1 + i * d0.ld1] * fma(d0.s, rs[d0.o2 + i * d0.ld2], d0.c0);
+      o.y = rs[d1.o1 + i * d1.ld1] * fma(d1.s, rs[d1.o2 + i * d1.ld2], d1.c0);
+      dst[ks * W] = o;
     }
   }
 }
@@ -405,8 +412,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // stage (written before the producer's release-arrive, read after the consumers' acquire-wait).
 template <int BN, int KC, int S>
 __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P, const double* __restrict__ afrag) {
+  // 128 -> 2x4 warps of 64x32; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32; 48 -> 8x1 of 16x48
   constexpr int NWARP = 8;
-  constexpr int WARPS_M = (BN == 128) ? 2 : 4, WARPS_N = NWARP / WARPS_M;
+  constexpr int WARPS_M = (BN == 128) ? 2 : (BN == 48 ? 8 : 4), WARPS_N = NWARP / WARPS_M;
   constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   constexpr int MT = WTM / 8, NTL = WTN / 8;
   constexpr int KS = KC / 4, PBA = BM / 16, PBB = BN / 16;
@@ -701,13 +709,14 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
 
 struct GemmJob {
   int BN, KC, nwarp = 8, nraw = 2;
-  bool bpre = false;        // B operand precomputed (k_bfrag) instead of generated
-  double* bfrag = nullptr;  // [tilesN][nchunks][GB_D]
-  int *va = nullptr, *vb = nullptr;  // per B column: vech (a, b), -1 for padding
-  bool apre = false;        // A operand materialised per evaluation (k_afrag) -> k_pipe_gemm
-  bool own_afrag = false;   // false: afrag borrowed from j1 (the tail job)
+  // Operand materialisation (k_frag): mat_b alone -> k_gen_gemm<..., BPRE> generates only A;
+  // mat_a && mat_b -> k_pipe_gemm (pure TMA/mbarrier pipeline). b_design: B depends only on the
+  // packed design rows (J1's x~_a x~_b), so it is rebuilt only after a re-pack.
+  bool mat_a = false, mat_b = false, b_design = false;
+  bool own_afrag = true;   // false: afrag borrowed from j1 (the J1 tail job shares j1's weights)
   double* afrag = nullptr;  // [tilesM][nchunks][GA_D]
-  int *ka = nullptr, *la = nullptr;  // per A row: pair (k, l), -1 for padding
+  double* bfrag = nullptr;  // [tilesN][nchunks][GB_D]
+  int dnseg = 0, dseg_id[3] = {0, 0, 0};  // stage layout the descriptors were built against
   bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
   int64_t nchunks;
@@ -737,6 +746,8 @@ struct HessPlan {
   size_t bytes = 0;
   int sms;
 };
+
+constexpr size_t kFragSmemMax = 220 * 1024;  // k_frag's staged rows
 
 static int choose_splits(int tiles, int64_t nchunks, int sms, int min_chunks) {
   int best = 1;
@@ -768,7 +779,8 @@ static int choose_bn(int MB) {
 }
 
 static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vector<ColDesc>& B, int BN,
-                      int KC, const Packed& pk, const int* segs, int nseg, int sms, size_t* bytes) {
+                      int KC, const Packed& pk, const int* segs, int nseg, int sms, size_t* bytes,
+                      bool pipe = false) {
   J.BN = BN;
   J.KC = KC;
   J.nwarp = (BN == 64 && getenv("MNL_J1_NWARP4")) ? 4 : 8;  // experiments: two 4-warp CTAs per SM
@@ -802,6 +814,7 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   if (cudaMalloc(&J.Cpart, cbytes * J.splits) != cudaSuccess) return false;
   if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
   *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
+  if (pipe) return true;  // k_pipe_gemm: no generator staging
   const size_t lim = J.nwarp == 4 ? 112 * 1024 : 220 * 1024;
   for (J.nraw = 2; J.nraw >= 1; --J.nraw) {  // prefer two raw stages; one if the stage is large
     J.smem = (size_t)(2 * (KC / 4) * 8 * 64 + 2 * (KC / 4) * (BN / 16) * 64 + J.nraw * J.stage_doubles) *
@@ -816,68 +829,43 @@ static void free_job(GemmJob& J) {
   cudaFree(J.dA);
   cudaFree(J.dB);
   cudaFree(J.bfrag);
-  cudaFree(J.va);
-  cudaFree(J.vb);
-  if (J.own_afrag) {
-    cudaFree(J.afrag);
-    cudaFree(J.ka);
-    cudaFree(J.la);
-  }
-  J.own_afrag = false;
-  J.bfrag = J.afrag = nullptr;
-  J.va = J.vb = J.ka = J.la = nullptr;
-  J.bpre = J.apre = false;
+  if (J.own_afrag) cudaFree(J.afrag);
+  J.own_afrag = true;
+  J.afrag = J.bfrag = nullptr;
+  J.mat_a = J.mat_b = J.b_design = false;
   cudaFree(J.Cpart);
   cudaFree(J.Cred);
   J.dA = J.dB = nullptr;
   J.Cpart = J.Cred = nullptr;
 }
 
-// Precomputed B fragments of vech columns [col0, col0 + ncols) of the (a <= b) enumeration.
-static bool alloc_bfrag(GemmJob& J, int col0, int ncols, int q, size_t* bytes) {
-  const size_t ncol = (size_t)J.tilesN * J.BN;
-  std::vector<int> va(ncol, -1), vb(ncol, -1);
-  for (int a = 0, v = 0; a < q; ++a)
-    for (int b = a; b < q; ++b, ++v)
-      if (v >= col0 && v < col0 + ncols) { va[v - col0] = a; vb[v - col0] = b; }
-  const size_t nfr = (size_t)J.tilesN * J.nchunks * ((J.KC / 4) * (J.BN / 16) * 64);
-  bool ok = cudaMalloc(&J.bfrag, nfr * sizeof(double)) == cudaSuccess &&
-            cudaMalloc(&J.va, ncol * sizeof(int)) == cudaSuccess && cudaMalloc(&J.vb, ncol * sizeof(int)) == cudaSuccess;
-  if (ok) {
-    cudaMemcpy(J.va, va.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
-    cudaMemcpy(J.vb, vb.data(), ncol * sizeof(int), cudaMemcpyHostToDevice);
-    *bytes += nfr * sizeof(double);
-  } else {
-    cudaGetLastError();
-    cudaFree(J.bfrag); cudaFree(J.va); cudaFree(J.vb);
-    J.bfrag = nullptr; J.va = J.vb = nullptr;
-  }
-  return ok;
-}
-
-// Materialised A fragments (pair weights) if they fit with 4 GB to spare; otherwise A stays generated.
-static void alloc_afrag(GemmJob& J, int K, const Packed& pk, size_t* bytes) {
-  const size_t afrag_bytes = (size_t)J.tilesM * BM * (size_t)pk.Npad * sizeof(double);
+// Fragment buffer of `tiles` operand tiles (128 rows for A, BN for B) over all chunks, if it fits
+// with 4 GB of HBM to spare (otherwise the operand stays generated in-kernel).
+static double* alloc_frag(int tiles, int width, const Packed& pk, size_t* bytes) {
+  const size_t fb = (size_t)tiles * width * (size_t)pk.Npad * sizeof(double);
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  if (afrag_bytes > ((size_t)48 << 30) || afrag_bytes + ((size_t)4 << 30) >= free_b) return;
-  const size_t nrow = (size_t)J.tilesM * BM;
-  std::vector<int> ka(nrow, -1), la(nrow, -1);
-  size_t r = 0;
-  for (int k = 1; k < K; ++k)
-    for (int l = k; l < K; ++l, ++r) { ka[r] = k; la[r] = l; }
-  J.apre = cudaMalloc(&J.afrag, afrag_bytes) == cudaSuccess && cudaMalloc(&J.ka, nrow * sizeof(int)) == cudaSuccess &&
-           cudaMalloc(&J.la, nrow * sizeof(int)) == cudaSuccess;
-  if (J.apre) {
-    J.own_afrag = true;
-    cudaMemcpy(J.ka, ka.data(), nrow * sizeof(int), cudaMemcpyHostToDevice);
-    cudaMemcpy(J.la, la.data(), nrow * sizeof(int), cudaMemcpyHostToDevice);
-    *bytes += afrag_bytes;
-  } else {
+  if (getenv("MNL_NO_MATERIALISE") || fb > ((size_t)48 << 30) || fb + ((size_t)4 << 30) >= free_b) return nullptr;
+  double* p = nullptr;
+  if (cudaMalloc(&p, fb) != cudaSuccess) {
     cudaGetLastError();
-    cudaFree(J.afrag); cudaFree(J.ka); cudaFree(J.la);
-    J.afrag = nullptr; J.ka = J.la = nullptr;
+    return nullptr;
   }
+  *bytes += fb;
+  return p;
+}
+
+// Tile widths k_pipe_gemm is instantiated for: the widest of {128, 96, 64, 48} within 5% of the
+// smallest padded width.
+static int choose_bn_pipe(int MB) {
+  int64_t min_pad = -1;
+  for (int bn : {128, 96, 64, 48}) {
+    const int64_t pad = (int64_t)(MB + bn - 1) / bn * bn;
+    if (min_pad < 0 || pad < min_pad) min_pad = pad;
+  }
+  for (int bn : {128, 96, 64, 48})
+    if ((double)((MB + bn - 1) / bn * bn) <= 1.05 * (double)min_pad) return bn;
+  return 48;
 }
 
 HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
@@ -900,41 +888,52 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
         for (int b = a; b < q; ++b) B.push_back(ColDesc{offX + a, pk.ldX, offX + b, pk.ldX, 0.0, 1.0});
       // padding columns point at Xp[.][0] (finite) with c0 = s = 0
       // Split the vech columns: whole 128-column tiles in j1, a narrow remainder job j1b (its own
-      // 64/96/128 width) instead of padding the last tile (c4: 1326 = 10 x 128 + 46).
+      // width) instead of padding the last tile (c4: 1326 = 10 x 128 + 46).
       const int nv = (int)B.size(), rem = nv % 128;
       const bool split = nv > 128 && rem > 0 && rem <= 96;
       hp->n1a = split ? nv - rem : nv;
       std::vector<ColDesc> Ba(B.begin(), B.begin() + hp->n1a), Bb(B.begin() + hp->n1a, B.end());
-      // B of the main job precomputed once per design if it fits comfortably in HBM
-      const int bn1 = split ? 128 : choose_bn(nv);
-      const size_t bfrag_bytes = (size_t)((hp->n1a + bn1 - 1) / bn1) * bn1 * (size_t)pk.Npad * sizeof(double);
-      size_t free_b = 0, total_b = 0;
-      cudaMemGetInfo(&free_b, &total_b);
-      const bool want_bpre = getenv("MNL_NO_BPRE") == nullptr && bfrag_bytes <= (size_t)32 << 30 &&
-                             bfrag_bytes + ((size_t)4 << 30) < free_b;
-      const int segs_p[1] = {0};
-      hp->j1.bpre = want_bpre;
-      bool good = setup_job(hp->j1, A, Ba, bn1, KC, pk, want_bpre ? segs_p : segs, want_bpre ? 1 : 2, sms, &bytes);
-      if (good && want_bpre) good = alloc_bfrag(hp->j1, 0, hp->n1a, q, &bytes);
-      // A materialised too (pure pipelined GEMM) when the per-evaluation write of N x 128*tilesM
-      // doubles is small next to the GEMM (~23/vech of it at the measured rates) and fits in HBM
-      if (good && want_bpre && getenv("MNL_NO_APRE") == nullptr && hp->j1.BN == 128 && KC == 32 && hp->n1a >= 512)
-        alloc_afrag(hp->j1, K, pk, &bytes);
+      const bool frag_fits = (size_t)KC * (pk.ldP + pk.ldX) * sizeof(double) <= kFragSmemMax;
+      // Materialise both operands (k_pipe_gemm) when the per-evaluation write of the weights
+      // (8 N 128 tilesM bytes) is small next to the GEMM (~23/vech of it at the measured rates):
+      // vech >= 256. Otherwise materialise only the design-only B (once per design) if it fits.
+      GemmJob& J = hp->j1;
+      const int tilesM = (int)((A.size() + BM - 1) / BM);
+      double* af = (KC == 32 && nv >= 256 && frag_fits && !getenv("MNL_NO_PIPE")) ? alloc_frag(tilesM, BM, pk, &bytes) : nullptr;
+      int bn1 = split ? 128 : (af ? choose_bn_pipe(nv) : choose_bn(nv));
+      double* bf = frag_fits ? alloc_frag((hp->n1a + bn1 - 1) / bn1, bn1, pk, &bytes) : nullptr;
+      if (af && !bf) {
+        cudaFree(af);
+        af = nullptr;
+        if (!split) bn1 = choose_bn(nv);
+      }
+      J.afrag = af;
+      J.bfrag = bf;
+      J.own_afrag = true;
+      J.mat_a = af != nullptr;
+      J.mat_b = bf != nullptr;
+      J.b_design = true;
+      J.dnseg = 2;
+      J.dseg_id[0] = 0;
+      J.dseg_id[1] = 1;
+      const int segs_p[1] = {0};  // k_gen_gemm<..., BPRE> stages only the probabilities
+      const bool bonly = J.mat_b && !J.mat_a;
+      bool good = setup_job(J, A, Ba, bn1, KC, pk, bonly ? segs_p : segs, bonly ? 1 : 2, sms, &bytes, J.mat_a);
       hp->has_j1b = split;
       if (good && split) {
-        const int bnt = choose_bn(rem);
-        const bool tail_pipe = hp->j1.apre && bnt == 64;  // the tail reuses j1's materialised weights
-        hp->j1b.bpre = tail_pipe;
-        good = setup_job(hp->j1b, A, Bb, bnt, KC, pk, tail_pipe ? segs_p : segs, tail_pipe ? 1 : 2, sms, &bytes);
-        if (good && tail_pipe) {
-          if (alloc_bfrag(hp->j1b, hp->n1a, nv - hp->n1a, q, &bytes)) {
-            hp->j1b.apre = true;
-            hp->j1b.afrag = hp->j1.afrag;  // borrowed (same pairs, tilesM and chunks)
-          } else {
-            free_job(hp->j1b);
-            good = setup_job(hp->j1b, A, Bb, bnt, KC, pk, segs, 2, sms, &bytes);
-          }
-        }
+        GemmJob& T = hp->j1b;
+        int bnt = J.mat_a ? choose_bn_pipe(rem) : choose_bn(rem);
+        double* tbf = J.mat_a ? alloc_frag(1, bnt, pk, &bytes) : nullptr;  // the tail shares j1's weights
+        if (J.mat_a && !tbf) bnt = choose_bn(rem);
+        T.bfrag = tbf;
+        T.afrag = tbf ? J.afrag : nullptr;
+        T.own_afrag = tbf == nullptr;
+        T.mat_a = T.mat_b = tbf != nullptr;
+        T.b_design = true;
+        T.dnseg = 2;
+        T.dseg_id[0] = 0;
+        T.dseg_id[1] = 1;
+        good = setup_job(T, A, Bb, bnt, KC, pk, segs, 2, sms, &bytes, T.mat_a);
       }
       if (good) break;
       free_job(hp->j1);
@@ -958,7 +957,28 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       A.insert(A.end(), AG.begin(), AG.end());
       B = AG;
       hp->j2.agen = false;
-      if (setup_job(hp->j2, A, B, choose_bn((int)B.size()), KC, pk, segs, nseg, sms, &bytes)) break;
+      // both operands depend on the probabilities: materialised per evaluation when the write
+      // (8 N (MA + MB) bytes) is small next to the GEMM (23 (1/MA + 1/MB) of it): MB >= 192, MA >= 512
+      GemmJob& J = hp->j2;
+      const int MA = (int)A.size(), MB = (int)B.size();
+      const bool frag_fits = (size_t)KC * (pk.ldP + pk.ldX + (d > 0 ? pk.ldZ : 0)) * sizeof(double) <= kFragSmemMax;
+      int bn2 = choose_bn(MB);
+      if (KC == 32 && MB >= 192 && MA >= 512 && frag_fits && !getenv("MNL_NO_PIPE")) {
+        const int bnp = choose_bn_pipe(MB);
+        J.afrag = alloc_frag((MA + BM - 1) / BM, BM, pk, &bytes);
+        J.bfrag = J.afrag ? alloc_frag((MB + bnp - 1) / bnp, bnp, pk, &bytes) : nullptr;
+        if (J.afrag && !J.bfrag) {
+          cudaFree(J.afrag);
+          J.afrag = nullptr;
+        }
+        if (J.bfrag) bn2 = bnp;
+      }
+      J.own_afrag = true;
+      J.mat_a = J.mat_b = J.bfrag != nullptr;
+      J.b_design = false;
+      J.dnseg = nseg;
+      for (int sg = 0; sg < 3; ++sg) J.dseg_id[sg] = segs[sg];
+      if (setup_job(J, A, B, bn2, KC, pk, segs, nseg, sms, &bytes, J.mat_a)) break;
       free_job(hp->j2);
       if (KC == 16) ok = false;
     }
@@ -1048,7 +1068,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
 
 template <int BN>
 static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaStream_t st) {
-  constexpr int KC = 32, S = BN == 128 ? 3 : 4;
+  constexpr int KC = 32, S = (200 * 1024) / ((KC / 4) * (BM / 16 + BN / 16) * 64 * 8);  // stages in ~200 KB
   constexpr size_t smem = (size_t)S * (KC / 4) * (BM / 16 + BN / 16) * 64 * sizeof(double);
   GemmParams P{};
   P.tilesM = J.tilesM;
@@ -1076,16 +1096,19 @@ static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaSt
 static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
                            cudaEvent_t after_gemm = nullptr) {
   cudaError_t e;
-  if (J.apre) {
-    e = J.BN == 128 ? run_pipe<128>(J, counter, sms, st) : run_pipe<64>(J, counter, sms, st);
+  if (J.mat_a) {
+    if (J.BN == 128) e = run_pipe<128>(J, counter, sms, st);
+    else if (J.BN == 96) e = run_pipe<96>(J, counter, sms, st);
+    else if (J.BN == 64) e = run_pipe<64>(J, counter, sms, st);
+    else e = run_pipe<48>(J, counter, sms, st);
   } else if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
     if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 4, true>(J, pk, counter, sms, st);
     else if (J.nwarp == 16) e = J.KC == 32 ? run_gemm<128, 32, 16, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 16, true>(J, pk, counter, sms, st);
-    else if (J.BN == 128 && J.bpre) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
+    else if (J.BN == 128 && J.mat_b) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true>(J, pk, counter, sms, st);
-    else if (J.BN == 96 && J.bpre) e = J.KC == 32 ? run_gemm<96, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true, true>(J, pk, counter, sms, st);
+    else if (J.BN == 96 && J.mat_b) e = J.KC == 32 ? run_gemm<96, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true>(J, pk, counter, sms, st);
-    else if (J.bpre) e = J.KC == 32 ? run_gemm<64, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true, true>(J, pk, counter, sms, st);
+    else if (J.mat_b) e = J.KC == 32 ? run_gemm<64, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true, true>(J, pk, counter, sms, st);
     else e = J.KC == 32 ? run_gemm<64, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, true>(J, pk, counter, sms, st);
   } else {  // J2: U^T U, plain products
     if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, false>(J, pk, counter, sms, st);
@@ -1101,29 +1124,46 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
   return cudaGetLastError();
 }
 
+static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStream_t st) {
+  FragArgs F;
+  F.desc = a_side ? J.dA : J.dB;
+  F.out = a_side ? J.afrag : J.bfrag;
+  F.tiles = a_side ? J.tilesM : J.tilesN;
+  F.BT = a_side ? BM : J.BN;
+  F.KC = J.KC;
+  F.nchunks = J.nchunks;
+  F.nseg = J.dnseg;
+  int off = 0;
+  for (int sg = 0; sg < J.dnseg; ++sg) {
+    const int id = J.dseg_id[sg];
+    F.seg_ptr[sg] = id == 0 ? pk.Pr : (id == 1 ? pk.Xp : pk.Zp);
+    F.seg_ld[sg] = id == 0 ? pk.ldP : (id == 1 ? pk.ldX : pk.ldZ);
+    F.seg_off[sg] = off;
+    off += J.KC * F.seg_ld[sg];
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFragSmemMax);
+    attr = true;
+  }
+  F.nh = (size_t)off * sizeof(double) > 48 * 1024 ? 2 : 1;
+  k_frag<<<(unsigned)(F.nh * J.nchunks), 256, (size_t)off / F.nh * sizeof(double), st>>>(F);
+  count_launch();
+}
+
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y, double* out,
                            int ld_out, double sign, cudaStream_t st) {
   cudaEventRecord(hp->ev[7], st);
-  if (hp->j1.bpre && !hp->bvalid) {  // once per design (the packed rows changed)
-    const GemmJob& J = hp->j1;
-    const int64_t total = (int64_t)J.tilesN * J.nchunks * ((J.KC / 4) * (J.BN / 16) * 64);
-    (void)total;
-    k_bfrag<<<(unsigned)J.nchunks, 256, (size_t)J.KC * pk.ldX * sizeof(double), st>>>(J.bfrag, J.tilesN, J.BN, J.KC,
-                                                                                     J.nchunks, J.va, J.vb, pk.Xp, pk.ldX);
-    count_launch();
-    if (hp->has_j1b && hp->j1b.bpre) {
-      const GemmJob& T = hp->j1b;
-      k_bfrag<<<(unsigned)T.nchunks, 256, (size_t)T.KC * pk.ldX * sizeof(double), st>>>(T.bfrag, T.tilesN, T.BN, T.KC,
-                                                                                       T.nchunks, T.va, T.vb, pk.Xp, pk.ldX);
-      count_launch();
+  {  // operand materialisation: weights every evaluation, design-only products after a re-pack
+    const GemmJob* jobs[3] = {&hp->j1, hp->has_j1b ? &hp->j1b : nullptr, hp->has_j2 ? &hp->j2 : nullptr};
+    for (const GemmJob* J : jobs) {
+      if (!J) continue;
+      if (J->mat_b && (!J->b_design || !hp->bvalid)) launch_frag(*J, pk, false, st);
+      if (J->mat_a && J->own_afrag) launch_frag(*J, pk, true, st);
     }
     hp->bvalid = true;
-  }
-  if (hp->j1.apre) {  // every evaluation (the weights depend on the probabilities)
-    const GemmJob& J = hp->j1;
-    k_afrag<<<(unsigned)J.nchunks, 256, (size_t)J.KC * pk.ldP * sizeof(double), st>>>(J.afrag, J.tilesM, J.KC, J.nchunks,
-                                                                                     J.ka, J.la, pk.Pr, pk.ldP);
-    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
   cudaEventRecord(hp->ev[0], st);
   cudaError_t e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
@@ -1187,7 +1227,8 @@ void hess_plan_design_changed(HessPlan* hp) {
 void hess_last_times(HessPlan* hp, double out[7]) {
   // [0] J1 GEMM (128-column tiles), [1] its split reduction, [2] J1 tail GEMM (narrow tile),
   // [3] its reduction, [4] Z/Y blocks (J2 + same-alternative), [5] assembly,
-  // [6] operand materialisation before J1 (k_afrag every evaluation, k_bfrag once per design)
+  // [6] operand materialisation before J1 (k_frag: weights every evaluation, design-only products
+  //     once per packed design)
   for (int i = 0; i < 7; ++i) {
     float ms = 0.f;
     if (!hp) { out[i] = 0.0; continue; }
