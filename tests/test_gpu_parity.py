@@ -106,6 +106,35 @@ def test_eval_parity_shapes(shape):
         assert np.array_equal(H, H.T)
 
 
+# Shapes that select each GEMM kernel: J2 materialised (K d + f >= 192) with a generated J1;
+# J1 split into 128-wide tiles + a 48-wide tail (vech 1326 = 10 x 128 + 46); vech 300 = 256 + 44.
+PATH_SHAPES = [(3000, 40, 10, 4, 5), (2500, 12, 50, 0, 0), (1500, 25, 24, 2, 2)]
+
+
+@pytest.mark.parametrize("mode", ["default", "MNL_NO_PIPE", "MNL_NO_MATERIALISE"])
+def test_hessian_kernel_paths(mode):
+    """Every GEMM path (materialised operands + k_pipe_gemm; B-only materialised + k_gen_gemm<BPRE>;
+    fully generated k_gen_gemm) against the oracle's full Hessian."""
+    if mode != "default":
+        os.environ[mode] = "1"
+    M.release()  # the plan (and its kernel choice) is rebuilt under the environment
+    try:
+        for N, K, p, f, d in PATH_SHAPES:
+            prob = datagen.custom(N, K, p, f, d, seed=5, coef_sd=0.3)
+            D = oracle_data(prob)
+            dp = device_problem(prob)
+            th = datagen.perturbed_theta(prob, 0.1)
+            l_o, g_o, H_o = O.mnl_eval(D, th)
+            l, g, H = gpu_eval(dp, th)
+            check_lg(l, g, l_o, g_o)
+            rel = np.linalg.norm(H - H_o) / np.linalg.norm(H_o)
+            assert rel <= 1e-9, (mode, (N, K, p, f, d), rel)
+            assert np.array_equal(H, H.T)
+    finally:
+        os.environ.pop(mode, None)
+        M.release()
+
+
 def test_eval_without_grad_and_hess_and_determinism():
     prob = datagen.make("c2")
     dp = device_problem(prob)
