@@ -38,8 +38,8 @@ struct EvalArgs {
   int64_t N;
   int K, p, f, d, q, n_p, off_alpha, off_gamma, QP, XS, TI, SCR;
   const double* X;
-  const double* Y;
-  const double* Z;
+  const double* Y;  // [N][K][f]
+  const double* Z;  // [N][K][d]
   const int32_t* choice;
   const double* coef;
   double* Pr;
@@ -70,25 +70,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Phase E (only with Y or Z): per individual, lanes over alternatives. The individual's Y and Z rows
-// are staged in this warp's smem slot by cp.async (the next individual's while this one computes):
-// corr = z.alpha + y.gamma, softmax, loglik, P (global Pr) and r (Rs), ybar, gamma/alpha gradients.
-__device__ __forceinline__ void stage_rows(const EvalArgs& A, double* slot, int64_t gi, int lane) {
-  const int ny = A.K * A.f, nz = A.K * A.d;
-  const double* ysrc = A.Y + gi * ny;
-  const double* zsrc = A.Z + gi * nz;
-  for (int t = lane; t < ny; t += 32)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                     static_cast<unsigned>(__cvta_generic_to_shared(slot + t))), "l"(ysrc + t) : "memory");
-  for (int t = lane; t < nz; t += 32)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                     static_cast<unsigned>(__cvta_generic_to_shared(slot + ny + t))), "l"(zsrc + t) : "memory");
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
+// Phase E (only with Y or Z): per individual, lanes over alternatives (k = lane + 32 kk). Lane k
+// reads its alternative's y_ik (f contiguous doubles) and z_ik (d) straight from the caller's
+// arrays: a warp-wide load touches one 32-byte sector per lane and the following components hit
+// the same sectors in L1 (the tile's Y and Z blocks were prefetched into L2). Pass 1: corr =
+// z.alpha + y.gamma, softmax, loglik, P (global Pr) and r (Rs); pass 2 (L1 hits): ybar and the
+// gamma / alpha gradients. This general version handles any f, d; phase_e_reg below keeps an
+// individual's values in registers when they fit.
+template <int KPL>
+__host__ __device__ constexpr int gam_regs() { return KPL <= 2 ? 16 : 8; }  // gamma-gradient partials held in registers
 
 template <int KPL>
-__device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, double* Rs, const int* ch_t, double* scr,
-                                        const double* alpha, const double* gamma, double* Wa, double (&gam)[8],
+__device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, double* Rs, const int* ch_t, double* red,
+                                        const double* alpha, const double* gamma, double* Wa, double (&gam)[gam_regs<KPL>()],
                                         double& l_s, double& l_c, int64_t i0, int nt, int KPS, int w, int lane) {
   const int K = A.K, d = A.d, f = A.f;
   const int rows = (A.TI + NW - 1) / NW;  // individuals per warp per tile
@@ -96,58 +90,76 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
   const int n_mine = min(rows, nt - ib);
   for (int ii = ib + max(n_mine, 0); ii < ib + rows; ++ii)  // ragged tail: zero residual rows
     for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
-  if (n_mine <= 0) return;
-  stage_rows(A, scr, i0 + ib, lane);
+  bool kok[KPL];  // this lane's alternatives exist
+#pragma unroll
+  for (int kk = 0; kk < KPL; ++kk) kok[kk] = lane + 32 * kk < K;
   for (int jj = 0; jj < n_mine; ++jj) {
     const int ii = ib + jj;
     const int64_t gi = i0 + ii;
-    double* cur = scr + (jj & 1) * A.SCR;
-    if (jj + 1 < n_mine) {
-      stage_rows(A, scr + ((jj + 1) & 1) * A.SCR, gi + 1, lane);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncwarp();
-    const double* Ys = cur;
-    const double* Zs = cur + K * f;
-    double u[KPL];
-    double m = -INFINITY;
-#pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const int k = lane + 32 * kk;
-      double v = -INFINITY;
-      if (k < K) {
-        v = Us[ii * KPS + k];
-        for (int c = 0; c < d; ++c) v = fma(Zs[k * d + c], alpha[k * d + c], v);
-        for (int e = 0; e < f; ++e) v = fma(Ys[k * f + e], gamma[e], v);
-      }
-      u[kk] = v;
-      m = fmax(m, v);
-    }
-    m = warp_max(m);
-    double ssum = 0.0;
-#pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const double e = (lane + 32 * kk < K) ? exp(u[kk] - m) : 0.0;
-      ssum += e;
-      u[kk] = e;
-    }
-    ssum = warp_sum(ssum);
+    const double* yl = A.Y + (gi * K + lane) * f;  // y_{i,lane+32kk,e} = yl[32 kk f + e]
+    const double* zl = A.Z + (gi * K + lane) * d;  // z_{i,lane+32kk,c} = zl[32 kk d + c]
     int y = ch_t[ii];
     if (y < 0 || y >= K) {
       if (lane == 0) atomicOr(A.err, 1);
       y = 0;
     }
-    // u at the chosen alternative: recompute it (cheap) on the owning lane
-    double uy_l = 0.0;
-    if ((y & 31) == lane) {
-      const int k = y;
-      double v = Us[ii * KPS + k];
-      for (int c = 0; c < d; ++c) v = fma(Zs[k * d + c], alpha[k * d + c], v);
-      for (int e = 0; e < f; ++e) v = fma(Ys[k * f + e], gamma[e], v);
-      uy_l = v;
+    // ---- pass 1: u_k += y_k . gamma + z_k . alpha_k (two accumulation chains per alternative) ----
+    double ua[KPL], ub[KPL];
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      ua[kk] = kok[kk] ? Us[ii * KPS + lane + 32 * kk] : 0.0;
+      ub[kk] = 0.0;
     }
+    {
+      constexpr int JB4 = KPL >= 4 ? 2 : 4;  // components per batch of loads
+      int j = 0;
+      for (; j + JB4 <= f; j += JB4) {
+        double v[JB4][KPL];
+#pragma unroll
+        for (int t = 0; t < JB4; ++t)
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk) v[t][kk] = kok[kk] ? __ldg(yl + 32 * kk * f + j + t) : 0.0;
+#pragma unroll
+        for (int t = 0; t < JB4; ++t) {
+          const double g = gamma[j + t];
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk) {
+            if (t & 1) ub[kk] = fma(v[t][kk], g, ub[kk]);
+            else ua[kk] = fma(v[t][kk], g, ua[kk]);
+          }
+        }
+      }
+      for (; j < f; ++j) {
+        const double g = gamma[j];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk)
+          if (kok[kk]) ua[kk] = fma(__ldg(yl + 32 * kk * f + j), g, ua[kk]);
+      }
+      for (int c = 0; c < d; ++c) {
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk)
+          if (kok[kk]) ((c & 1) ? ub : ua)[kk] = fma(__ldg(zl + 32 * kk * d + c), alpha[(lane + 32 * kk) * d + c],
+                                                   ((c & 1) ? ub : ua)[kk]);
+      }
+    }
+    double u[KPL];
+    double m = -INFINITY, uy_l = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const int k = lane + 32 * kk;
+      u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
+      if (k == y) uy_l = u[kk];
+      m = fmax(m, u[kk]);
+    }
+    m = warp_max(m);
+    double ssum = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
+      ssum += e;
+      u[kk] = e;
+    }
+    ssum = warp_sum(ssum);
     const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
     if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
     const double inv_s = 1.0 / ssum;
@@ -157,36 +169,34 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
       const int k = lane + 32 * kk;
       const double P = u[kk] * inv_s;
       u[kk] = P;
-      r[kk] = (k < K) ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
+      r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
       if (k < KPS) Rs[ii * KPS + k] = r[kk];
-      if (A.writeP && k < K) A.Pr[gi * A.ldP + k] = P;
+      if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
     }
-    // ybar_e = sum_k P_k y_ke and the gamma gradient, 8 components at a time; the cross-lane sums
-    // of ybar go through shared memory (red[8][33]): lane 4e'+j adds 8 of the 32 partials, then
-    // two shuffles - instead of a 5-step shuffle reduction per component
-    double* red = scr + 2 * A.SCR;  // [8][33] per warp
-    for (int e0 = 0; e0 < f; e0 += 8) {
-      double yb[8];
+    // ---- pass 2 (L1 hits): ybar_e = sum_k P_k y_ke, gamma and alpha gradients ----
+    // 8 components per batch; the cross-lane ybar sums go through red[8][33] (lane 4e'+j adds 8 of
+    // the 32 partials, then two shuffles). The first 16 gamma partials stay in registers.
+    auto ybar_batch = [&](int e0, double (&yb)[8], double (&gg)[8]) {
+      constexpr int TB = KPL >= 4 ? 2 : 4;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int e = e0 + t;
-        double ybt = 0.0, gg = 0.0;
-        if (e < f) {
+      for (int t0 = 0; t0 < 8; t0 += TB) {
+        double v[TB][KPL];
+#pragma unroll
+        for (int t = 0; t < TB; ++t)
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk)
+            v[t][kk] = (kok[kk] && e0 + t0 + t < f) ? __ldg(yl + 32 * kk * f + e0 + t0 + t) : 0.0;
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          double ybt = 0.0, g = 0.0;
 #pragma unroll
           for (int kk = 0; kk < KPL; ++kk) {
-            const int k = lane + 32 * kk;
-            if (k < K) {
-              const double yv = Ys[k * f + e];
-              ybt = fma(u[kk], yv, ybt);
-              gg = fma(yv, r[kk], gg);
-            }
+            ybt = fma(u[kk], v[t][kk], ybt);
+            g = fma(v[t][kk], r[kk], g);
           }
-          if (A.want_grad) {
-            if (e < 8) gam[t] += gg;  // e0 == 0 here
-            else Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gg;
-          }
+          yb[t0 + t] = ybt;
+          gg[t0 + t] = g;
         }
-        yb[t] = ybt;
       }
       if (A.writeP) {
 #pragma unroll
@@ -201,16 +211,186 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
         if (j == 0 && e0 + t < f) A.Pr[gi * A.ldP + K + e0 + t] = sacc;
         __syncwarp();
       }
-    }
-    if (A.want_grad && d) {
+    };
 #pragma unroll
-      for (int kk = 0; kk < KPL; ++kk) {
-        const int k = lane + 32 * kk;
-        if (k < K)
-          for (int c = 0; c < d; ++c) Wa[((w * KPL + kk) * d + c) * 32 + lane] += Zs[k * d + c] * r[kk];
+    for (int h = 0; h < gam_regs<KPL>() / 8; ++h) {
+      if (8 * h < f) {
+        double yb[8], gg[8];
+        ybar_batch(8 * h, yb, gg);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) gam[8 * h + t] += gg[t];  // components >= f add exact zeros
       }
     }
-    __syncwarp();  // done with this slot before it is refilled
+    for (int e0 = gam_regs<KPL>(); e0 < f; e0 += 8) {
+      double yb[8], gg[8];
+      ybar_batch(e0, yb, gg);
+      if (A.want_grad)
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (e0 + t < f) Wa[NW * KPL * d * 32 + (w * f + e0 + t) * 32 + lane] += gg[t];
+    }
+    if (A.want_grad && d) {
+      for (int c = 0; c < d; ++c)
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk)
+          if (kok[kk]) {
+            double* acc = Wa + ((w * KPL + kk) * d + c) * 32 + lane;
+            *acc = fma(__ldg(zl + 32 * kk * d + c), r[kk], *acc);
+          }
+    }
+  }
+}
+
+// Phase E when all (f + d) x KPL values of an individual fit in 32 registers per lane (c5: 15 x 2):
+// one batch of independent loads per individual, issued while the previous individual computes
+// (two register sets, ping-pong); both passes (utilities, then ybar and the gradients) read the
+// registers. JR = 32 / KPL component slots; slots >= f + d hold zeros.
+template <int KPL>
+__device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us, double* Rs, const int* ch_t,
+                                            double* red, const double* alpha, const double* gamma, double* Wa,
+                                            double (&gam)[gam_regs<KPL>()], double& l_s, double& l_c, int64_t i0, int nt,
+                                            int KPS, int w, int lane) {
+  constexpr int JR = 32 / KPL;
+  const int K = A.K, d = A.d, f = A.f, J = f + d;
+  const int rows = (A.TI + NW - 1) / NW;  // individuals per warp per tile
+  const int ib = w * rows;
+  const int n_mine = min(rows, nt - ib);
+  for (int ii = ib + max(n_mine, 0); ii < ib + rows; ++ii)  // ragged tail: zero residual rows
+    for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
+  if (n_mine <= 0) return;
+  bool kok[KPL];
+#pragma unroll
+  for (int kk = 0; kk < KPL; ++kk) kok[kk] = lane + 32 * kk < K;
+  auto load = [&](int64_t gi, double (&v)[JR][KPL]) {  // slots t < f: y_ike; f <= t < f + d: z_ik,t-f
+    const double* yl = A.Y + (gi * K + lane) * f;
+    const double* zl = A.Z + (gi * K + lane) * d;
+#pragma unroll
+    for (int t = 0; t < JR; ++t)
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk)
+        v[t][kk] = !kok[kk] ? 0.0 : (t < f ? __ldg(yl + 32 * kk * f + t) : (t < J ? __ldg(zl + 32 * kk * d + (t - f)) : 0.0));
+  };
+  auto process = [&](int ii, const double (&v)[JR][KPL]) {
+    const int64_t gi = i0 + ii;
+    int y = ch_t[ii];
+    if (y < 0 || y >= K) {
+      if (lane == 0) atomicOr(A.err, 1);
+      y = 0;
+    }
+    double ua[KPL], ub[KPL];
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      ua[kk] = kok[kk] ? Us[ii * KPS + lane + 32 * kk] : 0.0;
+      ub[kk] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < JR; ++t) {
+      if (t < f) {
+        const double g = gamma[t];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          if (t & 1) ub[kk] = fma(v[t][kk], g, ub[kk]);
+          else ua[kk] = fma(v[t][kk], g, ua[kk]);
+        }
+      } else if (t < J) {
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          const double a = kok[kk] ? alpha[(lane + 32 * kk) * d + (t - f)] : 0.0;
+          if (t & 1) ub[kk] = fma(v[t][kk], a, ub[kk]);
+          else ua[kk] = fma(v[t][kk], a, ua[kk]);
+        }
+      }
+    }
+    double u[KPL];
+    double m = -INFINITY, uy_l = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const int k = lane + 32 * kk;
+      u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
+      if (k == y) uy_l = u[kk];
+      m = fmax(m, u[kk]);
+    }
+    m = warp_max(m);
+    double ssum = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
+      ssum += e;
+      u[kk] = e;
+    }
+    ssum = warp_sum(ssum);
+    const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
+    if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
+    const double inv_s = 1.0 / ssum;
+    double r[KPL];
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      const int k = lane + 32 * kk;
+      const double P = u[kk] * inv_s;
+      u[kk] = P;
+      r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
+      if (k < KPS) Rs[ii * KPS + k] = r[kk];
+      if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+    }
+    // ybar (writeP) in groups of 8 components through red[8][33]; gamma partials (first 16 in
+    // registers); alpha partials read-modify-write in this warp's private Wa slots
+#pragma unroll
+    for (int t0 = 0; t0 < JR; t0 += 8) {
+      if (t0 < f) {
+        double yb[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          double ybt = 0.0, g = 0.0;
+          if (t0 + t < JR) {
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+              ybt = fma(u[kk], v[t0 + t][kk], ybt);
+              g = fma(v[t0 + t][kk], r[kk], g);
+            }
+          }
+          yb[t] = ybt;
+          if (t0 + t < f) {
+            if (t0 + t < 16) gam[(t0 + t) & 15] += g;
+            else Wa[NW * KPL * d * 32 + (w * f + t0 + t) * 32 + lane] += g;
+          }
+        }
+        if (A.writeP) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) red[t * 33 + lane] = yb[t];
+          __syncwarp();
+          const int t = lane >> 2, j = lane & 3;
+          double sacc = 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) sacc += red[t * 33 + j * 8 + q];
+          sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+          sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+          if (j == 0 && t0 + t < f) A.Pr[gi * A.ldP + K + t0 + t] = sacc;
+          __syncwarp();
+        }
+      }
+    }
+    if (A.want_grad) {
+#pragma unroll
+      for (int t = 0; t < JR; ++t)
+        if (t >= f && t < J) {
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk)
+            if (kok[kk]) {
+              double* acc = Wa + ((w * KPL + kk) * d + (t - f)) * 32 + lane;
+              *acc = fma(v[t][kk], r[kk], *acc);
+            }
+        }
+    }
+  };
+  double va[JR][KPL], vb[JR][KPL];
+  load(i0 + ib, va);
+  for (int jj = 0; jj < n_mine; jj += 2) {
+    if (jj + 1 < n_mine) load(i0 + ib + jj + 1, vb);
+    process(ib + jj, va);
+    if (jj + 1 < n_mine) {
+      if (jj + 2 < n_mine) load(i0 + ib + jj + 2, va);
+      process(ib + jj + 1, vb);
+    }
   }
 }
 
@@ -232,8 +412,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
                                                 // then [NW][f][32] gamma-gradient (e >= 8)
   double* Cf = Wa + NW * KPL * d * 32 + NW * f * 32;  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
-  double* Scr = Cf + K * d + f + 1 + TI;                  // [NW][2][SCR] Y|Z rows of one individual
-  if ((reinterpret_cast<uintptr_t>(Scr) & 15u) != 0) Scr += 1;
+  double* Red = Cf + K * d + f + 1 + TI;                  // [NW][8][33] ybar reductions
 
   for (int idx = tid; idx < QP * KPS; idx += blockDim.x) {
     const int a = idx / KPS, k = idx - a * KPS;
@@ -256,9 +435,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   for (int i = 0; i < CM_MAX; ++i)
 #pragma unroll
     for (int j = 0; j < CN; ++j) G[i][j][0] = G[i][j][1] = 0.0;
-  double gam[8];  // gamma-gradient lane partial (f <= 8 in registers, else phase D smem)
+  double gam[gam_regs<KPL>()];  // gamma-gradient lane partials (the first 8 or 16; the rest in Wa)
 #pragma unroll
-  for (int e = 0; e < 8; ++e) gam[e] = 0.0;
+  for (int e = 0; e < gam_regs<KPL>(); ++e) gam[e] = 0.0;
+
 
   double l_s = 0.0, l_c = 0.0;  // Neumaier loglik of this lane's rows (lanes with r4 == 0)
   const int64_t ntiles = (A.N + TI - 1) / TI;
@@ -281,15 +461,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
                    : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
     if (tid == 0) {  // warm L2 with the tile's alternative-varying rows (contiguous blocks)
-      if (f) {
-        const char* y0 = reinterpret_cast<const char*>(A.Y + i0 * K * f);
-        unsigned bytes = (unsigned)((int64_t)nt * K * f * 8) & ~15u;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(y0), "r"(bytes) : "memory");
-      }
-      if (d) {
-        const char* z0 = reinterpret_cast<const char*>(A.Z + i0 * K * d);
-        unsigned bytes = (unsigned)((int64_t)nt * K * d * 8) & ~15u;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(z0), "r"(bytes) : "memory");
+      const double* blk[2] = {f ? A.Y + i0 * K * f : nullptr, d ? A.Z + i0 * K * d : nullptr};
+      const int64_t len[2] = {(int64_t)nt * K * f * 8, (int64_t)nt * K * d * 8};
+      for (int b = 0; b < 2; ++b) {
+        if (!blk[b]) continue;
+        const char* b0 = reinterpret_cast<const char*>(blk[b]);
+        for (int64_t o = 0; o < len[b]; o += (1 << 20)) {  // <= 1 MB pieces, 16-byte multiples
+          const unsigned bytes = (unsigned)((len[b] - o < (1 << 20) ? len[b] - o : (1 << 20)) & ~int64_t(15));
+          if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0 + o), "r"(bytes) : "memory");
+        }
       }
     }
   };
@@ -333,7 +513,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
           *reinterpret_cast<double2*>(Ps + il * KPS + nb * 8 + 2 * r4) = make_double2(u[nb][0], u[nb][1]);
       }
       __syncthreads();
-      phase_e<KPL>(A, Ps, Rs, ch_t, Scr + w * (2 * A.SCR + 8 * 33 + 2), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+      bool done = false;
+      if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
+        if ((f + d) * KPL <= 32) {
+          phase_e_reg<KPL>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+          done = true;
+        }
+      }
+      if (!done)
+        phase_e<KPL>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
     } else {
     int y = valid ? ch_t[il] : 0;
     if (valid && (y < 0 || y >= K)) {
@@ -443,6 +631,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
         }
     }
   }
+  // register partials of gamma components 8..15 into Wa (each (warp, lane) slot is private)
+#pragma unroll
+  for (int e = 8; e < gam_regs<KPL>(); ++e)
+    if (e < f) Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gam[e];
   __syncthreads();
   // gamma partials: registers (e < 8) -> smem, then fixed-order sums
   double* gsc = Rs;  // [NW*32][8]
@@ -561,17 +753,12 @@ cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
 static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
-static int eval_scr(const Dims& D) {  // per-warp row staging: [2][Y row | Z row], 16-byte padded
-  const int n = D.K * D.f + D.K * D.d;
-  return (D.d + D.f) ? (n + 1) / 2 * 2 + 2 : 0;  // per slot; plus the [8][33] reduction area
-}
-
 static size_t eval_smem(const Dims& D, int kpl) {
   const int KP = 32 * kpl, KPS = KP + 4, TI = tile_rows(kpl, (D.d + D.f) > 0);
   const size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
                    ((D.d + D.f) ? (size_t)TI * KPS : 0) + (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32 +
                    (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
-                   (size_t)NW * (2 * eval_scr(D) + ((D.d + D.f) ? 8 * 33 + 2 : 0));
+                   ((D.d + D.f) ? (size_t)NW * 8 * 33 : 0);
   return n * sizeof(double);
 }
 
@@ -608,7 +795,7 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = eval_qp(D); a.XS = eval_xs(D);
-  a.TI = tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = eval_scr(D);
+  a.TI = tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = 0;
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
   a.Pr = writeP ? pk->Pr : nullptr;
   a.ldP = writeP ? pk->ldP : 0;
