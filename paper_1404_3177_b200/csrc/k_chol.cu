@@ -32,6 +32,22 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
+// out[M][N] = alpha * Am[M][K] Bm[K][N] from shared memory on DMMA (row-major operands; M, N
+// multiples of 8, K of 4); 8x8 output tiles dealt to warps wid, wid + nw, ...
+__device__ __forceinline__ void smem_gemm(double* out, int lo, const double* Am, int la, const double* Bm, int lb, int M,
+                                          int N, int K, double alpha, int wid, int nw) {
+  const int lane = threadIdx.x & 31, r = lane >> 2, kq = lane & 3;
+  const int tn_n = N / 8, tiles = (M / 8) * tn_n;
+  for (int t = wid; t < tiles; t += nw) {
+    const int tm = t / tn_n, tn = t - tm * tn_n;
+    double c0 = 0.0, c1 = 0.0;
+    for (int k0 = 0; k0 < K; k0 += 4)
+      dmma(c0, c1, Am[(tm * 8 + r) * la + k0 + kq], Bm[(k0 + kq) * lb + tn * 8 + r]);
+    out[(tm * 8 + r) * lo + tn * 8 + 2 * kq] = alpha * c0;
+    out[(tm * 8 + r) * lo + tn * 8 + 2 * kq + 1] = alpha * c1;
+  }
+}
+
 // k_potrf_inv: Cholesky of the jb x jb diagonal block fused with X = L^{-1}, blocked by 16:
 // for each 16-column sub-panel: (1) one warp factors the 16 x 16 diagonal block in registers with
 // shuffles (lanes 0-15: rows of L, lanes 16-31: rows of its inverse), (2) L21 = A21 X11^T,
@@ -160,23 +176,24 @@ __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, in
     }
   }
   if (tid == 0 && bad_any) atomicCAS(info, 0, j0 + 1);
-  // (4) off-diagonal blocks of X = L^{-1}: X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj, block rows in order
-  for (int bi = 1; bi < NB / SB; ++bi) {
-    const int i0 = bi * SB;
-    // T[j-cols] = sum_k L_ik X_kj for all j < i0 (16 x i0), then X_i,<i0 = -X_ii T
-    for (int e = tid; e < SB * i0; e += 256) {
-      const int ii = e / i0, jj = e % i0;
-      double acc = 0.0;
-      for (int t = (jj / SB) * SB; t < i0; ++t) acc = fma(S[i0 + ii][t], X[t][jj], acc);
-      T[jj][ii] = acc;
-    }
+  // (4) off-diagonal blocks of X = L^{-1} (the 16 x 16 diagonal blocks came from step 1) on DMMA:
+  // X_ba = -X_bb (L_ba X_aa) for the 16-blocks of each 32-block, then for the two 32-blocks.
+  // The strict upper triangle of S is zeroed first (the blocks are read whole).
+  for (int e = tid; e < NB * NB; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    if (c > r) S[r][c] = 0.0;
+  }
+  __syncthreads();
+  {
+    double(*T2)[33] = reinterpret_cast<double(*)[33]>(&T[0][0]);  // 32 x 33 view of T (64 x 17)
+    const int h = w >> 2, o = 32 * h;
+    smem_gemm(&T2[16 * h][0], 33, &S[o + 16][o], LDR, &X[o][o], LDR, 16, 16, 16, 1.0, w & 3, 4);
     __syncthreads();
-    for (int e = tid; e < SB * i0; e += 256) {
-      const int ii = e / i0, jj = e % i0;
-      double acc = 0.0;
-      for (int t = 0; t <= ii; ++t) acc = fma(X[i0 + ii][i0 + t], T[jj][t], acc);
-      X[i0 + ii][jj] = -acc;
-    }
+    smem_gemm(&X[o + 16][o], LDR, &X[o + 16][o + 16], LDR, &T2[16 * h][0], 33, 16, 16, 16, -1.0, w & 3, 4);
+    __syncthreads();
+    smem_gemm(&T2[0][0], 33, &S[32][0], LDR, &X[0][0], LDR, 32, 32, 32, 1.0, w, 8);
+    __syncthreads();
+    smem_gemm(&X[32][0], LDR, &X[32][32], LDR, &T2[0][0], 33, 32, 32, 32, -1.0, w, 8);
     __syncthreads();
   }
   for (int e = tid; e < NB * NB; e += 256) {
@@ -224,6 +241,25 @@ __global__ void __launch_bounds__(256) k_trtri_blocks(int n, const double* A, in
 }
 
 
+// 64 x 64 tile A[row0 + r][col0 + c] -> T[r][c] (zero for r >= nr or c >= nc), all 16 loads of a
+// thread in flight at once (clamped addresses, masked values; plain loads: trsm rewrites the tile)
+__device__ __forceinline__ void load_tile(double (*T)[LDS], const double* A, int lda, int row0, int col0, int nr,
+                                          int nc) {
+  const int tid = threadIdx.x;
+  double v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+    const int rr = r < nr ? r : (nr > 0 ? nr - 1 : 0), cc = c < nc ? c : (nc > 0 ? nc - 1 : 0);
+    v[m] = (nr > 0 && nc > 0) ? A[(int64_t)(row0 + rr) * lda + col0 + cc] : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+    T[r][c] = (r < nr && c < nc) ? v[m] : 0.0;
+  }
+}
+
 // out[64x64] = X[64x64] * Y[64x64]^T from two smem tiles (row-major, LDS); 8 warps of 16x32
 __device__ __forceinline__ void tile_xyT(const double (*Xs)[LDS], const double (*Ys)[LDS], double acc[2][4][2]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -256,10 +292,13 @@ __global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, in
   const int jb = min(NB, n - j0);
   const int r0 = j0 + jb + blockIdx.x * NB;
   const int tid = threadIdx.x;
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    Xs[r][c] = (r0 + r < n && c < jb) ? A[(int64_t)(r0 + r) * lda + j0 + c] : 0.0;
-    Ys[r][c] = Linv[e];
+  load_tile(Xs, A, lda, r0, j0, n - r0, jb);  // rows beyond n / columns beyond jb: zero
+  {
+    double v[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = __ldg(Linv + tid + 256 * m);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) Ys[(tid + 256 * m) >> 6][(tid + 256 * m) & 63] = v[m];
   }
   if (x && tid < NB) yv[tid] = tid < jb ? x[j0 + tid] : 0.0;
   __syncthreads();
@@ -313,11 +352,8 @@ __global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, i
   }
   const int ri = s0 + ti * NB, rj = s0 + tj * NB;
   const int tid = threadIdx.x;
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    Li[r][c] = (ri + r < n && c < jb) ? A[(int64_t)(ri + r) * lda + j0 + c] : 0.0;
-    Lj[r][c] = (rj + r < n && c < jb) ? A[(int64_t)(rj + r) * lda + j0 + c] : 0.0;
-  }
+  load_tile(Li, A, lda, ri, j0, n - ri, jb);
+  load_tile(Lj, A, lda, rj, j0, n - rj, jb);
   __syncthreads();
   double acc[2][4][2];
   tile_xyT(Li, Lj, acc);
