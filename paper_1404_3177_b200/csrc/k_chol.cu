@@ -49,41 +49,11 @@ __device__ __forceinline__ void smem_gemm(double* out, int lo, const double* Am,
 }
 
 // k_potrf_inv: Cholesky of the jb x jb diagonal block fused with X = L^{-1}, blocked by 16:
-// for each 16-column sub-panel: (1) one warp factors the 16 x 16 diagonal block in registers with
-// shuffles (lanes 0-15: rows of L, lanes 16-31: rows of its inverse), (2) L21 = A21 X11^T,
-// (3) A22 -= L21 L21^T on DMMA by all warps; finally the off-diagonal blocks of X are
-// X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj. With x != null it also applies the forward-solve piece
-// y_j = Linv b_j (b_j already holds every earlier panel's update).
+// for each 16-column sub-panel: (1) the 16 x 16 diagonal block and its inverse by the whole CTA
+// (one thread per entry), (2) L21 = A21 X11^T, (3) A22 -= L21 L21^T on DMMA by all warps;
+// finally the off-diagonal blocks of X = L^{-1} on DMMA. With x != null it also applies the
+// forward-solve piece y_j = Linv b_j (b_j already holds every earlier panel's update).
 constexpr int SB = 16;
-// One step of the in-warp 16 x 16 Cholesky + inverse (compile-time C so that every register index
-// is static; lanes 0-15 hold rows of L, lanes 16-31 rows of L^{-1}).
-template <int C>
-__device__ __forceinline__ void chol16_step(double (&d)[16], bool isS, int r, bool& bad_any) {
-  const double piv = __shfl_sync(0xffffffffu, d[C], C);
-  const bool bad = !(piv > 0.0) || !isfinite(piv);
-  bad_any |= bad;
-  const double rd = bad ? 1.0 : rsqrt(piv);
-  if (isS) {
-    if (r == C) d[C] = bad ? 1.0 : piv * rd;
-    else if (r > C) d[C] *= rd;
-  } else if (r == C) {
-#pragma unroll
-    for (int j = 0; j <= C; ++j) d[j] *= rd;
-  }
-#pragma unroll
-  for (int cc = C + 1; cc < 16; ++cc) {
-    const double lcc = __shfl_sync(0xffffffffu, d[C], cc);
-    if (isS && r >= cc) d[cc] = fma(-d[C], lcc, d[cc]);
-  }
-  const double lrc = __shfl_sync(0xffffffffu, d[C], r);  // L[r][C] from S-lane r
-#pragma unroll
-  for (int j = 0; j <= C; ++j) {
-    const double xcj = __shfl_sync(0xffffffffu, d[j], 16 + C);
-    if (!isS && r > C) d[j] = fma(-lrc, xcj, d[j]);
-  }
-  if constexpr (C + 1 < 16) chol16_step<C + 1>(d, isS, r, bad_any);
-}
-
 __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, int j0, double* Linv, int* info,
                                                    double* x) {
   extern __shared__ __align__(16) double dsm[];
@@ -91,6 +61,7 @@ __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, in
   double(*X)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + NB * LDR);
   __shared__ double T[NB][SB + 1];
   __shared__ double bv[NB];
+  __shared__ double colb[2][SB], xrow[2][SB], pv16[SB];
   const int jb = min(NB, n - j0);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   {  // all 16 loads of a thread in flight at once (clamped addresses, masked values)
@@ -113,22 +84,44 @@ __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, in
   __syncthreads();
   bool bad_any = false;
   for (int c0 = 0; c0 < NB; c0 += SB) {
-    // (1) warp 0: 16 x 16 diagonal block and its inverse, in registers
-    if (w == 0) {
-      const bool isS = lane < SB;
-      const int r = lane & (SB - 1);
-      double d[SB];
-#pragma unroll
-      for (int j = 0; j < SB; ++j) d[j] = isS ? (j <= r ? S[c0 + r][c0 + j] : 0.0) : (j == r ? 1.0 : 0.0);
-      chol16_step<0>(d, isS, r, bad_any);
-#pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        if (isS) {
-          if (j <= r) S[c0 + r][c0 + j] = d[j];
-        } else {
-          X[c0 + r][c0 + j] = (j <= r) ? d[j] : 0.0;
+    // (1) the 16 x 16 diagonal block and its inverse with all 256 threads, thread (r, c) holding
+    // entry (r, c) in a register and one barrier per column: factor with the unscaled update
+    // a_rc -= a_rC a_cC / a_CC (column C published to colb at the end of step C - 1), scale once;
+    // then X = L^{-1} row by row (row C scaled by 1 / L_CC and published, rows r > C updated).
+    {
+      const int r = tid >> 4, c = tid & 15;
+      double a = (c <= r) ? S[c0 + r][c0 + c] : 0.0;
+      if (c == 0) colb[0][r] = a;
+      __syncthreads();
+      for (int C = 0; C < SB; ++C) {
+        const double* cb = colb[C & 1];
+        double piv = cb[C];
+        const bool bad = !(piv > 0.0) || !isfinite(piv);
+        if (bad) piv = 1.0;  // keep the values finite; info reports the failure
+        if (tid == 0) {
+          pv16[C] = piv;
+          bad_any |= bad;
         }
+        const double inv = 1.0 / piv;
+        if (c > C && r >= c) a = fma(-cb[r] * inv, cb[c], a);
+        if (c == C + 1) colb[(C + 1) & 1][r] = a;
+        __syncthreads();
       }
+      if (c <= r) {
+        const double rs = rsqrt(pv16[c]);
+        S[c0 + r][c0 + c] = (r == c) ? pv16[c] * rs : a * rs;
+      }
+      __syncthreads();
+      double xv = (r == c) ? 1.0 : 0.0;
+      for (int C = 0; C < SB; ++C) {
+        if (r == C && c <= C) {
+          xv *= 1.0 / S[c0 + C][c0 + C];
+          xrow[C & 1][c] = xv;
+        }
+        __syncthreads();
+        if (r > C && c <= C) xv = fma(-S[c0 + r][c0 + C], xrow[C & 1][c], xv);
+      }
+      X[c0 + r][c0 + c] = (c <= r) ? xv : 0.0;
     }
     __syncthreads();
     const int r0 = c0 + SB, R = NB - r0;
