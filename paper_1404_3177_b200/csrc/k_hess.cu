@@ -551,13 +551,25 @@ __global__ void k_reduce_splits(double* __restrict__ dst, const double* __restri
 // through L1); a warp owns a 64 x 32 panel of T_k (MT x NT 8x8 DMMA blocks) and loads its fragment
 // elements straight from the packed rows (A = P_ik e_ik, B = f_ik, inner dimension = individuals).
 // Item = (alternative group, e-panel, f-panel, split); split partials are reduced in fixed order.
+// Same-alternative terms T_k[e][f] = sum_i P_ik s_e(i, k) t_f(i, k) with s = [x~_i | z_ik | y_ik]
+// (the x~ part absent for alternative 0) and t = [z_ik | y_ik] (the arrow of the block
+// structure). CTA = 8 alternatives (one warp each) x an (e, f) tile x a range of individuals.
+// Per chunk of CI individuals the rows every warp needs are staged once in shared memory by
+// cp.async (16-byte pieces where aligned, double-buffered, zero-filled beyond N / K):
+// row i = [x~_i (q, padded to even) | P_i,k0..k0+7 | z_i,k0..k0+7 (8d) | y_i,k0..k0+7 (8f) | 0],
+// stride RS = 4 (mod 16) doubles so the 4-row x 8-column fragment gathers are conflict free.
+// Each warp builds its fragments from smem; P_ik scales the (narrower) t side.
+__host__ __device__ inline int arrow_qe(int q) { return (q + 1) & ~1; }
+__host__ __device__ inline int arrow_row_len(int q, int d, int f) { return arrow_qe(q) + 8 + 8 * d + 8 * f + 1; }
+
 template <int MT, int NT>
 __global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, int f, int splits, int64_t Npad,
-                                               int n_ep, int n_fp, const double* __restrict__ Pr, int ldP,
-                                               const double* __restrict__ Xp, int ldX,
+                                               int n_ep, int n_fp, int CI, int RS, const double* __restrict__ Pr,
+                                               int ldP, const double* __restrict__ Xp, int ldX,
                                                const double* __restrict__ Zp, int ldZ,
                                                const double* __restrict__ Y, double* Tpart, int64_t tstride) {
-  const int E = q + d + f, F = d + f;
+  extern __shared__ __align__(16) double sst[];  // [2][CI][RS]
+  const int E = q + d + f, F = d + f, RL = arrow_row_len(q, d, f), qe = arrow_qe(q);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n_kg = (K + 7) / 8;
   int item = blockIdx.x;
@@ -565,63 +577,93 @@ __global__ void __launch_bounds__(256) k_arrow(int64_t N, int K, int q, int d, i
   const int ep = item % n_ep; item /= n_ep;
   const int fp = item % n_fp; item /= n_fp;
   const int split = item;
-  const int k = kg * 8 + w;
-  if (k >= K) return;
-  const int64_t nq = Npad / 4;
-  const int64_t q_begin = split * nq / splits, q_end = (split + 1) * nq / splits;
+  const int k0 = kg * 8, k = k0 + w;
+  const int64_t nch = Npad / CI;
+  const int64_t c_begin = split * nch / splits, c_end = (split + 1) * nch / splits;
   const int r4 = lane & 3, c8 = lane >> 2;
-  // per (lane, block) source: element (i, col) = src[i * str] * sc, no divergent branches
-  // (sc = 0 for padding / the x~ part of alternative 0; src then points at a valid zero-weight row)
-  const double* esrc[MT];
-  int64_t estr[MT];
-  double esc[MT];
-  const double* fsrc[NT];
-  int64_t fstr[NT];
+  const int oP = qe, oZ = qe + 8, oY = qe + 8 + 8 * d, o0 = RL - 1;  // o0: a zero
+  int eoff[MT];
 #pragma unroll
   for (int mb = 0; mb < MT; ++mb) {
     const int e = ep * MT * 8 + mb * 8 + c8;
-    esc[mb] = 1.0;
-    if (e < q) { esrc[mb] = Xp + e; estr[mb] = ldX; if (k == 0) esc[mb] = 0.0; }
-    else if (e < q + d) { esrc[mb] = Zp + k * d + (e - q); estr[mb] = ldZ; }
-    else if (e < E) { esrc[mb] = Y + (int64_t)k * f + (e - q - d); estr[mb] = (int64_t)K * f; }
-    else { esrc[mb] = Xp; estr[mb] = ldX; esc[mb] = 0.0; }
+    if (e < q) eoff[mb] = (k == 0) ? o0 : e;
+    else if (e < q + d) eoff[mb] = oZ + w * d + (e - q);
+    else if (e < E) eoff[mb] = oY + w * f + (e - q - d);
+    else eoff[mb] = o0;
   }
+  int foff[NT];
 #pragma unroll
   for (int nb = 0; nb < NT; ++nb) {
     const int fi = fp * NT * 8 + nb * 8 + c8;
-    if (fi < d) { fsrc[nb] = Zp + k * d + fi; fstr[nb] = ldZ; }
-    else if (fi < F) { fsrc[nb] = Y + (int64_t)k * f + (fi - d); fstr[nb] = (int64_t)K * f; }
-    else { fsrc[nb] = Xp; fstr[nb] = 0; }  // finite filler; its A partner rows are multiplied by 0 below
+    foff[nb] = fi < d ? oZ + w * d + fi : (fi < F ? oY + w * f + (fi - d) : o0);
   }
+  for (int r = threadIdx.x; r < 2 * CI; r += blockDim.x) sst[(size_t)r * RS + o0] = 0.0;  // never staged
+  auto cp8 = [](double* dst, const double* src, bool ok) {  // zero-fill when !ok
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0)
+                 : "memory");
+  };
+  auto cp16 = [](double* dst, const double* src, int bytes) {  // bytes in {0, 8, 16}; rest zero-filled
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+                 : "memory");
+  };
+  const int nz = min(8, K - k0) * d, ny = min(8, K - k0) * f;  // this group's z / y values per row
+  const bool y16 = (f % 2) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  auto stage = [&](int64_t c, int buf) {  // warp per row, lanes across each segment
+    double* base = sst + (size_t)buf * CI * RS;
+    for (int r = w; r < CI; r += 8) {
+      const int64_t i = c * CI + r;
+      double* row = base + (size_t)r * RS;
+      const double* xr = Xp + i * ldX;  // ldX >= qe: the pair read past an odd q stays in the row
+      for (int t = 2 * lane; t < qe; t += 64) cp16(row + t, xr + t, 16);
+      if (lane < 4) cp16(row + oP + 2 * lane, Pr + i * ldP + k0 + 2 * lane,
+                         8 * max(0, min(2, K - (k0 + 2 * lane))));
+      const double* zr = Zp + i * ldZ + k0 * d;
+      for (int t = 2 * lane; t < 8 * d; t += 64) cp16(row + oZ + t, zr + (t < nz ? t : 0), 8 * max(0, min(2, nz - t)));
+      const double* yr = Y + ((i < N ? i : 0) * K + k0) * f;
+      if (y16) {
+        for (int t = 2 * lane; t < 8 * f; t += 64)
+          cp16(row + oY + t, yr + (t < ny ? t : 0), i < N ? 8 * max(0, min(2, ny - t)) : 0);
+      } else {
+        for (int t = lane; t < 8 * f; t += 32) cp8(row + oY + t, yr + (t < ny ? t : 0), i < N && t < ny);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   double acc[MT][NT][2];
 #pragma unroll
   for (int a = 0; a < MT; ++a)
 #pragma unroll
     for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  constexpr int U = 2;  // quads of individuals whose loads are issued together
-  for (int64_t qq0 = q_begin; qq0 < q_end; qq0 += U) {
-    double av[U][MT], bv[U][NT];
+  if (c_begin < c_end) stage(c_begin, 0);
+  int buf = 0;
+  for (int64_t c = c_begin; c < c_end; ++c, buf ^= 1) {
+    if (c + 1 < c_end) stage(c + 1, buf ^ 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (k < K) {
+      const double* base = sst + (size_t)buf * CI * RS;
+#pragma unroll 2
+      for (int qq = 0; qq < CI / 4; ++qq) {
+        const double* row = base + (size_t)(4 * qq + r4) * RS;
+        const double pk = row[oP + w];
+        double av[MT], bv[NT];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int64_t i = (qq0 + u) * 4 + r4;
-      const double w8 = (qq0 + u < q_end) ? 1.0 : 0.0;
-      const double pk = w8 * __ldg(Pr + i * ldP + k);  // 0 for padding rows (i >= N)
-      const int64_t ic = i < N ? i : N - 1;            // Y has only N rows
+        for (int mb = 0; mb < MT; ++mb) av[mb] = row[eoff[mb]];
 #pragma unroll
-      for (int mb = 0; mb < MT; ++mb) av[u][mb] = pk * esc[mb] * __ldg(esrc[mb] + ic * estr[mb]);
+        for (int nb = 0; nb < NT; ++nb) bv[nb] = pk * row[foff[nb]];
 #pragma unroll
-      for (int nb = 0; nb < NT; ++nb) bv[u][nb] = __ldg(fsrc[nb] + ic * fstr[nb]);
+        for (int mb = 0; mb < MT; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NT; ++nb)
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
+                : "d"(av[mb]), "d"(bv[nb]));
+      }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int mb = 0; mb < MT; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NT; ++nb)
-          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-              : "+d"(acc[mb][nb][0]), "+d"(acc[mb][nb][1])
-              : "d"(av[u][mb]), "d"(bv[u][nb]));
+    __syncthreads();  // done with buf before it is refilled
   }
+  if (k >= K) return;
   double* out = Tpart + split * tstride + (int64_t)k * E * F;
 #pragma unroll
   for (int mb = 0; mb < MT; ++mb) {
@@ -738,7 +780,7 @@ struct HessPlan {
   GemmJob j1, j1b, j2;  // j1b: the vech columns beyond the last whole 128-column tile of j1
   bool has_j1b = false;
   int n1a = 0;          // vech columns computed by j1
-  int ar_splits, ar_mt, ar_nt, ar_ep, ar_fp;
+  int ar_splits, ar_mt, ar_nt, ar_ep, ar_fp, ar_ci, ar_rs;
   double* Tpart = nullptr;
   double* T = nullptr;
   unsigned* counters = nullptr;  // [2]
@@ -991,8 +1033,12 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
     hp->ar_ep = (E + hp->ar_mt * 8 - 1) / (hp->ar_mt * 8);
     hp->ar_fp = (F + hp->ar_nt * 8 - 1) / (hp->ar_nt * 8);
     const int base_items = (K + 7) / 8 * hp->ar_ep * hp->ar_fp;
+    hp->ar_rs = pad4mod16(arrow_row_len(q, d, f));
+    hp->ar_ci = 32;
+    while (hp->ar_ci > 4 && (size_t)2 * hp->ar_ci * hp->ar_rs * sizeof(double) > (size_t)200 * 1024) hp->ar_ci /= 2;
+    const int64_t nch = pk.Npad / hp->ar_ci;
     int S = 1;
-    while ((int64_t)base_items * S < 2 * sms && pk.Npad / 4 / (S * 2) >= 64) S *= 2;
+    while ((int64_t)base_items * S < 2 * sms && nch / (S * 2) >= 8) S *= 2;
     hp->ar_splits = S;
     const size_t tb = ((size_t)K * E * F + 1) / 2 * 2 * sizeof(double);
     if (cudaMalloc(&hp->Tpart, tb * S) != cudaSuccess) ok = false;
@@ -1184,8 +1230,16 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
       const int items = (D.K + 7) / 8 * hp->ar_ep * hp->ar_fp * hp->ar_splits;
       const int64_t tstride = ((int64_t)D.K * E * F + 1) / 2 * 2;
 #define MNL_ARROW(MT_, NT_)                                                                                  \
-  k_arrow<MT_, NT_><<<items, 256, 0, st>>>(D.N, D.K, D.q, D.d, D.f, hp->ar_splits, pk.Npad, hp->ar_ep, hp->ar_fp, \
-                                           pk.Pr, pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y, hp->Tpart, tstride)
+  do {                                                                                                       \
+    static bool attr_ = false;                                                                               \
+    if (!attr_) {                                                                                            \
+      cudaFuncSetAttribute(k_arrow<MT_, NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);      \
+      attr_ = true;                                                                                          \
+    }                                                                                                        \
+    k_arrow<MT_, NT_><<<items, 256, (size_t)2 * hp->ar_ci * hp->ar_rs * sizeof(double), st>>>(               \
+        D.N, D.K, D.q, D.d, D.f, hp->ar_splits, pk.Npad, hp->ar_ep, hp->ar_fp, hp->ar_ci, hp->ar_rs, pk.Pr,   \
+        pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y, hp->Tpart, tstride);                                        \
+  } while (0)
       if (hp->ar_mt == 8 && hp->ar_nt == 4) MNL_ARROW(8, 4);
       else if (hp->ar_mt == 8) MNL_ARROW(8, 2);
       else if (hp->ar_mt == 6 && hp->ar_nt == 4) MNL_ARROW(6, 4);
