@@ -54,9 +54,9 @@ __device__ __forceinline__ void smem_gemm(double* out, int lo, const double* Am,
 // finally the off-diagonal blocks of X = L^{-1} on DMMA. With x != null it also applies the
 // forward-solve piece y_j = Linv b_j (b_j already holds every earlier panel's update).
 constexpr int SB = 16;
-__global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, int j0, double* Linv, int* info,
-                                                   double* x) {
-  extern __shared__ __align__(16) double dsm[];
+__device__ __noinline__ void potrf_block(int n, double* A, int lda, int j0, double* Linv, int* info, double* x,
+                                         double* dsm) {
+  __syncthreads();  // the CTA may have used dsm for another step just before
   double(*S)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm);
   double(*X)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + NB * LDR);
   __shared__ double T[NB][SB + 1];
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, in
     for (int m = 0; m < 16; ++m) {
       const int e = tid + 256 * m, r = e >> 6, c = e & 63;
       const int rr = r < jb ? r : jb - 1, ccl = c < jb ? c : jb - 1;
-      v[m] = __ldg(A + (int64_t)(j0 + rr) * lda + j0 + ccl);
+      v[m] = __ldcg(A + (int64_t)(j0 + rr) * lda + j0 + ccl);  // L2: other CTAs updated it
     }
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, in
       X[r][c] = 0.0;
     }
   }
-  if (x && tid < NB) bv[tid] = tid < jb ? x[j0 + tid] : 0.0;
+  if (x && tid < NB) bv[tid] = tid < jb ? __ldcg(x + j0 + tid) : 0.0;
   __syncthreads();
   bool bad_any = false;
   for (int c0 = 0; c0 < NB; c0 += SB) {
@@ -204,6 +204,12 @@ __global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, in
   }
 }
 
+__global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, int j0, double* Linv, int* info,
+                                                   double* x) {
+  extern __shared__ __align__(16) double dsm[];
+  potrf_block(n, A, lda, j0, Linv, info, x, dsm);
+}
+
 __global__ void __launch_bounds__(256) k_trtri_blocks(int n, const double* A, int lda, double* Linv) {
   extern __shared__ __align__(16) double dsm[];
   double(*S)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm);
@@ -235,7 +241,8 @@ __global__ void __launch_bounds__(256) k_trtri_blocks(int n, const double* A, in
 
 
 // 64 x 64 tile A[row0 + r][col0 + c] -> T[r][c] (zero for r >= nr or c >= nc), all 16 loads of a
-// thread in flight at once (clamped addresses, masked values; plain loads: trsm rewrites the tile)
+// thread in flight at once (clamped addresses, masked values; L2 loads: other CTAs of the
+// persistent factorisation wrote the tile, and trsm rewrites it)
 __device__ __forceinline__ void load_tile(double (*T)[LDS], const double* A, int lda, int row0, int col0, int nr,
                                           int nc) {
   const int tid = threadIdx.x;
@@ -244,7 +251,7 @@ __device__ __forceinline__ void load_tile(double (*T)[LDS], const double* A, int
   for (int m = 0; m < 16; ++m) {
     const int e = tid + 256 * m, r = e >> 6, c = e & 63;
     const int rr = r < nr ? r : (nr > 0 ? nr - 1 : 0), cc = c < nc ? c : (nc > 0 ? nc - 1 : 0);
-    v[m] = (nr > 0 && nc > 0) ? A[(int64_t)(row0 + rr) * lda + col0 + cc] : 0.0;
+    v[m] = (nr > 0 && nc > 0) ? __ldcg(A + (int64_t)(row0 + rr) * lda + col0 + cc) : 0.0;
   }
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
@@ -276,24 +283,25 @@ __device__ __forceinline__ void tile_xyT(const double (*Xs)[LDS], const double (
   }
 }
 
-// rows [j0+jb + 64*blockIdx.x, +64): L21 = A21 Linv^T; with x: x_r -= L21_r . y_j
-__global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, int j0, const double* Linv, double* x) {
-  extern __shared__ __align__(16) double dsm[];
+// rows [j0+jb + 64*tile, +64): L21 = A21 Linv^T; with x: x_r -= L21_r . y_j
+__device__ __noinline__ void trsm_tile(int n, double* A, int lda, int j0, const double* Linv, double* x, int tile,
+                                       double* dsm) {
+  __syncthreads();  // smem reuse across consecutive tiles
   double(*Xs)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
   double(*Ys)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + NB * LDS);
   __shared__ double yv[NB];
   const int jb = min(NB, n - j0);
-  const int r0 = j0 + jb + blockIdx.x * NB;
+  const int r0 = j0 + jb + tile * NB;
   const int tid = threadIdx.x;
   load_tile(Xs, A, lda, r0, j0, n - r0, jb);  // rows beyond n / columns beyond jb: zero
   {
     double v[16];
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = __ldg(Linv + tid + 256 * m);
+    for (int m = 0; m < 16; ++m) v[m] = __ldcg(Linv + tid + 256 * m);
 #pragma unroll
     for (int m = 0; m < 16; ++m) Ys[(tid + 256 * m) >> 6][(tid + 256 * m) & 63] = v[m];
   }
-  if (x && tid < NB) yv[tid] = tid < jb ? x[j0 + tid] : 0.0;
+  if (x && tid < NB) yv[tid] = tid < jb ? __ldcg(x + j0 + tid) : 0.0;
   __syncthreads();
   double acc[2][4][2];
   tile_xyT(Xs, Ys, acc);
@@ -317,32 +325,23 @@ __global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, in
     for (int t = q4; t < jb; t += 4) s = fma(Xs[r][t], yv[t], s);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (q4 == 0 && r0 + r < n) x[r0 + r] -= s;
+    if (q4 == 0 && r0 + r < n) x[r0 + r] = __ldcg(x + r0 + r) - s;
   }
 }
 
-// trailing update: lower tiles (ti >= tj) of A22 -= L21 L21^T.
-// col_only = 1: only block-column 0 of the trailing matrix (the next panel, lookahead path);
-// col_only = 0: the lower triangle starting at tile (first, first).
-__global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, int j0, int col_only, int first) {
+__global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, int j0, const double* Linv, double* x) {
   extern __shared__ __align__(16) double dsm[];
+  trsm_tile(n, A, lda, j0, Linv, x, blockIdx.x, dsm);
+}
+
+// trailing update tile (ti, tj), ti >= tj, of A22 -= L21 L21^T (tile coordinates relative to the
+// first row/column after panel j0)
+__device__ __noinline__ void syrk_tile(int n, double* A, int lda, int j0, int ti, int tj, double* dsm) {
+  __syncthreads();  // smem reuse across consecutive tiles
   double(*Li)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
   double(*Lj)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + NB * LDS);
   const int jb = min(NB, n - j0);
   const int s0 = j0 + jb;
-  int ti, tj;
-  if (col_only) {
-    ti = blockIdx.x;
-    tj = 0;
-  } else {
-    const int t = blockIdx.x;  // -> (ti, tj), ti >= tj, row-major over the lower triangle
-    ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    while (ti * (ti + 1) / 2 > t) --ti;
-    tj = t - ti * (ti + 1) / 2;
-    ti += first;
-    tj += first;
-  }
   const int ri = s0 + ti * NB, rj = s0 + tj * NB;
   const int tid = threadIdx.x;
   load_tile(Li, A, lda, ri, j0, n - ri, jb);
@@ -359,8 +358,32 @@ __global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, i
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = ri + wr + a * 8 + lr, c = rj + wc + b * 8 + 2 * lk + h;
-        if (r < n && c < n && c <= r) A[(int64_t)r * lda + c] -= acc[a][b][h];
+        if (r < n && c < n && c <= r) A[(int64_t)r * lda + c] = __ldcg(A + (int64_t)r * lda + c) - acc[a][b][h];
       }
+}
+
+// linear index over the lower triangle of tiles (row-major) -> (ti, tj), ti >= tj
+__device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
+  ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  tj = t - ti * (ti + 1) / 2;
+}
+
+// col_only = 1: only block-column 0 of the trailing matrix (the next panel, lookahead path);
+// col_only = 0: the lower triangle starting at tile (first, first).
+__global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, int j0, int col_only, int first) {
+  extern __shared__ __align__(16) double dsm[];
+  int ti, tj;
+  if (col_only) {
+    ti = blockIdx.x;
+    tj = 0;
+  } else {
+    tri_tile(blockIdx.x, ti, tj);
+    ti += first;
+    tj += first;
+  }
+  syrk_tile(n, A, lda, j0, ti, tj, dsm);
 }
 
 // ---- triangular solve wavefront ------------------------------------------------------------
@@ -453,7 +476,70 @@ __global__ void __launch_bounds__(256) k_trsv_wave(int n, const double* L, int l
   if (tid == 0) st_release(flags + b, epoch);
 }
 
+// ---- persistent factorisation (one cooperative launch) -------------------------------------
+// Grid barrier over all CTAs of a cooperative launch: count + generation (sense) in global memory.
+// Writes before the barrier are published with a gpu-scope fence; the phases read A / Linv / x
+// through L2 (__ldcg), never through a possibly stale L1.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned& my_gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned g = my_gen;
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+    } else {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+        if (v == g) __nanosleep(32);
+      } while (v == g);
+    }
+  }
+  my_gen += 1;
+  __syncthreads();
+}
+
+// The blocked right-looking factorisation of factor() in one kernel (n <= 2816), with the same one-panel
+// lookahead: per panel j, (B) all CTAs compute the trsm tiles of panel j, (C) all CTAs update
+// block column j+1, (A) CTA 0 factors panel j+1 while the other CTAs apply the rest of panel j's
+// trailing update. Every tile runs exactly the arithmetic of the multi-kernel path (same device
+// functions, same order per entry), so the factor is bitwise identical; only launch and
+// cross-stream synchronisation costs go away. bar = {count, generation}.
+__global__ void __launch_bounds__(256, 1) k_chol_persist(int n, double* A, int lda, double* Linv, int* info, double* x,
+                                                         unsigned* bar) {
+  extern __shared__ __align__(16) double dsm[];
+  const unsigned G = gridDim.x, b = blockIdx.x;
+  unsigned my_gen = 0;
+  if (threadIdx.x == 0) my_gen = *reinterpret_cast<volatile unsigned*>(bar + 1);
+  const int np = (n + NB - 1) / NB;
+  if (b == 0) potrf_block(n, A, lda, 0, Linv, info, x, dsm);
+  grid_barrier(bar, bar + 1, my_gen, G);
+  for (int j = 0; j + 1 < np; ++j) {
+    const int j0 = j * NB, rem = n - j0 - NB, mt = (rem + NB - 1) / NB;
+    const double* Lj = Linv + (size_t)j * NB * NB;
+    for (int t = b; t < mt; t += G) trsm_tile(n, A, lda, j0, Lj, x, t, dsm);          // (B)
+    grid_barrier(bar, bar + 1, my_gen, G);
+    for (int t = b; t < mt; t += G) syrk_tile(n, A, lda, j0, t, 0, dsm);             // (C)
+    grid_barrier(bar, bar + 1, my_gen, G);
+    if (b == 0) {                                                                    // (A)
+      potrf_block(n, A, lda, j0 + NB, Linv + (size_t)(j + 1) * NB * NB, info, x, dsm);
+    } else {
+      const int nrest = (mt - 1) * mt / 2;
+      for (int t = b - 1; t < nrest; t += G - 1) {
+        int ti, tj;
+        tri_tile(t, ti, tj);
+        syrk_tile(n, A, lda, j0, ti + 1, tj + 1, dsm);
+      }
+    }
+    grid_barrier(bar, bar + 1, my_gen, G);
+  }
+}
+
 struct CholWork {
+  unsigned* bar = nullptr;  // k_chol_persist's grid barrier {count, generation}
+  int persist_grid = -1;    // CTAs of the cooperative launch (0: not available)
   double* Linv = nullptr;
   size_t cap = 0;
   const double* factor = nullptr;  // matrix whose Linv blocks are current
@@ -526,9 +612,41 @@ cudaEvent_t la_event(size_t i) {
 // Factorisation with a one-panel lookahead; with x != null also the forward solve x <- L^{-1} x.
 // side stream: [A22 update of the next panel's block column] -> potrf(j+1) -> trsm(j+1)
 // main stream: the rest of panel j's trailing update, concurrently.
+cudaError_t factor_persist(int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
+  cudaMemsetAsync(info, 0, sizeof(int), st);
+  void* args[] = {(void*)&n, (void*)&A, (void*)&lda, (void*)&g_cw.Linv, (void*)&info, (void*)&x, (void*)&g_cw.bar};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_chol_persist, dim3(g_cw.persist_grid), dim3(256), args,
+                                              kDyn, st);
+  count_launch();
+  g_cw.factor = A;
+  g_cw.factor_n = n;
+  return e;
+}
+
+// CTAs for k_chol_persist: one per SM when the kernel fits there (0 disables the persistent path)
+int persist_grid() {
+  if (g_cw.persist_grid >= 0) return g_cw.persist_grid;
+  g_cw.persist_grid = 0;
+  if (getenv("MNL_CHOL_STREAMS")) return 0;
+  int dev = 0, sms = 0, coop = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop || cudaFuncSetAttribute(k_chol_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn) != cudaSuccess)
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chol_persist, 256, kDyn) != cudaSuccess || occ < 1) return 0;
+  if (cudaMalloc(&g_cw.bar, 2 * sizeof(unsigned)) != cudaSuccess) return 0;
+  cudaMemset(g_cw.bar, 0, 2 * sizeof(unsigned));
+  g_cw.persist_grid = sms;  // one CTA per SM: the panel CTA has its SM to itself
+  return g_cw.persist_grid;
+}
+
 cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
   set_attrs();
   if (!ensure_work(n)) return cudaErrorMemoryAllocation;
+  // persistent single launch while the panel chain dominates; above ~3000 the trailing updates
+  // dominate and the multi-kernel path (3 CTAs per SM for them) is faster (measured crossover)
+  if (n <= 2816 && persist_grid() > 1) return factor_persist(n, A, lda, info, x, st);
   if (!g_la.side) {
     int lo = 0, hi = 0;  // the panel chain is the critical path: give it the highest priority
     cudaDeviceGetStreamPriorityRange(&lo, &hi);

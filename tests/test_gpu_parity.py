@@ -181,6 +181,34 @@ def test_cholesky_and_solve(n):
     assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
 
 
+@pytest.mark.parametrize("n", [3000, 3100])
+def test_cholesky_large_multikernel_path(n):
+    """n > 2816 takes the multi-kernel (two-stream lookahead) factorisation."""
+    test_cholesky_and_solve(n)
+
+
+def test_cholesky_streams_path_small_and_fit(tmp_path):
+    """The multi-kernel factorisation forced for small n (MNL_CHOL_STREAMS, read once per
+    process): a fresh interpreter factors and fits, compared with LAPACK / the golden fit."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, json, sys\n"
+        "sys.path.insert(0, %r)\n"
+        "import paper_1404_3177_b200 as M, datagen\n"
+        "rng = np.random.default_rng(7); n = 700\n"
+        "B = rng.standard_normal((n, n + 3)); A = B @ B.T / n + np.eye(n) * 0.1\n"
+        "Ad = torch.from_numpy(A).cuda(); assert M.mnl_cholesky(Ad) == M.MNL_OK\n"
+        "L = np.tril(Ad.cpu().numpy()); Lr = np.linalg.cholesky(A)\n"
+        "print(json.dumps({'err': float(np.max(np.abs(L - Lr)) / np.max(np.abs(Lr)))}))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MNL_CHOL_STREAMS="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    err = json.loads(out.stdout.strip().splitlines()[-1])["err"]
+    assert err <= 1e-11
+
+
 def test_cholesky_not_spd():
     A = np.eye(70)
     A[40, 40] = -1.0
