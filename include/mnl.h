@@ -108,7 +108,34 @@ typedef struct {
   double total_ms;          /* wall time of the call */
   double gemm_ms;           /* device time of the beta-beta DMMA GEMMs (J1 + tail), summed */
   int32_t halvings_per_iter[64];  /* first 64 iterations */
+  double delta_loglik;      /* |l_t - l_(t-1)| of the last accepted update (0 without one) */
+  int32_t stop_reason;      /* mnl_stop_reason */
+  int32_t cg_iters;         /* total conjugate-gradient iterations (method MNL_METHOD_CG) */
 } mnl_fit_stats;
+
+/* Why a fit stopped: the first of the paper's three conditions met. */
+typedef enum {
+  MNL_STOP_NONE = 0,        /* an error status ended the fit */
+  MNL_STOP_GTOL = 1,        /* ||g||_2 < gtol */
+  MNL_STOP_FTOL = 2,        /* |l_t - l_(t-1)| < ftol after an accepted update */
+  MNL_STOP_MAXITER = 3      /* max_iter updates taken (status MNL_MAXITER) */
+} mnl_stop_reason;
+
+typedef enum {
+  MNL_METHOD_NEWTON = 0,    /* exact Hessian + Cholesky (the paper's method) */
+  MNL_METHOD_CG = 1         /* truncated Newton: conjugate gradients on Hessian-vector products,
+                               H never formed (the paper's stated extension) */
+} mnl_method;
+
+/* Options of mnl_newton_fit_opts. */
+typedef struct {
+  double gtol;              /* ||g||_2 threshold, > 0 (reading R10) */
+  double ftol;              /* |l_t - l_(t-1)| threshold tested after each accepted update; 0 = off */
+  int32_t max_iter;         /* >= 0 Newton updates */
+  int32_t method;           /* mnl_method */
+  int32_t cg_max_iter;      /* MNL_METHOD_CG: CG iterations per Newton step; 0 => n_p */
+  double cg_rtol;           /* MNL_METHOD_CG: stop CG at ||r|| <= cg_rtol ||g||; 0 => min(0.5, sqrt(||g||)) */
+} mnl_fit_options;
 
 /* mnl_newton_fit plus the report (stats may be NULL). */
 int mnl_newton_fit_ex(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
@@ -116,6 +143,25 @@ int mnl_newton_fit_ex(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
                       const double* coef0, double tol, int32_t max_iter,
                       double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats,
                       void* stream);
+
+/* The fit with the paper's full stopping set (gtol, ftol, maxiter: the first met ends it) and a
+ * choice of Newton step (mnl_method). With MNL_METHOD_NEWTON and ftol = 0 it is mnl_newton_fit_ex.
+ * MNL_METHOD_CG solves (-H) delta = g approximately by conjugate gradients with one
+ * mnl_hessvec-style product per CG iteration (never forming H; memory O(N (K + f) + n_p)), then
+ * takes the same step-halving line search; MNL_ERR_NOT_SPD if a CG curvature p'(-H)p <= 0 occurs
+ * before any progress. opts must be non-NULL. */
+int mnl_newton_fit_opts(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                        const double* X, const double* Y, const double* Z, const int32_t* choice,
+                        const double* coef0, const mnl_fit_options* opts,
+                        double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats, void* stream);
+
+/* Hessian-vector product at `coef`: hv = H v (P:462-476 applied to v without forming H):
+ *   hv = -sum_i J_i^T (diag(P_i) - P_i P_i^T) J_i v,  J_i = d u_i / d theta
+ * (u_i the K utilities of individual i). v, hv: dev [n_p] (may not alias). Same inputs and errors
+ * as mnl_eval. */
+int mnl_hessvec(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                const double* X, const double* Y, const double* Z, const int32_t* choice,
+                const double* coef, const double* v, double* hv, void* stream);
 
 /* Host-buffer variants: every pointer is HOST memory (pinned or pageable). The call copies the
  * inputs to the device, runs the same path and copies the outputs back, all inside the call. */

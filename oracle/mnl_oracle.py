@@ -255,6 +255,24 @@ def hessian_entries(D: Data, theta, rows, cols, P: np.ndarray | None = None) -> 
     return out
 
 
+def hessvec(D: Data, theta, v, P: np.ndarray | None = None) -> np.ndarray:
+    """H v = -sum_i J_i^T (diag p_i - p_i p_i^T) (J_i v)  (applied to v; the product form of
+    the paper's Hessian-free extension): s_i = J_i v, w_ik = p_ik (s_ik - p_i.s_i),
+    (Hv)_r = -sum_i sum_k J_i[k, r] w_ik. Never forms H."""
+    if P is None:
+        P = probabilities(utilities(D, theta))
+    v = np.asarray(v, dtype=np.float64)
+    S = np.zeros((D.N, D.K))
+    cols = [jac_column(D, r) for r in range(D.n_p)]
+    for r, (ks, vals) in enumerate(cols):
+        S[:, ks] += vals * v[r]
+    W = P * (S - np.sum(P * S, axis=1, keepdims=True))
+    out = np.empty(D.n_p)
+    for r, (ks, vals) in enumerate(cols):
+        out[r] = -np.sum(vals * W[:, ks])
+    return out
+
+
 def mnl_eval(D: Data, theta, want_grad=True, want_hess=True):
     """(loglik, grad, hess) at theta -- the oracle twin of the ABI's mnl_eval."""
     theta = np.asarray(theta, dtype=np.float64)
@@ -278,15 +296,23 @@ class FitLog:
     coef: np.ndarray | None = None
     history: list = field(default_factory=list)   # per iteration: dict(l, gnorm, halvings, margin)
     grad_norm: float = float("nan")
+    stop_reason: int = 0       # 0 error, 1 gtol, 2 ftol, 3 maxiter (the ABI's mnl_stop_reason)
+    delta_loglik: float = 0.0  # |l_t - l_(t-1)| of the last accepted update
+    cg_iters: int = 0          # newton_cg_fit only
 
 
-def newton_fit(D: Data, coef0=None, tol: float = 1e-6, max_iter: int = 50, hess_fn=None) -> FitLog:
+def newton_fit(D: Data, coef0=None, tol: float = 1e-6, max_iter: int = 50, hess_fn=None,
+               ftol: float = 0.0, step_fn=None) -> FitLog:
     """theta_new = theta_old - H^{-1} dl/dtheta (Eq. "NR update"), with step halving
-    until the log-likelihood is "not lower than" at theta_old (R7 floor tau), stopping on
-    ||g||_2 < tol tested before forming H (R10, R11) or iters == max_iter."""
+    until the log-likelihood is "not lower than" at theta_old (R7 floor tau). Stops at
+    the first of the paper's conditions met: ||g||_2 < tol tested before
+    forming H (R10, R11), |l_t - l_(t-1)| < ftol after an accepted update (ftol = 0: off), or
+    iters == max_iter. step_fn(theta, P, g, l) -> (status, delta) replaces the Cholesky solve of
+    (-H) delta = g (newton_cg_fit)."""
     theta = np.zeros(D.n_p) if coef0 is None else np.array(coef0, dtype=np.float64)
     log = FitLog()
     hess_fn = hess_fn or hessian
+    ftol_met = False
     while True:
         V = utilities(D, theta)
         P = probabilities(V)
@@ -298,18 +324,27 @@ def newton_fit(D: Data, coef0=None, tol: float = 1e-6, max_iter: int = 50, hess_
         gnorm = float(np.sqrt(np.sum(g * g)))
         log.loglik, log.grad_norm = l, gnorm
         if gnorm < tol:
-            log.status = MNL_OK
+            log.status, log.stop_reason = MNL_OK, 1
+            break
+        if ftol_met:
+            log.status, log.stop_reason = MNL_OK, 2
             break
         if log.iters == max_iter:
-            log.status = MNL_MAXITER
+            log.status, log.stop_reason = MNL_MAXITER, 3
             break
-        H = hess_fn(D, theta, P)
-        try:
-            L = np.linalg.cholesky(-H)
-        except np.linalg.LinAlgError:
-            log.status = MNL_ERR_NOT_SPD
-            break
-        delta = solve_triangular(L.T, solve_triangular(L, g, lower=True), lower=False)  # (-H) delta = g
+        if step_fn is not None:
+            status, delta = step_fn(theta, P, g, l)
+            if status != MNL_OK:
+                log.status = status
+                break
+        else:
+            H = hess_fn(D, theta, P)
+            try:
+                L = np.linalg.cholesky(-H)
+            except np.linalg.LinAlgError:
+                log.status = MNL_ERR_NOT_SPD
+                break
+            delta = solve_triangular(L.T, solve_triangular(L, g, lower=True), lower=False)  # (-H) delta = g
         tau = TAU_REL * max(1.0, abs(l))
         accepted = False
         for j in range(MAX_HALVINGS + 1):
@@ -323,7 +358,50 @@ def newton_fit(D: Data, coef0=None, tol: float = 1e-6, max_iter: int = 50, hess_
             break
         log.history.append(dict(l=l, gnorm=gnorm, halvings=j, l_new=l_j,
                                 margin=(l_j - l) / max(1.0, abs(l))))
+        log.delta_loglik = abs(l_j - l)
+        ftol_met = ftol > 0.0 and log.delta_loglik < ftol
         theta = theta_j
         log.iters += 1
     log.coef = theta
+    return log
+
+
+def newton_cg_fit(D: Data, coef0=None, tol: float = 1e-6, max_iter: int = 50, ftol: float = 0.0,
+                  cg_max_iter: int = 0, cg_rtol: float = 0.0) -> FitLog:
+    """Truncated Newton (the paper's Hessian-free extension): the Newton system
+    (-H) delta = g is solved approximately by conjugate gradients from delta = 0 using only products
+    H p (hessvec), stopping at ||r|| <= eta ||g||, eta = cg_rtol or min(0.5, sqrt(||g||))
+    (Eisenstat-Walker forcing), or after cg_max_iter (0: n_p) iterations, or at non-positive
+    curvature (an error before the first step); then the same line search and stopping set as
+    newton_fit."""
+    counter = {"cg": 0}
+
+    def step(theta, P, g, l):
+        gn = float(np.sqrt(g @ g))
+        eta = cg_rtol if cg_rtol > 0 else min(0.5, math.sqrt(gn))
+        cmax = cg_max_iter if cg_max_iter > 0 else D.n_p
+        delta = np.zeros(D.n_p)
+        r = g.copy()
+        pv = g.copy()
+        rr = float(r @ r)
+        for it in range(cmax):
+            ap = -hessvec(D, theta, pv, P)
+            pap = float(pv @ ap)
+            if not (pap > 0 and np.isfinite(pap)):
+                if it == 0:
+                    return MNL_ERR_NOT_SPD, None
+                break
+            alpha = rr / pap
+            delta = delta + alpha * pv
+            r = r - alpha * ap
+            rr_new = float(r @ r)
+            counter["cg"] += 1
+            if math.sqrt(rr_new) <= eta * gn:
+                break
+            pv = r + (rr_new / rr) * pv
+            rr = rr_new
+        return MNL_OK, delta
+
+    log = newton_fit(D, coef0, tol, max_iter, ftol=ftol, step_fn=step)
+    log.cg_iters = counter["cg"]
     return log

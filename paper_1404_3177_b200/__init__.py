@@ -22,7 +22,10 @@ MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_
 
 EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex", "mnl_eval_host",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
-            "mnl_status_string", "mnl_release", "mnl_last_hessian_times")
+            "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec")
+
+MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
+MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
 
 
 class MnlError(RuntimeError):
@@ -31,12 +34,19 @@ class MnlError(RuntimeError):
         self.code = code
 
 
+class FitOptions(ctypes.Structure):
+    """mnl_fit_options (include/mnl.h)."""
+    _fields_ = [("gtol", ctypes.c_double), ("ftol", ctypes.c_double), ("max_iter", ctypes.c_int32),
+                ("method", ctypes.c_int32), ("cg_max_iter", ctypes.c_int32), ("cg_rtol", ctypes.c_double)]
+
+
 class FitStats(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("halvings", ctypes.c_int32), ("evals", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("grad_norm", ctypes.c_double), ("loglik", ctypes.c_double),
                 ("hess_ms", ctypes.c_double), ("chol_ms", ctypes.c_double), ("eval_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("gemm_ms", ctypes.c_double),
-                ("halvings_per_iter", ctypes.c_int32 * 64)]
+                ("halvings_per_iter", ctypes.c_int32 * 64), ("delta_loglik", ctypes.c_double),
+                ("stop_reason", ctypes.c_int32), ("cg_iters", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "halvings_per_iter"}
@@ -70,6 +80,11 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_ex.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, D, I32, V,
                                       ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(FitStats), V]
     lib.mnl_newton_fit_ex.restype = ctypes.c_int
+    lib.mnl_newton_fit_opts.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, ctypes.POINTER(FitOptions), V,
+                                        ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(FitStats), V]
+    lib.mnl_newton_fit_opts.restype = ctypes.c_int
+    lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
+    lib.mnl_hessvec.restype = ctypes.c_int
     lib.mnl_eval_host.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_eval_host.restype = ctypes.c_int
     lib.mnl_newton_fit_host.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, D, I32, V,
@@ -198,20 +213,37 @@ class FitResult:
 
 
 def mnl_newton_fit(prob: Problem, coef0=None, tol: float = 1e-6, max_iter: int = 50, stream=None,
-                   raise_on_error: bool = True) -> FitResult:
+                   raise_on_error: bool = True, ftol: float = 0.0, method: str = "newton",
+                   cg_max_iter: int = 0, cg_rtol: float = 0.0) -> FitResult:
+    """Newton-Raphson fit (mnl_newton_fit_opts): gtol = tol, ftol (0 = off), method "newton" (exact
+    Hessian + Cholesky) or "cg" (truncated Newton on Hessian-vector products)."""
     torch = _torch()
     coef = torch.empty(prob.n_p, dtype=torch.float64, device=prob.choice.device)
     it = ctypes.c_int32(0)
     ll = ctypes.c_double(0.0)
     st = FitStats()
+    opts = FitOptions(tol, ftol, max_iter, {"newton": MNL_METHOD_NEWTON, "cg": MNL_METHOD_CG}[method],
+                      cg_max_iter, cg_rtol)
     X, Y, Z, ch = prob.ptrs()
-    rc = load().mnl_newton_fit_ex(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, ch,
-                                  coef0.data_ptr() if coef0 is not None else None, tol, max_iter,
-                                  coef.data_ptr(), ctypes.byref(it), ctypes.byref(ll), ctypes.byref(st),
-                                  _stream(stream))
+    rc = load().mnl_newton_fit_opts(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, ch,
+                                    coef0.data_ptr() if coef0 is not None else None, ctypes.byref(opts),
+                                    coef.data_ptr(), ctypes.byref(it), ctypes.byref(ll), ctypes.byref(st),
+                                    _stream(stream))
     if raise_on_error and rc not in (MNL_OK, MNL_MAXITER):
         raise MnlError(rc, "mnl_newton_fit")
     return FitResult(coef, it.value, ll.value, rc, st.as_dict())
+
+
+def mnl_hessvec(prob: Problem, coef, v, stream=None):
+    """H v at coef (CUDA float64 [n_p] each), without forming H."""
+    torch = _torch()
+    hv = torch.empty(prob.n_p, dtype=torch.float64, device=prob.choice.device)
+    X, Y, Z, ch = prob.ptrs()
+    rc = load().mnl_hessvec(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, ch, coef.data_ptr(), v.data_ptr(),
+                            hv.data_ptr(), _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_hessvec")
+    return hv
 
 
 def mnl_cholesky(A, stream=None):

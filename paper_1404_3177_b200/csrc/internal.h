@@ -59,6 +59,17 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
                         cudaStream_t st);
 // Fixed-order reduction of the CTA partials -> loglik, grad (optional); scal[0] = l,
 // scal[1] = ||g||^2, scal[2] = err flag (as double). `counter` is a zeroed int.
+// Hessian-vector product pass: part receives H v (gradient slots) from P_i in pk->Pr (written by the
+// last evaluation with writeP) and s_i = J_i v.
+cudaError_t launch_hessvec(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
+                           const int32_t* choice, const double* v, const Packed* pk, double* part, int* err,
+                           cudaStream_t st);
+// CG vector steps (single CTA, n <= 16384, deterministic): Ap = -Hp & out = p.Ap;
+// delta += alpha p, r -= alpha Ap & out = r.r; p = r + beta p
+cudaError_t launch_cg_curv(int n, const double* p, const double* hp, double* ap, double* out, cudaStream_t st);
+cudaError_t launch_cg_update(int n, double alpha, const double* p, const double* ap, double* delta, double* r,
+                             double* out, cudaStream_t st);
+cudaError_t launch_cg_dir(int n, double beta, const double* r, double* p, cudaStream_t st);
 cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const double* part,
                                  bool want_grad, double* grad, double* loglik_out, double* scal,
                                  const int* err, unsigned* counter, cudaStream_t st);

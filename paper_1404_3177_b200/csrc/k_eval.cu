@@ -80,7 +80,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int KPL>
 __host__ __device__ constexpr int gam_regs() { return KPL <= 2 ? 16 : 8; }  // gamma-gradient partials held in registers
 
-template <int KPL>
+template <int KPL, bool HV>
 __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, double* Rs, const int* ch_t, double* red,
                                         const double* alpha, const double* gamma, double* Wa, double (&gam)[gam_regs<KPL>()],
                                         double& l_s, double& l_c, int64_t i0, int nt, int KPS, int w, int lane) {
@@ -142,36 +142,51 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
                                                    ((c & 1) ? ub : ua)[kk]);
       }
     }
-    double u[KPL];
-    double m = -INFINITY, uy_l = 0.0;
+    double u[KPL], r[KPL];
+    if constexpr (HV) {  // Hessian-vector product: s_k = ua + ub, r_k = -P_k (s_k - sum_l P_l s_l)
+      double ps = 0.0;
 #pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const int k = lane + 32 * kk;
-      u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
-      if (k == y) uy_l = u[kk];
-      m = fmax(m, u[kk]);
-    }
-    m = warp_max(m);
-    double ssum = 0.0;
+      for (int kk = 0; kk < KPL; ++kk) {
+        u[kk] = kok[kk] ? __ldg(A.Pr + gi * A.ldP + lane + 32 * kk) : 0.0;
+        ps = fma(u[kk], ua[kk] + ub[kk], ps);
+      }
+      ps = warp_sum(ps);
 #pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
-      ssum += e;
-      u[kk] = e;
-    }
-    ssum = warp_sum(ssum);
-    const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
-    if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
-    const double inv_s = 1.0 / ssum;
-    double r[KPL];
-#pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const int k = lane + 32 * kk;
-      const double P = u[kk] * inv_s;
-      u[kk] = P;
-      r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
-      if (k < KPS) Rs[ii * KPS + k] = r[kk];
-      if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        r[kk] = kok[kk] ? -u[kk] * ((ua[kk] + ub[kk]) - ps) : 0.0;
+        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+      }
+    } else {
+      double m = -INFINITY, uy_l = 0.0;
+  #pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
+        if (k == y) uy_l = u[kk];
+        m = fmax(m, u[kk]);
+      }
+      m = warp_max(m);
+      double ssum = 0.0;
+  #pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
+        ssum += e;
+        u[kk] = e;
+      }
+      ssum = warp_sum(ssum);
+      const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
+      if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
+      const double inv_s = 1.0 / ssum;
+  #pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        const double P = u[kk] * inv_s;
+        u[kk] = P;
+        r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
+        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+        if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+      }
     }
     // ---- pass 2 (L1 hits): ybar_e = sum_k P_k y_ke, gamma and alpha gradients ----
     // 8 components per batch; the cross-lane ybar sums go through red[8][33] (lane 4e'+j adds 8 of
@@ -245,7 +260,7 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
 // one batch of independent loads per individual, issued while the previous individual computes
 // (two register sets, ping-pong); both passes (utilities, then ybar and the gradients) read the
 // registers. JR = 32 / KPL component slots; slots >= f + d hold zeros.
-template <int KPL>
+template <int KPL, bool HV>
 __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us, double* Rs, const int* ch_t,
                                             double* red, const double* alpha, const double* gamma, double* Wa,
                                             double (&gam)[gam_regs<KPL>()], double& l_s, double& l_c, int64_t i0, int nt,
@@ -301,36 +316,51 @@ __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us,
         }
       }
     }
-    double u[KPL];
-    double m = -INFINITY, uy_l = 0.0;
+    double u[KPL], r[KPL];
+    if constexpr (HV) {  // Hessian-vector product: s_k = ua + ub, r_k = -P_k (s_k - sum_l P_l s_l)
+      double ps = 0.0;
 #pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const int k = lane + 32 * kk;
-      u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
-      if (k == y) uy_l = u[kk];
-      m = fmax(m, u[kk]);
-    }
-    m = warp_max(m);
-    double ssum = 0.0;
+      for (int kk = 0; kk < KPL; ++kk) {
+        u[kk] = kok[kk] ? __ldg(A.Pr + gi * A.ldP + lane + 32 * kk) : 0.0;
+        ps = fma(u[kk], ua[kk] + ub[kk], ps);
+      }
+      ps = warp_sum(ps);
 #pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
-      ssum += e;
-      u[kk] = e;
-    }
-    ssum = warp_sum(ssum);
-    const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
-    if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
-    const double inv_s = 1.0 / ssum;
-    double r[KPL];
-#pragma unroll
-    for (int kk = 0; kk < KPL; ++kk) {
-      const int k = lane + 32 * kk;
-      const double P = u[kk] * inv_s;
-      u[kk] = P;
-      r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
-      if (k < KPS) Rs[ii * KPS + k] = r[kk];
-      if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        r[kk] = kok[kk] ? -u[kk] * ((ua[kk] + ub[kk]) - ps) : 0.0;
+        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+      }
+    } else {
+      double m = -INFINITY, uy_l = 0.0;
+  #pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
+        if (k == y) uy_l = u[kk];
+        m = fmax(m, u[kk]);
+      }
+      m = warp_max(m);
+      double ssum = 0.0;
+  #pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
+        ssum += e;
+        u[kk] = e;
+      }
+      ssum = warp_sum(ssum);
+      const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
+      if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
+      const double inv_s = 1.0 / ssum;
+  #pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        const double P = u[kk] * inv_s;
+        u[kk] = P;
+        r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
+        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+        if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+      }
     }
     // ybar (writeP) in groups of 8 components through red[8][33]; gamma partials (first 16 in
     // registers); alpha partials read-modify-write in this warp's private Wa slots
@@ -394,7 +424,7 @@ __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us,
   }
 }
 
-template <int KPL, int CM_MAX>
+template <int KPL, int CM_MAX, bool HV>
 __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   extern __shared__ __align__(16) double sm[];
   constexpr int KP = 32 * KPL, KPS = KP + 4;   // alternatives padded; smem row stride = 4 (mod 16)
@@ -516,12 +546,37 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
       bool done = false;
       if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
         if ((f + d) * KPL <= 32) {
-          phase_e_reg<KPL>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+          phase_e_reg<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
           done = true;
         }
       }
       if (!done)
-        phase_e<KPL>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+        phase_e<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+    } else {
+    if constexpr (HV) {
+      // Hessian-vector product: u holds s_ik = (J_i v)_k; with P_i from the last evaluation
+      // (Pr), r_ik = -P_ik (s_ik - sum_l P_il s_il), so that the gradient contractions below
+      // accumulate H v (P:462-476 applied to v)
+      double pk[NBN][2], ps = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NBN; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = nb * 8 + 2 * r4 + h;
+          pk[nb][h] = (valid && k < K) ? __ldg(A.Pr + i * A.ldP + k) : 0.0;
+          ps = fma(pk[nb][h], u[nb][h], ps);
+        }
+      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+      double* Rrow = Rs + il * KPS;
+#pragma unroll
+      for (int nb = 0; nb < NBN; ++nb) {
+        const int k = nb * 8 + 2 * r4;
+        double2 R2;
+        R2.x = -pk[nb][0] * (u[nb][0] - ps);
+        R2.y = -pk[nb][1] * (u[nb][1] - ps);
+        if (in_b) *reinterpret_cast<double2*>(Rrow + k) = R2;
+      }
     } else {
     int y = valid ? ch_t[il] : 0;
     if (valid && (y < 0 || y >= K)) {
@@ -575,6 +630,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
         else if (k < K) pr[0] = P2.x;
       }
     }
+    }  // !HV
     }
     __syncthreads();  // Rs complete
 
@@ -734,18 +790,65 @@ __global__ void k_axpy_pow2(int n, const double* theta, const double* delta, int
   if (r < n) out[r] = theta[r] + ldexp(delta[r], -j);  // a7: theta + delta / 2^j, exact scaling
 }
 
-template <int KPL, int CM>
+template <int KPL, int CM, bool HV>
 cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  k_eval_kernel<KPL, CM><<<plan.grid, plan.block, plan.smem, st>>>(a);
+  k_eval_kernel<KPL, CM, HV><<<plan.grid, plan.block, plan.smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
+}
+
+// ---- small single-CTA vector kernels of the truncated-Newton (CG) step (n <= 16384) ----------
+// Every reduction runs in one CTA in a fixed order (deterministic).
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;  // valid in thread 0
+}
+
+// Ap = -Hp, out[0] = p . Ap
+__global__ void __launch_bounds__(1024) k_cg_curv(int n, const double* p, const double* hp, double* ap, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double a = -hp[i];
+    ap[i] = a;
+    s = fma(p[i], a, s);
+  }
+  s = cta_sum(s, red);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// delta += alpha p, r -= alpha Ap, out[0] = r . r
+__global__ void __launch_bounds__(1024) k_cg_update(int n, double alpha, const double* p, const double* ap,
+                                                   double* delta, double* r, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    delta[i] = fma(alpha, p[i], delta[i]);
+    const double ri = fma(-alpha, ap[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = cta_sum(s, red);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// p = r + beta p
+__global__ void __launch_bounds__(1024) k_cg_dir(int n, double beta, const double* r, double* p) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = fma(beta, p[i], r[i]);
 }
 
 }  // namespace
@@ -787,25 +890,29 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   return true;
 }
 
-cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
-                        const double* Z, const int32_t* choice, const double* coef,
-                        const Packed* pk, bool want_grad, bool writeP, double* part, int* err,
-                        cudaStream_t st) {
+static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
+                                    const double* Z, const int32_t* choice, const double* coef, const Packed* pk,
+                                    bool want_grad, bool writeP, bool hv, double* part, int* err, cudaStream_t st) {
   EvalArgs a;
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = eval_qp(D); a.XS = eval_xs(D);
   a.TI = tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = 0;
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
-  a.Pr = writeP ? pk->Pr : nullptr;
-  a.ldP = writeP ? pk->ldP : 0;
-  a.want_grad = want_grad; a.writeP = writeP;
+  a.Pr = (writeP || hv) ? pk->Pr : nullptr;
+  a.ldP = (writeP || hv) ? pk->ldP : 0;
+  a.want_grad = want_grad; a.writeP = writeP && !hv;
   a.part = part; a.n_part = plan.n_part; a.err = err;
-#define MNL_EVAL_CASE(KPL_)                                   \
-  case KPL_:                                                  \
-    if (plan.cm == 2) return launch_k<KPL_, 2>(plan, a, st);  \
-    if (plan.cm == 4) return launch_k<KPL_, 4>(plan, a, st);  \
-    return launch_k<KPL_, 8>(plan, a, st);
+#define MNL_EVAL_CASE(KPL_)                                                                   \
+  case KPL_:                                                                                  \
+    if (hv) {                                                                                 \
+      if (plan.cm == 2) return launch_k<KPL_, 2, true>(plan, a, st);                          \
+      if (plan.cm == 4) return launch_k<KPL_, 4, true>(plan, a, st);                          \
+      return launch_k<KPL_, 8, true>(plan, a, st);                                            \
+    }                                                                                         \
+    if (plan.cm == 2) return launch_k<KPL_, 2, false>(plan, a, st);                           \
+    if (plan.cm == 4) return launch_k<KPL_, 4, false>(plan, a, st);                           \
+    return launch_k<KPL_, 8, false>(plan, a, st);
   switch (plan.kpl) {
     MNL_EVAL_CASE(1)
     MNL_EVAL_CASE(2)
@@ -814,6 +921,38 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
   }
 #undef MNL_EVAL_CASE
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
+                        const double* Z, const int32_t* choice, const double* coef,
+                        const Packed* pk, bool want_grad, bool writeP, double* part, int* err,
+                        cudaStream_t st) {
+  return launch_eval_impl(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, false, part, err, st);
+}
+
+cudaError_t launch_hessvec(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
+                           const int32_t* choice, const double* v, const Packed* pk, double* part, int* err,
+                           cudaStream_t st) {
+  return launch_eval_impl(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
+}
+
+cudaError_t launch_cg_curv(int n, const double* p, const double* hp, double* ap, double* out, cudaStream_t st) {
+  k_cg_curv<<<1, 1024, 0, st>>>(n, p, hp, ap, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_update(int n, double alpha, const double* p, const double* ap, double* delta, double* r,
+                             double* out, cudaStream_t st) {
+  k_cg_update<<<1, 1024, 0, st>>>(n, alpha, p, ap, delta, r, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_dir(int n, double beta, const double* r, double* p, cudaStream_t st) {
+  k_cg_dir<<<1, 1024, 0, st>>>(n, beta, r, p);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const double* part,

@@ -50,6 +50,8 @@ struct Workspace {
   // Newton vectors / matrix
   double *theta = nullptr, *trial = nullptr, *grad = nullptr, *delta = nullptr, *A = nullptr;
   size_t ctheta = 0, ctrial = 0, cgrad = 0, cdelta = 0, cA = 0;
+  double* cg = nullptr;  // truncated Newton: r, p, Hp, Ap [4][n_p] + 2 scalars
+  size_t ccg = 0;
   // cached hessian plan
   HessPlan* hp = nullptr;
   Dims hp_dims{};
@@ -142,6 +144,16 @@ int run_eval(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X, c
   return MNL_OK;
 }
 
+// H v at the coefficients of the last evaluation with writeP (P_i in pk->Pr); hv dev [n_p].
+int run_hessvec(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X, const double* Y, const double* Z,
+                const int32_t* choice, const double* v, const Packed* pk, double* hv, cudaStream_t st) {
+  if (!grow(&W.part, &W.cpart, (size_t)ep.grid * ep.n_part)) return MNL_ERR_CUDA;
+  cudaError_t e = launch_hessvec(D, ep, X, Y, Z, choice, v, pk, W.part, W.err, st);
+  if (e != cudaSuccess) return MNL_ERR_CUDA;
+  e = launch_eval_finalize(D, ep, W.part, true, hv, nullptr, W.scal, W.err, W.counter, st);
+  return e == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
+}
+
 bool check_inputs(const Dims& D, const double* X, const double* Y, const double* Z, const int32_t* choice) {
   if ((D.p > 0) != (X != nullptr) || (D.f > 0) != (Y != nullptr) || (D.d > 0) != (Z != nullptr) || !choice)
     return false;
@@ -186,13 +198,28 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+mnl_fit_options default_options(double tol, int32_t max_iter) {
+  mnl_fit_options o;
+  o.gtol = tol;
+  o.ftol = 0.0;
+  o.max_iter = max_iter;
+  o.method = MNL_METHOD_NEWTON;
+  o.cg_max_iter = 0;
+  o.cg_rtol = 0.0;
+  return o;
+}
+
 int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
-             const double* Z, const int32_t* choice, const double* coef0, double tol, int32_t max_iter,
+             const double* Z, const int32_t* choice, const double* coef0, const mnl_fit_options& o,
              double* coef, int32_t* iters_out, double* loglik_out, mnl_fit_stats* stats, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
   Dims D;
+  const double tol = o.gtol;
+  const int32_t max_iter = o.max_iter;
+  const bool use_cg = o.method == MNL_METHOD_CG;
   if (!dims_of(N, K, p, f, d, &D) || !check_inputs(D, X, Y, Z, choice) || !coef || !iters_out || !loglik_out ||
-      !(tol > 0.0) || max_iter < 0)
+      !(tol > 0.0) || max_iter < 0 || !(o.ftol >= 0.0) || (o.method != MNL_METHOD_NEWTON && !use_cg) ||
+      o.cg_max_iter < 0 || !(o.cg_rtol >= 0.0) || !(o.cg_rtol < 1.0))
     return MNL_ERR_ARG;
   Workspace& W = g_ws;
   int rc = init_device(W);
@@ -203,12 +230,14 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
   if (!ensure_packed(W, D, &pk)) return MNL_ERR_CUDA;
   const int n = D.n_p;
   if (!grow(&W.theta, &W.ctheta, n) || !grow(&W.trial, &W.ctrial, n) || !grow(&W.grad, &W.cgrad, n) ||
-      !grow(&W.delta, &W.cdelta, n) || !grow(&W.A, &W.cA, (size_t)n * n))
+      !grow(&W.delta, &W.cdelta, n))
     return MNL_ERR_CUDA;
-  HessPlan* hp = get_hess_plan(W, D, pk);
-  if (!hp) return MNL_ERR_CUDA;
+  if (!use_cg && !grow(&W.A, &W.cA, (size_t)n * n)) return MNL_ERR_CUDA;
+  if (use_cg && !grow(&W.cg, &W.ccg, (size_t)4 * n + 2)) return MNL_ERR_CUDA;
+  HessPlan* hp = use_cg ? nullptr : get_hess_plan(W, D, pk);
+  if (!use_cg && !hp) return MNL_ERR_CUDA;
   if (launch_pack(D, pk, X, Z, st) != cudaSuccess) return MNL_ERR_CUDA;
-  hess_plan_design_changed(hp);
+  if (hp) hess_plan_design_changed(hp);
   if (coef0) cudaMemcpyAsync(W.theta, coef0, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
   else cudaMemsetAsync(W.theta, 0, n * sizeof(double), st);
 
@@ -222,10 +251,55 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
   int status = MNL_OK;
   int iters = 0;
   double l = scal[0], g2 = scal[1];
+  bool ftol_met = false;
   while (rc == MNL_OK) {
     if (!std::isfinite(l)) { status = MNL_ERR_NONFINITE; break; }
-    if (std::sqrt(g2) < tol) { status = MNL_OK; break; }         // a8, before forming H (R11)
-    if (iters == max_iter) { status = MNL_MAXITER; break; }
+    // the paper's stopping set, first met ends the fit: gtol is tested
+    // before forming H (R11), ftol after an accepted update, then max_iter
+    if (std::sqrt(g2) < tol) { status = MNL_OK; S.stop_reason = MNL_STOP_GTOL; break; }
+    if (ftol_met) { status = MNL_OK; S.stop_reason = MNL_STOP_FTOL; break; }
+    if (iters == max_iter) { status = MNL_MAXITER; S.stop_reason = MNL_STOP_MAXITER; break; }
+    if (use_cg) {
+      // truncated Newton: CG on (-H) delta = g with H v products, never forming H
+      cudaEventRecord(ev[0], st);
+      double* r = W.cg;
+      double* pv = W.cg + n;
+      double* hpv = W.cg + 2 * n;
+      double* apv = W.cg + 3 * n;
+      double* sc = W.cg + 4 * n;
+      cudaMemsetAsync(W.delta, 0, n * sizeof(double), st);
+      cudaMemcpyAsync(r, W.grad, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(pv, W.grad, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      const double gn = std::sqrt(g2);
+      const double eta = o.cg_rtol > 0.0 ? o.cg_rtol : std::min(0.5, std::sqrt(gn));
+      const int cg_max = o.cg_max_iter > 0 ? o.cg_max_iter : n;
+      double rr = g2;
+      bool fail = false;
+      for (int it = 0; it < cg_max; ++it) {
+        rc = run_hessvec(W, D, ep, X, Y, Z, choice, pv, &pk, hpv, st);
+        if (rc) break;
+        double h2[2];
+        if (launch_cg_curv(n, pv, hpv, apv, sc, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
+        cudaMemcpyAsync(h2, sc, sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
+        const double pAp = h2[0];
+        if (!(pAp > 0.0) || !std::isfinite(pAp)) { fail = it == 0; break; }  // negative curvature
+        const double alpha = rr / pAp;
+        if (launch_cg_update(n, alpha, pv, apv, W.delta, r, sc + 1, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
+        cudaMemcpyAsync(h2 + 1, sc + 1, sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
+        ++S.cg_iters;
+        const double rr_new = h2[1];
+        if (std::sqrt(rr_new) <= eta * gn) break;
+        if (launch_cg_dir(n, rr_new / rr, r, pv, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }
+        rr = rr_new;
+      }
+      cudaEventRecord(ev[1], st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) rc = MNL_ERR_CUDA;
+      if (rc) break;
+      S.hess_ms += elapsed(ev[0], ev[1]);
+      if (fail) { status = MNL_ERR_NOT_SPD; break; }
+    } else {
     cudaEventRecord(ev[0], st);
     if (launch_hessian(hp, D, pk, Y, W.A, n, -1.0, st) != cudaSuccess) { rc = MNL_ERR_CUDA; break; }  // A = -H
     cudaEventRecord(ev[1], st);
@@ -245,6 +319,7 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
       S.gemm_ms += ht[0] + ht[2];  // the beta-beta GEMM: whole tiles + narrow tail
     }
     if (info != 0) { status = MNL_ERR_NOT_SPD; break; }
+    }
     // a7: step halving, accept the first l_j >= l - tau (R7, R8)
     const double tau = 1e-12 * std::max(1.0, std::fabs(l));
     bool accepted = false;
@@ -265,6 +340,8 @@ int fit_impl(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double
     S.halvings += j;
     std::swap(W.theta, W.trial);
     std::swap(W.ctheta, W.ctrial);
+    S.delta_loglik = std::fabs(lt - l);
+    ftol_met = o.ftol > 0.0 && S.delta_loglik < o.ftol;
     l = lt;
     g2 = g2t;
     ++iters;
@@ -331,8 +408,42 @@ int mnl_newton_fit_ex(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, con
                       double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_launches = 0;
-  return fit_impl(N, K, p, f, d, X, Y, Z, choice, coef0, tol, max_iter, coef, iters, loglik, stats,
+  return fit_impl(N, K, p, f, d, X, Y, Z, choice, coef0, default_options(tol, max_iter), coef, iters, loglik, stats,
                   (cudaStream_t)stream);
+}
+
+int mnl_newton_fit_opts(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
+                        const double* Z, const int32_t* choice, const double* coef0, const mnl_fit_options* opts,
+                        double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_launches = 0;
+  if (!opts) return MNL_ERR_ARG;
+  return fit_impl(N, K, p, f, d, X, Y, Z, choice, coef0, *opts, coef, iters, loglik, stats, (cudaStream_t)stream);
+}
+
+int mnl_hessvec(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
+                const double* Z, const int32_t* choice, const double* coef, const double* v, double* hv,
+                void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_launches = 0;
+  Dims D;
+  if (!dims_of(N, K, p, f, d, &D) || !check_inputs(D, X, Y, Z, choice) || !coef || !v || !hv || v == hv)
+    return MNL_ERR_ARG;
+  Workspace& W = g_ws;
+  int rc = init_device(W);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  EvalPlan ep;
+  if (!eval_plan(D, &ep, W.sms)) return MNL_ERR_ARG;
+  Packed pk{};
+  if (!ensure_packed(W, D, &pk)) return MNL_ERR_CUDA;  // for Pr
+  double scal[3];
+  rc = run_eval(W, D, ep, X, Y, Z, choice, coef, &pk, true, nullptr, nullptr, scal, st);  // P_i at coef
+  if (rc) return rc;
+  if (!std::isfinite(scal[0])) return MNL_ERR_NONFINITE;
+  rc = run_hessvec(W, D, ep, X, Y, Z, choice, v, &pk, hv, st);
+  if (rc) return rc;
+  return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
 }
 
 int mnl_newton_fit(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
@@ -396,7 +507,7 @@ int mnl_newton_fit_host(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, c
   cudaMemcpyAsync(W.hch, choice, N * sizeof(int32_t), cudaMemcpyHostToDevice, st);
   if (coef0) cudaMemcpyAsync(W.hcoef, coef0, n * sizeof(double), cudaMemcpyHostToDevice, st);
   rc = fit_impl(N, K, p, f, d, p ? W.hX : nullptr, f ? W.hY : nullptr, d ? W.hZ : nullptr, W.hch,
-                coef0 ? W.hcoef : nullptr, tol, max_iter, W.hcoef, iters, loglik, nullptr, st);
+                coef0 ? W.hcoef : nullptr, default_options(tol, max_iter), W.hcoef, iters, loglik, nullptr, st);
   if (rc != MNL_OK && rc != MNL_MAXITER) return rc;
   cudaMemcpyAsync(coef, W.hcoef, n * sizeof(double), cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return MNL_ERR_CUDA;
@@ -433,7 +544,7 @@ void mnl_release(void) {
   Workspace& W = g_ws;
   hess_plan_destroy(W.hp);
   W.hp = nullptr;
-  double* ds[] = {W.Xp, W.Zp, W.Pr, W.part, W.scal, W.theta, W.trial, W.grad, W.delta, W.A,
+  double* ds[] = {W.Xp, W.Zp, W.Pr, W.part, W.scal, W.theta, W.trial, W.grad, W.delta, W.A, W.cg,
                   W.hX, W.hY, W.hZ, W.hcoef, W.hout, W.hH};
   for (double* p : ds) cudaFree(p);
   cudaFree(W.err);

@@ -294,3 +294,84 @@ def test_fit_from_host_buffers_matches_device():
     coef, iters, ll, rc = M.mnl_newton_fit_host(prob.X, prob.Y, prob.Z, prob.choice, prob.spec.K, tol=1e-8)
     assert rc == M.MNL_OK and iters == r.iters
     assert np.array_equal(coef, r.coef.cpu().numpy()) and ll == r.loglik
+
+
+# --- ftol stop (f2), Hessian-vector products and truncated Newton (f4) -------
+
+HV_CASES = ["c1", "c2", "c3", (999, 7, 5, 3, 2), (300, 33, 3, 1, 1), (700, 3, 64, 5, 16), (2049, 6, 17, 2, 3)]
+
+
+@pytest.mark.parametrize("case", HV_CASES, ids=[str(c) for c in HV_CASES])
+def test_hessvec_parity(case):
+    prob = datagen.make(case) if isinstance(case, str) else datagen.custom(*case, seed=21, coef_sd=0.4,
+                                                                         require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    rng = np.random.default_rng(5)
+    th = datagen.perturbed_theta(prob, 0.1)
+    P = O.probabilities(O.utilities(D, th))
+    for _ in range(2):
+        v = rng.standard_normal(D.n_p)
+        hv_o = O.hessvec(D, th, v, P)
+        hv = M.mnl_hessvec(dp, dev(th), dev(v)).cpu().numpy()
+        assert np.linalg.norm(hv - hv_o) <= 1e-10 * np.linalg.norm(hv_o)
+
+
+def test_hessvec_full_size_c5():
+    prob = datagen.make("c5")
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    v = np.random.default_rng(6).standard_normal(D.n_p)
+    hv_o = O.hessvec(D, prob.theta_true, v)
+    hv = M.mnl_hessvec(dp, dev(prob.theta_true), dev(v)).cpu().numpy()
+    assert np.linalg.norm(hv - hv_o) <= 1e-10 * np.linalg.norm(hv_o)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_ftol_fit_parity(cfg):
+    """The first of gtol / ftol / maxiter ends the fit: same stop, iterations and iterate."""
+    prob = datagen.make(cfg)
+    D = oracle_data(prob)
+    full = O.newton_fit(D, tol=1e-12)
+    dls = [abs(h["l_new"] - h["l"]) for h in full.history]
+    ftol = math_sqrt_mid(dls[1], dls[2]) if len(dls) > 2 else dls[-1] * 1.5
+    f = O.newton_fit(D, tol=1e-12, ftol=ftol)
+    assert f.stop_reason == 2
+    r = M.mnl_newton_fit(device_problem(prob), tol=1e-12, ftol=ftol, max_iter=50)
+    assert r.status == M.MNL_OK and r.stats["stop_reason"] == M.MNL_STOP_FTOL
+    assert r.iters == f.iters
+    assert r.stats["delta_loglik"] == pytest.approx(f.delta_loglik, rel=1e-9)
+    coef = r.coef.cpu().numpy()
+    assert np.linalg.norm(coef - f.coef) <= 1e-10 * np.linalg.norm(f.coef)
+
+
+def math_sqrt_mid(a, b):
+    return float(np.sqrt(a * b))
+
+
+def test_cg_fit_parity_small():
+    prob = datagen.make("c2")
+    D = oracle_data(prob)
+    exact = O.newton_fit(D, tol=1e-8)
+    cg_o = O.newton_cg_fit(D, tol=1e-8)
+    r = M.mnl_newton_fit(device_problem(prob), tol=1e-8, method="cg")
+    assert r.status == M.MNL_OK and r.stats["cg_iters"] > 0
+    coef = r.coef.cpu().numpy()
+    assert np.linalg.norm(coef - exact.coef) <= 1e-8 * np.linalg.norm(exact.coef)
+    assert np.linalg.norm(coef - cg_o.coef) <= 1e-8 * np.linalg.norm(cg_o.coef)
+    assert abs(r.iters - cg_o.iters) <= 1
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_cg_fit_reaches_golden_mle(cfg):
+    """Truncated Newton converges to the same maximum-likelihood estimate as the exact Newton fit
+    of the oracle (the MLE is unique by concavity)."""
+    path = os.path.join(GOLDEN, f"{cfg}_fit.json")
+    g = json.load(open(path))
+    prob = datagen.make(cfg)
+    r = M.mnl_newton_fit(device_problem(prob), tol=g["tol"], method="cg")
+    assert r.status == M.MNL_OK
+    coef = r.coef.cpu().numpy()
+    ref = np.array(g["coef"])
+    assert np.linalg.norm(coef - ref) <= 1e-8 * np.linalg.norm(ref)
+    assert abs(r.loglik - g["loglik"]) <= 1e-10 * abs(g["loglik"])

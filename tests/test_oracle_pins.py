@@ -320,3 +320,71 @@ def test_recovery_of_true_coefficients_c2():
     z = (fit.coef - pr.theta_true) / se
     assert np.max(np.abs(z)) < 5.0
     assert 0.85 < np.sqrt(np.mean(z * z)) < 1.15
+
+
+# --- Hessian-vector products and truncated Newton --------------
+
+@pytest.mark.parametrize("shape", [(150, 4, 3, 2, 1), (120, 3, 2, 0, 2), (100, 5, 2, 3, 0), (90, 4, 0, 2, 0)])
+def test_hessvec_equals_hessian_times_v(shape):
+    N, K, p, f, d = shape
+    prob = tiny(N, K, p, f, d, seed=11)
+    D = data_of(prob)
+    rng = np.random.default_rng(3)
+    th = prob.theta_true + 0.1 * rng.standard_normal(D.n_p)
+    H = O.hessian(D, th)
+    for _ in range(3):
+        v = rng.standard_normal(D.n_p)
+        hv = O.hessvec(D, th, v)
+        assert np.linalg.norm(hv - H @ v) <= 1e-12 * np.linalg.norm(H @ v)
+
+
+def test_hessvec_matches_central_fd_of_gradient():
+    prob = tiny(150, 4, 3, 2, 1, seed=12)
+    D = data_of(prob)
+    rng = np.random.default_rng(4)
+    th = prob.theta_true
+    v = rng.standard_normal(D.n_p)
+    v /= np.linalg.norm(v)
+    eps = 1e-5
+    fd = (O.gradient(D, th + eps * v) - O.gradient(D, th - eps * v)) / (2 * eps)
+    hv = O.hessvec(D, th, v)
+    assert np.linalg.norm(fd - hv) <= 1e-6 * np.linalg.norm(hv)
+
+
+def test_ftol_stop_first_met_semantics():
+    """P:219-221 / P:282-283: the fit ends at the first of gtol, ftol, maxiter; ftol compares
+    successive log-likelihood values after an accepted update."""
+    prob = tiny(400, 4, 3, 2, 1, seed=13)
+    D = data_of(prob)
+    full = O.newton_fit(D, tol=1e-10)
+    assert full.status == O.MNL_OK and full.stop_reason == 1
+    dls = [abs(h["l_new"] - h["l"]) for h in full.history]
+    ftol = 0.5 * (dls[1] + dls[2]) if dls[1] > dls[2] else dls[2] * 1.01   # between the 2nd and 3rd changes
+    fit = O.newton_fit(D, tol=1e-10, ftol=ftol)
+    assert fit.status == O.MNL_OK and fit.stop_reason == 2
+    k = fit.iters
+    assert abs(fit.history[-1]["l_new"] - fit.history[-1]["l"]) < ftol
+    assert all(abs(h["l_new"] - h["l"]) >= ftol for h in fit.history[:-1])
+    assert k < full.iters and np.allclose(fit.coef, O.newton_fit(D, tol=1e-10, max_iter=k).coef, rtol=0, atol=0)
+    assert fit.delta_loglik == pytest.approx(dls[k - 1], rel=0, abs=0)
+
+
+def test_newton_cg_fit_reaches_the_mle():
+    prob = tiny(400, 5, 3, 2, 1, seed=14)
+    D = data_of(prob)
+    exact = O.newton_fit(D, tol=1e-10)
+    cg = O.newton_cg_fit(D, tol=1e-10)
+    assert cg.status == O.MNL_OK and cg.cg_iters > 0
+    assert np.linalg.norm(cg.coef - exact.coef) <= 1e-8 * np.linalg.norm(exact.coef)
+    assert O.np.linalg.norm(O.gradient(D, cg.coef)) < 1e-10
+
+
+def test_newton_cg_with_exhaustive_cg_is_the_newton_step():
+    """CG run to a tiny residual solves (-H) delta = g: the iterates equal exact Newton's."""
+    prob = tiny(300, 4, 2, 1, 1, seed=15)
+    D = data_of(prob)
+    exact = O.newton_fit(D, tol=1e-9)
+    cg = O.newton_cg_fit(D, tol=1e-9, cg_rtol=1e-14)
+    assert cg.iters == exact.iters
+    assert [h["halvings"] for h in cg.history] == [h["halvings"] for h in exact.history]
+    assert np.linalg.norm(cg.coef - exact.coef) <= 1e-10 * np.linalg.norm(exact.coef)
