@@ -47,6 +47,7 @@ void count_launch(int n = 1);
 // Per-CTA partials layout: [2 + n_p] doubles: l_sum, l_comp, grad[n_p].
 struct EvalPlan {
   int grid, block, kpl, cm;
+  int yzs, ns;  // alternative-varying rows staged per warp (bulk copies into an ns-slot ring)
   size_t smem;
   int n_part;  // 2 + n_p
 };

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -37,6 +38,7 @@ __host__ __device__ constexpr int tile_rows(int kpl, bool yz) { return (kpl >= 8
 struct EvalArgs {
   int64_t N;
   int K, p, f, d, q, n_p, off_alpha, off_gamma, QP, XS, TI, SCR;
+  int NS, SLOT;  // YZS path: ring slots per warp, doubles per slot (K (f + d))
   const double* X;
   const double* Y;  // [N][K][f]
   const double* Z;  // [N][K][d]
@@ -57,6 +59,29 @@ __device__ __forceinline__ void neu_add(double& s, double& c, double x) {
   if (fabs(s) >= fabs(x)) c += (s - t) + x;
   else c += (x - t) + s;
   s = t;
+}
+
+// e^x for the shifted utilities x = u - m <= ~0 (a2). x = n ln2 + r (|r| <= ln2/2, Cody-Waite with
+// fdlibm's split ln2, exact n ln2_hi), e^r by its Taylor polynomial to degree 12 (truncation
+// < 2e-16 relative) in Estrin form (short dependency chain), times 2^n built in the exponent field.
+// x < -708 (e^x < 3.3e-308, below the normal range) returns 0; NaN propagates; -inf gives 0.
+__device__ __forceinline__ double exp_shifted(double x) {
+  const double t = rint(x * 1.4426950408889634);
+  double r = fma(t, -6.93147180369123816490e-01, x);
+  r = fma(t, -1.90821492927058770002e-10, r);
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double p01 = 1.0 + r;
+  const double p23 = fma(r, 1.0 / 6.0, 0.5);
+  const double p45 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  const double p67 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+  const double p89 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
+  const double pab = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
+  const double q0 = fma(r2, p23, p01), q1 = fma(r2, p67, p45);
+  const double q2 = fma(r2, pab, p89), q3 = 1.0 / 479001600.0;
+  const double s0 = fma(r4, q1, q0), s1 = fma(r4, q3, q2);
+  const double e = fma(r8, s1, s0);
+  const double scale = __longlong_as_double((long long)(__double2int_rn(t) + 1023) << 52);
+  return x < -708.0 ? 0.0 : e * scale;
 }
 
 __device__ __forceinline__ double warp_max(double v) {
@@ -170,7 +195,7 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
       double ssum = 0.0;
   #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
+        const double e = kok[kk] ? exp_shifted(u[kk] - m) : 0.0;
         ssum += e;
         u[kk] = e;
       }
@@ -344,7 +369,7 @@ __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us,
       double ssum = 0.0;
   #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        const double e = kok[kk] ? exp(u[kk] - m) : 0.0;
+        const double e = kok[kk] ? exp_shifted(u[kk] - m) : 0.0;
         ssum += e;
         u[kk] = e;
       }
@@ -424,7 +449,238 @@ __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us,
   }
 }
 
-template <int KPL, int CM_MAX, bool HV>
+// ---- Phase E with the alternative-varying rows staged in shared memory (YZS path) -----------
+// Every warp streams the Y and Z rows of ITS OWN individuals (one contiguous K f and K d block
+// each) into a private ring of NS slots with cp.async.bulk (mbarrier complete_tx), NS - 1
+// individuals ahead of the one it computes: the reads from HBM are whole 16-byte-multiple blocks
+// and lane k then reads alternative k's f (16-byte pairs) and d values from shared memory.
+// Conditions (eval_plan): KPL <= 2, f even <= 16, d <= 8, K f and K d even.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {  // a: shared address
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// Per-warp state of the YZS pipeline: this warp's rows in tile order form a sequence s = 0, 1, ...
+// (R = TI / NW rows per tile); position s lives in ring slot s mod NS.
+struct YzsState {
+  unsigned ring_s, bar_s;  // shared addresses of this warp's ring and mbarriers
+  int slot, par;           // consume pointer: slot and phase parity of the next row
+  int s_issue, slot_i;     // next position to stage and its slot (lane 0 only)
+  int lg_cnt;              // deferred logs: lane lg_cnt receives the next individual's (uy - m, s)
+  double lg_a, lg_s;
+};
+// lane 0: stage the next position of this warp's sequence (if it exists)
+template <int R>
+__device__ __forceinline__ void yzs_issue(const EvalArgs& A, YzsState& st, int w) {
+  const int s = st.s_issue;
+  const int64_t gi = (blockIdx.x + (int64_t)(s / R) * gridDim.x) * A.TI + w * R + (s % R);
+  if (gi >= A.N) return;
+  const unsigned by = (unsigned)A.K * A.f * 8u, bz = (unsigned)A.K * A.d * 8u;
+  const unsigned bar = st.bar_s + 8u * st.slot_i;
+  const unsigned dst = st.ring_s + 8u * (unsigned)(st.slot_i * A.SLOT);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's previous generic reads
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(by + bz) : "memory");
+  if (by)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(A.Y + gi * A.K * A.f), "r"(by), "r"(bar)
+                 : "memory");
+  if (bz)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + by),
+                 "l"(A.Z + gi * A.K * A.d), "r"(bz), "r"(bar)
+                 : "memory");
+  st.s_issue = s + 1;
+  st.slot_i = (st.slot_i + 1 == A.NS) ? 0 : st.slot_i + 1;
+}
+
+constexpr int YZS_F = 16, YZS_D = 8;  // register capacity of the YZS path (gamma, alpha partials)
+
+template <int KPL, bool HV>
+__device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, const int* ch_t, double* red,
+                                             const double (&acoef)[KPL][YZS_D], const double* gamma,
+                                             double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
+                                             int64_t i0, int nt, int KPS, int w, int lane, const double* ring_w,
+                                             YzsState& st) {
+  constexpr int R = tile_rows(KPL, true) / NW;
+  const int K = A.K, d = A.d, f = A.f;
+  const int ib = w * R;
+  const int n_mine = min(R, nt - ib);
+  for (int ii = ib + max(n_mine, 0); ii < ib + R; ++ii)  // ragged tail: zero residual rows
+    for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
+  bool kok[KPL];
+#pragma unroll
+  for (int kk = 0; kk < KPL; ++kk) kok[kk] = lane + 32 * kk < K;
+  for (int jj = 0; jj < n_mine; ++jj) {
+    __syncwarp();
+    if (lane == 0) yzs_issue<R>(A, st, w);  // into the slot the previous row just released
+    const int ii = ib + jj;
+    const int64_t gi = i0 + ii;
+    int y = ch_t[ii];
+    if (y < 0 || y >= K) {
+      if (lane == 0) atomicOr(A.err, 1);
+      y = 0;
+    }
+    double ua[KPL], ub[KPL];
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk) {
+      ua[kk] = kok[kk] ? Rs[ii * KPS + lane + 32 * kk] : 0.0;
+      ub[kk] = 0.0;
+    }
+    mbar_wait(st.bar_s + 8u * st.slot, (unsigned)st.par);
+    const double* ys = ring_w + st.slot * A.SLOT;  // [K][f]
+    const double* zs = ys + K * f;                 // [K][d]
+    if (++st.slot == A.NS) {
+      st.slot = 0;
+      st.par ^= 1;
+    }
+    // ---- u_k += y_k . gamma + z_k . alpha_k ----
+#pragma unroll
+    for (int e = 0; e < YZS_F; e += 2) {
+      if (e < f) {
+        const double g0 = gamma[e], g1 = gamma[e + 1];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          const double2 v = kok[kk] ? *reinterpret_cast<const double2*>(ys + (lane + 32 * kk) * f + e)
+                                    : make_double2(0.0, 0.0);
+          ua[kk] = fma(v.x, g0, ua[kk]);
+          ub[kk] = fma(v.y, g1, ub[kk]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < YZS_D; ++c) {
+      if (c < d) {
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          const double z = kok[kk] ? zs[(lane + 32 * kk) * d + c] : 0.0;
+          if (c & 1) ub[kk] = fma(z, acoef[kk][c], ub[kk]);
+          else ua[kk] = fma(z, acoef[kk][c], ua[kk]);
+        }
+      }
+    }
+    double u[KPL], r[KPL];
+    if constexpr (HV) {  // Hessian-vector product: s_k = ua + ub, r_k = -P_k (s_k - sum_l P_l s_l)
+      double ps = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        u[kk] = kok[kk] ? __ldg(A.Pr + gi * A.ldP + lane + 32 * kk) : 0.0;
+        ps = fma(u[kk], ua[kk] + ub[kk], ps);
+      }
+      ps = warp_sum(ps);
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        r[kk] = kok[kk] ? -u[kk] * ((ua[kk] + ub[kk]) - ps) : 0.0;
+        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+      }
+    } else {
+      // shift by the (fp32-rounded) maximum: any shift is exact for the softmax; this one only has
+      // to keep e^{u - m} <= ~1 (R12), so the cross-lane max runs on 32-bit shuffles
+      float mf = -INFINITY;
+      double uy_l = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
+        if (k == y) uy_l = u[kk];
+        mf = fmaxf(mf, (float)u[kk]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+      const double m = (double)mf;
+      double ssum = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const double e = kok[kk] ? exp_shifted(u[kk] - m) : 0.0;
+        ssum += e;
+        u[kk] = e;
+      }
+      ssum = warp_sum(ssum);
+      const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
+      // l_i = uy - m - log s: lane lg_cnt keeps (uy - m, s); every 32 individuals each lane takes one log
+      if (lane == st.lg_cnt) {
+        st.lg_a = uy - m;
+        st.lg_s = ssum;
+      }
+      if (++st.lg_cnt == 32) {
+        neu_add(l_s, l_c, st.lg_a - log(st.lg_s));
+        st.lg_cnt = 0;
+      }
+      const double inv_s = 1.0 / ssum;
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk) {
+        const int k = lane + 32 * kk;
+        const double P = u[kk] * inv_s;
+        u[kk] = P;
+        r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
+        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+        if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+      }
+    }
+    // ---- ybar_e = sum_k P_k y_ke (writeP), gamma partials sum_k y_ke r_k, alpha partials z_kc r_k ----
+    double yb[YZS_F];
+#pragma unroll
+    for (int e = 0; e < YZS_F; e += 2) {
+      yb[e] = yb[e + 1] = 0.0;
+      if (e < f) {
+        double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          const double2 v = kok[kk] ? *reinterpret_cast<const double2*>(ys + (lane + 32 * kk) * f + e)
+                                    : make_double2(0.0, 0.0);
+          yb[e] = fma(u[kk], v.x, yb[e]);
+          yb[e + 1] = fma(u[kk], v.y, yb[e + 1]);
+          g0 = fma(v.x, r[kk], g0);
+          g1 = fma(v.y, r[kk], g1);
+        }
+        gam[e] += g0;
+        gam[e + 1] += g1;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < YZS_D; ++c) {
+      if (c < d) {
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          const double z = kok[kk] ? zs[(lane + 32 * kk) * d + c] : 0.0;
+          alp[kk][c] = fma(z, r[kk], alp[kk][c]);
+        }
+      }
+    }
+    if (!HV && A.writeP) {
+      // cross-lane ybar sums, 8 components per round through red[8][33]
+#pragma unroll
+      for (int e0 = 0; e0 < YZS_F; e0 += 8) {
+        if (e0 < f) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) red[t * 33 + lane] = yb[e0 + t];
+          __syncwarp();
+          const int t = lane >> 2, j = lane & 3;
+          double sacc = 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) sacc += red[t * 33 + j * 8 + q];
+          sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+          sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+          if (j == 0 && e0 + t < f) A.Pr[gi * A.ldP + K + e0 + t] = sacc;
+          __syncwarp();
+        }
+      }
+    }
+  }
+}
+
+template <int KPL, int CM_MAX, bool HV, bool YZS>
 __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   extern __shared__ __align__(16) double sm[];
   constexpr int KP = 32 * KPL, KPS = KP + 4;   // alternatives padded; smem row stride = 4 (mod 16)
@@ -437,22 +693,55 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   double* Bs = sm;                              // [QP][KPS]  Bs[a][k] = beta_k[a]
   double* Xs = Bs + QP * KPS;                   // [2][TI][XS] x~ tiles (col 0 = 1)
   double* Rs = Xs + 2 * TI * XS;                // [TI][KPS]  residuals
-  double* Ps = Rs + TI * KPS;                   // [TI][KPS]  probabilities (only with Y)
-  double* Wa = Ps + ((d + f) ? TI * KPS : 0);   // [NW][KPL][d][32] alpha-gradient, lane-private,
-                                                // then [NW][f][32] gamma-gradient (e >= 8)
-  double* Cf = Wa + NW * KPL * d * 32 + NW * f * 32;  // [K*d + f]  alpha, gamma
+  // [TI][KPS] utilities from phase B (YZS: in place in Rs, each lane overwrites its own u by r)
+  double* Ps = YZS ? Rs : Rs + TI * KPS;
+  double* Wa = Rs + ((d + f) && !YZS ? 2 * TI * KPS : TI * KPS);  // [NW][KPL][d][32] alpha-gradient,
+                                                // lane-private, then [NW][f][32] gamma-gradient (e >= 8)
+  double* Cf = Wa + (YZS ? 0 : NW * KPL * d * 32 + NW * f * 32);  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
   double* Red = Cf + K * d + f + 1 + TI;                  // [NW][8][33] ybar reductions
+  // YZS: per-warp mbarriers [NW][NS] and rings [NW][NS][SLOT] (16-byte aligned)
+  const int red_end = (int)(Red - sm) + ((d + f) ? NW * 8 * 33 : 0);
+  uint64_t* Bar = reinterpret_cast<uint64_t*>(sm + ((red_end + 1) & ~1));
+  double* Ring = sm + ((red_end + 1) & ~1) + NW * A.NS;
 
   for (int idx = tid; idx < QP * KPS; idx += blockDim.x) {
     const int a = idx / KPS, k = idx - a * KPS;
     Bs[idx] = (a < q && k >= 1 && k < K) ? A.coef[(k - 1) * q + a] : 0.0;
   }
   for (int idx = tid; idx < 2 * TI * XS; idx += blockDim.x) Xs[idx] = ((idx % XS) == 0) ? 1.0 : 0.0;
-  for (int idx = tid; idx < NW * KPL * d * 32 + NW * f * 32; idx += blockDim.x) Wa[idx] = 0.0;
+  if (!YZS)
+    for (int idx = tid; idx < NW * KPL * d * 32 + NW * f * 32; idx += blockDim.x) Wa[idx] = 0.0;
   for (int idx = tid; idx < K * d + f; idx += blockDim.x) Cf[idx] = A.coef[A.off_alpha + idx];
   const double* alpha = Cf;
   const double* gamma = Cf + K * d;
+  // YZS: this lane's alpha_k coefficients and alpha / gamma gradient partials live in registers
+  double acoef[YZS ? KPL : 1][YZS_D], alp[YZS ? KPL : 1][YZS_D], gamz[YZS_F];
+  YzsState yst;
+  if constexpr (YZS) {
+    yst.ring_s = static_cast<unsigned>(__cvta_generic_to_shared(Ring + (size_t)w * A.NS * A.SLOT));
+    yst.bar_s = static_cast<unsigned>(__cvta_generic_to_shared(Bar + w * A.NS));
+    yst.slot = yst.par = yst.s_issue = yst.slot_i = yst.lg_cnt = 0;
+    yst.lg_a = 0.0;
+    yst.lg_s = 1.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk)
+#pragma unroll
+      for (int c = 0; c < YZS_D; ++c) {
+        const int k = lane + 32 * kk;
+        acoef[kk][c] = (k < K && c < d) ? A.coef[A.off_alpha + k * d + c] : 0.0;
+        alp[kk][c] = 0.0;
+      }
+#pragma unroll
+    for (int e = 0; e < YZS_F; ++e) gamz[e] = 0.0;
+    if (lane == 0) {
+      for (int j = 0; j < A.NS; ++j) mbar_init(Bar + w * A.NS + j, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0)  // only lane 0 tracks the issue pointer
+      for (int j = 0; j < A.NS - 1; ++j) yzs_issue<tile_rows(KPL, true) / NW>(A, yst, w);
+  }
 
   // phase-C warp grid over (m-blocks of a, n-blocks of k)
   const int MB = QP / 8 + ((QP & 7) ? 1 : 0);
@@ -490,7 +779,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
                    "l"(A.choice + i0 + i)
                    : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
-    if (tid == 0) {  // warm L2 with the tile's alternative-varying rows (contiguous blocks)
+    if (!YZS && tid == 0) {  // warm L2 with the tile's alternative-varying rows (contiguous blocks)
       const double* blk[2] = {f ? A.Y + i0 * K * f : nullptr, d ? A.Z + i0 * K * d : nullptr};
       const int64_t len[2] = {(int64_t)nt * K * f * 8, (int64_t)nt * K * d * 8};
       for (int b = 0; b < 2; ++b) {
@@ -544,7 +833,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
       }
       __syncthreads();
       bool done = false;
-      if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
+      if constexpr (YZS) {
+        phase_e_smem<KPL, HV>(A, Rs, ch_t, Red + w * (8 * 33), acoef, gamma, gamz, alp, l_s, l_c, i0, nt, KPS, w,
+                              lane, Ring + (size_t)w * A.NS * A.SLOT, yst);
+        done = true;
+      } else if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
         if ((f + d) * KPL <= 32) {
           phase_e_reg<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
           done = true;
@@ -602,7 +895,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
       for (int h = 0; h < 2; ++h) {
         const int k = nb * 8 + 2 * r4 + h;
         if (k == y) uy = u[nb][h];
-        const double e = (k < K) ? exp(u[nb][h] - m) : 0.0;
+        const double e = (k < K) ? exp_shifted(u[nb][h] - m) : 0.0;
         u[nb][h] = e;
         ssum += e;
       }
@@ -658,6 +951,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   }
 
   // ---------------- CTA partials (fixed order) ----------------
+  if constexpr (YZS)
+    if (lane < yst.lg_cnt) neu_add(l_s, l_c, yst.lg_a - log(yst.lg_s));  // the deferred logs left over
   __syncthreads();
   double* out = A.part + (size_t)blockIdx.x * A.n_part;
   double* scratch = Rs;  // reuse
@@ -667,7 +962,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   __syncthreads();
   if (tid == 0) {
     double s = 0.0, c = 0.0;
-    for (int t = 0; t < NW * 32; t += 4) { neu_add(s, c, scratch[2 * t]); neu_add(s, c, scratch[2 * t + 1]); }
+    for (int t = 0; t < NW * 32; t += (YZS ? 1 : 4)) { neu_add(s, c, scratch[2 * t]); neu_add(s, c, scratch[2 * t + 1]); }
     out[0] = s;
     out[1] = c;
   }
@@ -686,6 +981,34 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
           if (a < q && k >= 1 && k < K) out[2 + (k - 1) * q + a] = G[mi][j][h];
         }
     }
+  }
+  if constexpr (YZS) {
+    // alpha / gamma register partials -> the (drained) rings as [NW][KPL][d][32] + [NW][f][32],
+    // then fixed-order sums over warps and lanes
+    double* sa = Ring;
+    double* sg = Ring + NW * KPL * d * 32;
+#pragma unroll
+    for (int kk = 0; kk < KPL; ++kk)
+#pragma unroll
+      for (int c = 0; c < YZS_D; ++c)
+        if (c < d) sa[((w * KPL + kk) * d + c) * 32 + lane] = alp[kk][c];
+#pragma unroll
+    for (int e = 0; e < YZS_F; ++e)
+      if (e < f) sg[(w * f + e) * 32 + lane] = gamz[e];
+    __syncthreads();
+    for (int idx = tid; idx < K * d; idx += blockDim.x) {
+      const int k = idx / d, c = idx - k * d, kk = k >> 5, ln = k & 31;
+      double v = 0.0;
+      for (int ww = 0; ww < NW; ++ww) v += sa[((ww * KPL + kk) * d + c) * 32 + ln];
+      out[2 + A.off_alpha + idx] = v;
+    }
+    for (int e = tid; e < f; e += blockDim.x) {
+      double v = 0.0;
+      for (int ww = 0; ww < NW; ++ww)
+        for (int ln = 0; ln < 32; ++ln) v += sg[(ww * f + e) * 32 + ln];
+      out[2 + A.off_gamma + e] = v;
+    }
+    return;
   }
   // register partials of gamma components 8..15 into Wa (each (warp, lane) slot is private)
 #pragma unroll
@@ -790,16 +1113,16 @@ __global__ void k_axpy_pow2(int n, const double* theta, const double* delta, int
   if (r < n) out[r] = theta[r] + ldexp(delta[r], -j);  // a7: theta + delta / 2^j, exact scaling
 }
 
-template <int KPL, int CM, bool HV>
+template <int KPL, int CM, bool HV, bool YZS>
 cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM, HV, YZS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  k_eval_kernel<KPL, CM, HV><<<plan.grid, plan.block, plan.smem, st>>>(a);
+  k_eval_kernel<KPL, CM, HV, YZS><<<plan.grid, plan.block, plan.smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
@@ -856,12 +1179,19 @@ __global__ void __launch_bounds__(1024) k_cg_dir(int n, double beta, const doubl
 static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
-static size_t eval_smem(const Dims& D, int kpl) {
+static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns) {
   const int KP = 32 * kpl, KPS = KP + 4, TI = tile_rows(kpl, (D.d + D.f) > 0);
-  const size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
-                   ((D.d + D.f) ? (size_t)TI * KPS : 0) + (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32 +
-                   (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
-                   ((D.d + D.f) ? (size_t)NW * 8 * 33 : 0);
+  size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
+             ((D.d + D.f) && !yzs ? (size_t)TI * KPS : 0) +
+             (yzs ? 0 : (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32) +
+             (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
+             ((D.d + D.f) ? (size_t)NW * 8 * 33 : 0);
+  if (yzs) {
+    n = (n + 1) & ~(size_t)1;
+    const size_t ring = (size_t)NW * ns * D.K * (D.f + D.d);
+    const size_t scr = (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32;  // finalisation scratch
+    n += (size_t)NW * ns + (ring > scr ? ring : scr);
+  }
   return n * sizeof(double);
 }
 
@@ -876,7 +1206,24 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   while (cm < (mb + wm - 1) / wm) cm *= 2;
   if (cm > 8 || 2 * cm * cn + 2 * nbn > 96) return false;
   plan->cm = cm;
-  size_t smem = eval_smem(D, kpl);
+  // YZS (alternative-varying rows staged per warp with bulk copies): f even <= 16, d <= 8, whole
+  // 16-byte rows (K f, K d even), K <= 64; 3 ring slots if they fit, else 2
+  plan->yzs = 0;
+  plan->ns = 0;
+  const bool yzs_ok = (D.d + D.f) > 0 && kpl <= 2 && D.f % 2 == 0 && D.f <= YZS_F && D.d <= YZS_D &&
+                      (D.K * D.f) % 2 == 0 && (D.K * D.d) % 2 == 0 && !getenv("MNL_NO_YZS");
+  size_t smem = eval_smem(D, kpl, false, 0);
+  if (yzs_ok) {
+    for (int ns = 3; ns >= 2; --ns) {
+      const size_t sz = eval_smem(D, kpl, true, ns);
+      if (sz <= 227 * 1024) {
+        plan->yzs = 1;
+        plan->ns = ns;
+        smem = sz;
+        break;
+      }
+    }
+  }
   if (smem > 227 * 1024) return false;  // sm_100a opt-in maximum (232448 bytes)
   plan->kpl = kpl;
   plan->smem = smem;
@@ -903,22 +1250,34 @@ static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const d
   a.ldP = (writeP || hv) ? pk->ldP : 0;
   a.want_grad = want_grad; a.writeP = writeP && !hv;
   a.part = part; a.n_part = plan.n_part; a.err = err;
-#define MNL_EVAL_CASE(KPL_)                                                                   \
-  case KPL_:                                                                                  \
-    if (hv) {                                                                                 \
-      if (plan.cm == 2) return launch_k<KPL_, 2, true>(plan, a, st);                          \
-      if (plan.cm == 4) return launch_k<KPL_, 4, true>(plan, a, st);                          \
-      return launch_k<KPL_, 8, true>(plan, a, st);                                            \
-    }                                                                                         \
-    if (plan.cm == 2) return launch_k<KPL_, 2, false>(plan, a, st);                           \
-    if (plan.cm == 4) return launch_k<KPL_, 4, false>(plan, a, st);                           \
-    return launch_k<KPL_, 8, false>(plan, a, st);
+  a.NS = plan.ns;
+  a.SLOT = D.K * (D.f + D.d);
+#define MNL_EVAL_CM(KPL_, HV_, YZS_)                                                         \
+  if (plan.cm == 2) return launch_k<KPL_, 2, HV_, YZS_>(plan, a, st);                        \
+  if (plan.cm == 4) return launch_k<KPL_, 4, HV_, YZS_>(plan, a, st);                        \
+  return launch_k<KPL_, 8, HV_, YZS_>(plan, a, st);
+#define MNL_EVAL_CASE(KPL_)                                                                  \
+  case KPL_:                                                                                 \
+    if (hv) { MNL_EVAL_CM(KPL_, true, false) }                                               \
+    MNL_EVAL_CM(KPL_, false, false)
+  if (plan.yzs) {
+    if (plan.kpl == 1) {
+      if (hv) { MNL_EVAL_CM(1, true, true) }
+      MNL_EVAL_CM(1, false, true)
+    }
+    if (plan.kpl == 2) {
+      if (hv) { MNL_EVAL_CM(2, true, true) }
+      MNL_EVAL_CM(2, false, true)
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (plan.kpl) {
     MNL_EVAL_CASE(1)
     MNL_EVAL_CASE(2)
     MNL_EVAL_CASE(4)
     MNL_EVAL_CASE(8)
   }
+#undef MNL_EVAL_CM
 #undef MNL_EVAL_CASE
   return cudaErrorInvalidValue;
 }

@@ -89,6 +89,8 @@ SHAPES = [  # ragged N (not a multiple of the 32/64-row tiles), K at KPL boundar
     (999, 7, 5, 3, 2), (300, 32, 4, 0, 0), (300, 33, 3, 1, 1), (200, 64, 2, 2, 0), (150, 65, 1, 0, 1),
     (70, 129, 2, 0, 0), (40, 256, 1, 1, 1), (2049, 6, 17, 2, 3), (5000, 9, 63, 0, 0), (700, 3, 64, 5, 16),
     (300, 4, 10, 64, 0),
+    # staged alternative-varying rows (YZS path): ragged N, odd K, f at its 16 limit (2 ring slots)
+    (77, 9, 3, 4, 2), (45, 31, 0, 6, 0), (500, 50, 2, 16, 8), (129, 64, 1, 2, 1),
 ]
 
 
@@ -104,6 +106,30 @@ def test_eval_parity_shapes(shape):
         check_lg(l, g, l_o, g_o)
         assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
         assert np.array_equal(H, H.T)
+
+
+@pytest.mark.parametrize("mode", ["default", "MNL_NO_YZS"])
+def test_eval_yz_paths(mode):
+    """Pass 1 with alternative-varying data: rows staged per warp in shared memory (YZS, bulk
+    copies) and the direct L1 path, both against the oracle (loglik, gradient, P through the Hessian)
+    and through the Hessian-vector product."""
+    if mode != "default":
+        os.environ[mode] = "1"
+    try:
+        for N, K, p, f, d in [(1000, 4, 3, 2, 1), (333, 50, 5, 10, 5), (2049, 6, 17, 2, 3), (65, 20, 0, 4, 0)]:
+            prob = datagen.custom(N, K, p, f, d, seed=7, coef_sd=0.3, require_all_classes=False)
+            D = oracle_data(prob)
+            dp = device_problem(prob)
+            th = datagen.perturbed_theta(prob, 0.2)
+            l_o, g_o, H_o = O.mnl_eval(D, th)
+            l, g, H = gpu_eval(dp, th)
+            check_lg(l, g, l_o, g_o)
+            assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+            v = np.random.default_rng(3).standard_normal(D.n_p)
+            hv = M.mnl_hessvec(dp, dev(th), dev(v)).cpu().numpy()
+            assert np.linalg.norm(hv - H_o @ v) <= 1e-10 * np.linalg.norm(H_o @ v)
+    finally:
+        os.environ.pop(mode, None)
 
 
 # Shapes that select each GEMM kernel: J2 materialised (K d + f >= 192) with a generated J1;

@@ -25,9 +25,18 @@ def main():
                    torch.from_numpy(prob.choice.astype(np.int32)).to(dev), K=s.K)
     th = torch.from_numpy(prob.theta_true).to(dev)
     for r in range(reps):
-        if mode == "fit":
-            f = M.mnl_newton_fit(dp, tol=1e-6)
-            print(cfg, "fit", f.iters, f.loglik, f.stats, flush=True)
+        if mode in ("fit", "fitcg"):
+            f = M.mnl_newton_fit(dp, tol=1e-6, method="cg" if mode == "fitcg" else "newton")
+            print(cfg, mode, f.iters, f.loglik, f.stats, flush=True)
+        elif mode == "hv":
+            v = th.clone()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            M.mnl_eval(dp, th, grad=True, hess=False)
+            e0.record()
+            hv = M.mnl_hessvec(dp, th, v)
+            e1.record()
+            torch.cuda.synchronize()
+            print(cfg, "hessvec ms %.3f" % e0.elapsed_time(e1), flush=True)
         else:
             ll, g, H = M.mnl_eval(dp, th, grad=True, hess=True)
             torch.cuda.synchronize()
