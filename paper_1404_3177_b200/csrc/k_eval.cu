@@ -84,6 +84,30 @@ __device__ __forceinline__ double exp_shifted(double x) {
   return x < -708.0 ? 0.0 : e * scale;
 }
 
+// Sums of 8 per-lane values over the warp (reduce-scatter by butterfly): returns, in every lane, the
+// warp sum of component (lane >> 2) & 7.
+__device__ __forceinline__ double warp_sum8(const double (&v)[8], int lane) {
+  const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+  double a[4], b[2], c;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {  // xor 16: keep components 4 h4 .. 4 h4 + 3
+    const double keep = h4 ? v[4 + t] : v[t], send = h4 ? v[t] : v[4 + t];
+    a[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {  // xor 8: keep 2 of them
+    const double keep = h3 ? a[2 + t] : a[t], send = h3 ? a[t] : a[2 + t];
+    b[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {  // xor 4: keep 1
+    const double keep = h2 ? b[1] : b[0], send = h2 ? b[0] : b[1];
+    c = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  c += __shfl_xor_sync(0xffffffffu, c, 1);
+  return c;  // component 4 h4 + 2 h3 + h2
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -472,24 +496,26 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {  // a: 
       : "memory");
 }
 // Per-warp state of the YZS pipeline: this warp's rows in tile order form a sequence s = 0, 1, ...
-// (R = TI / NW rows per tile); position s lives in ring slot s mod NS.
+// (YZS_R = YZS_TI / NW rows per tile); position s lives in ring slot s mod NS.
+constexpr int NWY = 8;  // warps per CTA of the YZS kernel
+constexpr int YZS_TI = 16, YZS_R = YZS_TI / NWY;
 struct YzsState {
   unsigned ring_s, bar_s;  // shared addresses of this warp's ring and mbarriers
   int slot, par;           // consume pointer: slot and phase parity of the next row
+  int s_cur;               // sequence position of the next row to compute
   int s_issue, slot_i;     // next position to stage and its slot (lane 0 only)
   int lg_cnt;              // deferred logs: lane lg_cnt receives the next individual's (uy - m, s)
   double lg_a, lg_s;
 };
-// lane 0: stage the next position of this warp's sequence (if it exists)
-template <int R>
-__device__ __forceinline__ void yzs_issue(const EvalArgs& A, YzsState& st, int w) {
+// lane 0: stage the next position of this warp's sequence; false if it does not exist
+__device__ __forceinline__ bool yzs_issue(const EvalArgs& A, YzsState& st, int w) {
   const int s = st.s_issue;
-  const int64_t gi = (blockIdx.x + (int64_t)(s / R) * gridDim.x) * A.TI + w * R + (s % R);
-  if (gi >= A.N) return;
+  const int64_t gi = (blockIdx.x + (int64_t)(s / YZS_R) * gridDim.x) * YZS_TI + w * YZS_R + (s % YZS_R);
+  if (gi >= A.N) return false;
   const unsigned by = (unsigned)A.K * A.f * 8u, bz = (unsigned)A.K * A.d * 8u;
   const unsigned bar = st.bar_s + 8u * st.slot_i;
   const unsigned dst = st.ring_s + 8u * (unsigned)(st.slot_i * A.SLOT);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's previous generic reads
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's previous generic accesses
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(by + bz) : "memory");
   if (by)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -502,190 +528,317 @@ __device__ __forceinline__ void yzs_issue(const EvalArgs& A, YzsState& st, int w
                  : "memory");
   st.s_issue = s + 1;
   st.slot_i = (st.slot_i + 1 == A.NS) ? 0 : st.slot_i + 1;
+  return true;
 }
 
 constexpr int YZS_F = 16, YZS_D = 8;  // register capacity of the YZS path (gamma, alpha partials)
 
-template <int KPL, bool HV>
-__device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, const int* ch_t, double* red,
-                                             const double (&acoef)[KPL][YZS_D], const double* gamma,
-                                             double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
-                                             int64_t i0, int nt, int KPS, int w, int lane, const double* ring_w,
-                                             YzsState& st) {
-  constexpr int R = tile_rows(KPL, true) / NW;
+// NI consecutive rows of this warp (ii0 ..), computed together so that their dependency chains
+// (loads -> utilities -> max / sum shuffles -> exp -> gradient sums) interleave. Lane k holds
+// alternatives k + 32 kk. Reads its rows' staged Y [K][f] and Z [K][d] from the ring.
+template <int KPL, bool HV, int NI>
+__device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const int* ch_t, double* red_w,
+                                         const double* alpha, const double* gamma,
+                                         double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
+                                         int64_t i0, int ii0, int KPS, int w, int lane, const double* ring_w,
+                                         YzsState& st) {
   const int K = A.K, d = A.d, f = A.f;
-  const int ib = w * R;
-  const int n_mine = min(R, nt - ib);
-  for (int ii = ib + max(n_mine, 0); ii < ib + R; ++ii)  // ragged tail: zero residual rows
-    for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
-  bool kok[KPL];
+  bool kok[KPL];  // lane's alternatives exist (always for kk < KPL - 1: K > 32 (KPL - 1))
 #pragma unroll
-  for (int kk = 0; kk < KPL; ++kk) kok[kk] = lane + 32 * kk < K;
-  for (int jj = 0; jj < n_mine; ++jj) {
-    __syncwarp();
-    if (lane == 0) yzs_issue<R>(A, st, w);  // into the slot the previous row just released
-    const int ii = ib + jj;
-    const int64_t gi = i0 + ii;
-    int y = ch_t[ii];
-    if (y < 0 || y >= K) {
-      if (lane == 0) atomicOr(A.err, 1);
-      y = 0;
+  for (int kk = 0; kk < KPL; ++kk) kok[kk] = (kk < KPL - 1) || (lane + 32 * kk < K);
+  __syncwarp();
+  if (lane == 0)  // stage ahead into the slots released by the previous rows
+    while (st.s_issue <= st.s_cur + A.NS - 1 && yzs_issue(A, st, w)) {
     }
-    double ua[KPL], ub[KPL];
+  int y[NI];
+  int64_t gi[NI];
+  double ua[NI][KPL], ub[NI][KPL];
+  const double* ys[NI];
+  const double* zs[NI];
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    const int ii = ii0 + j;
+    gi[j] = i0 + ii;
+    y[j] = ch_t[ii];
+    if (y[j] < 0 || y[j] >= K) {
+      if (lane == 0) atomicOr(A.err, 1);
+      y[j] = 0;
+    }
 #pragma unroll
     for (int kk = 0; kk < KPL; ++kk) {
-      ua[kk] = kok[kk] ? Rs[ii * KPS + lane + 32 * kk] : 0.0;
-      ub[kk] = 0.0;
+      ua[j][kk] = kok[kk] ? Rs[ii * KPS + lane + 32 * kk] : 0.0;
+      ub[j][kk] = 0.0;
     }
+  }
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
     mbar_wait(st.bar_s + 8u * st.slot, (unsigned)st.par);
-    const double* ys = ring_w + st.slot * A.SLOT;  // [K][f]
-    const double* zs = ys + K * f;                 // [K][d]
+    ys[j] = ring_w + st.slot * A.SLOT;  // [K][f]
+    zs[j] = ys[j] + K * f;              // [K][d]
     if (++st.slot == A.NS) {
       st.slot = 0;
       st.par ^= 1;
     }
-    // ---- u_k += y_k . gamma + z_k . alpha_k ----
+  }
+  st.s_cur += NI;
+  // ---- u_k += y_k . gamma + z_k . alpha_k (components in chunks of 4: all loads of a chunk first) ----
 #pragma unroll
-    for (int e = 0; e < YZS_F; e += 2) {
-      if (e < f) {
-        const double g0 = gamma[e], g1 = gamma[e + 1];
+  for (int e = 0; e < YZS_F; e += 4) {
+    if (e + 4 <= f) {
+      double2 v[2][NI][KPL];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk)
+            v[h][j][kk] = kok[kk] ? *reinterpret_cast<const double2*>(ys[j] + (lane + 32 * kk) * f + e + 2 * h)
+                                  : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double g0 = gamma[e + 2 * h], g1 = gamma[e + 2 * h + 1];
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk) {
+            ua[j][kk] = fma(v[h][j][kk].x, g0, ua[j][kk]);
+            ub[j][kk] = fma(v[h][j][kk].y, g1, ub[j][kk]);
+          }
+      }
+    } else if (e < f) {  // the last 2 (f even)
+      const double g0 = gamma[e], g1 = gamma[e + 1];
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
-          const double2 v = kok[kk] ? *reinterpret_cast<const double2*>(ys + (lane + 32 * kk) * f + e)
+          const double2 v = kok[kk] ? *reinterpret_cast<const double2*>(ys[j] + (lane + 32 * kk) * f + e)
                                     : make_double2(0.0, 0.0);
-          ua[kk] = fma(v.x, g0, ua[kk]);
-          ub[kk] = fma(v.y, g1, ub[kk]);
+          ua[j][kk] = fma(v.x, g0, ua[j][kk]);
+          ub[j][kk] = fma(v.y, g1, ub[j][kk]);
         }
-      }
     }
+  }
 #pragma unroll
-    for (int c = 0; c < YZS_D; ++c) {
-      if (c < d) {
+  for (int c0 = 0; c0 < YZS_D; c0 += 4) {
+    if (c0 + 4 <= d) {
+      double z[4][NI][KPL], ac[4][KPL];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
-          const double z = kok[kk] ? zs[(lane + 32 * kk) * d + c] : 0.0;
-          if (c & 1) ub[kk] = fma(z, acoef[kk][c], ub[kk]);
-          else ua[kk] = fma(z, acoef[kk][c], ua[kk]);
+          ac[t][kk] = kok[kk] ? alpha[(lane + 32 * kk) * d + c0 + t] : 0.0;
+#pragma unroll
+          for (int j = 0; j < NI; ++j) z[t][j][kk] = kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
+        }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk) {
+            if (t & 1) ub[j][kk] = fma(z[t][j][kk], ac[t][kk], ub[j][kk]);
+            else ua[j][kk] = fma(z[t][j][kk], ac[t][kk], ua[j][kk]);
+          }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (c0 + t < d) {
+#pragma unroll
+          for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+              const double z = kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
+              const double ac = kok[kk] ? alpha[(lane + 32 * kk) * d + c0 + t] : 0.0;
+              if (t & 1) ub[j][kk] = fma(z, ac, ub[j][kk]);
+              else ua[j][kk] = fma(z, ac, ua[j][kk]);
+            }
         }
       }
     }
-    double u[KPL], r[KPL];
-    if constexpr (HV) {  // Hessian-vector product: s_k = ua + ub, r_k = -P_k (s_k - sum_l P_l s_l)
-      double ps = 0.0;
+  }
+  double u[NI][KPL], r[NI][KPL];
+  if constexpr (HV) {  // Hessian-vector product: s_k = ua + ub, r_k = -P_k (s_k - sum_l P_l s_l)
+    double ps[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      ps[j] = 0.0;
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        u[kk] = kok[kk] ? __ldg(A.Pr + gi * A.ldP + lane + 32 * kk) : 0.0;
-        ps = fma(u[kk], ua[kk] + ub[kk], ps);
+        u[j][kk] = kok[kk] ? __ldg(A.Pr + gi[j] * A.ldP + lane + 32 * kk) : 0.0;
+        ps[j] = fma(u[j][kk], ua[j][kk] + ub[j][kk], ps[j]);
       }
-      ps = warp_sum(ps);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) ps[j] += __shfl_xor_sync(0xffffffffu, ps[j], o);
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
-        r[kk] = kok[kk] ? -u[kk] * ((ua[kk] + ub[kk]) - ps) : 0.0;
-        if (k < KPS) Rs[ii * KPS + k] = r[kk];
+        r[j][kk] = kok[kk] ? -u[j][kk] * ((ua[j][kk] + ub[j][kk]) - ps[j]) : 0.0;
+        if (k < KPS) Rs[(ii0 + j) * KPS + k] = r[j][kk];
       }
-    } else {
-      // shift by the (fp32-rounded) maximum: any shift is exact for the softmax; this one only has
-      // to keep e^{u - m} <= ~1 (R12), so the cross-lane max runs on 32-bit shuffles
-      float mf = -INFINITY;
-      double uy_l = 0.0;
+  } else {
+    // shift by the (fp32-rounded) maximum: any shift is exact for the softmax; this one only has
+    // to keep e^{u - m} <= ~1 (R12), so the cross-lane max runs on 32-bit shuffles
+    float mf[NI];
+    double uy_l[NI], ssum[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      mf[j] = -INFINITY;
+      uy_l[j] = 0.0;
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
-        u[kk] = kok[kk] ? ua[kk] + ub[kk] : -INFINITY;
-        if (k == y) uy_l = u[kk];
-        mf = fmaxf(mf, (float)u[kk]);
+        u[j][kk] = kok[kk] ? ua[j][kk] + ub[j][kk] : -INFINITY;
+        if (k == y[j]) uy_l[j] = u[j][kk];
+        mf[j] = fmaxf(mf[j], (float)u[j][kk]);
       }
+    }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, o));
-      const double m = (double)mf;
-      double ssum = 0.0;
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) mf[j] = fmaxf(mf[j], __shfl_xor_sync(0xffffffffu, mf[j], o));
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const double m = (double)mf[j];
+      ssum[j] = 0.0;
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        const double e = kok[kk] ? exp_shifted(u[kk] - m) : 0.0;
-        ssum += e;
-        u[kk] = e;
+        const double e = kok[kk] ? exp_shifted(u[j][kk] - m) : 0.0;
+        ssum[j] += e;
+        u[j][kk] = e;
       }
-      ssum = warp_sum(ssum);
-      const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) ssum[j] += __shfl_xor_sync(0xffffffffu, ssum[j], o);
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const double uy = __shfl_sync(0xffffffffu, uy_l[j], y[j] & 31);
       // l_i = uy - m - log s: lane lg_cnt keeps (uy - m, s); every 32 individuals each lane takes one log
       if (lane == st.lg_cnt) {
-        st.lg_a = uy - m;
-        st.lg_s = ssum;
+        st.lg_a = uy - (double)mf[j];
+        st.lg_s = ssum[j];
       }
       if (++st.lg_cnt == 32) {
         neu_add(l_s, l_c, st.lg_a - log(st.lg_s));
         st.lg_cnt = 0;
       }
-      const double inv_s = 1.0 / ssum;
+      const double inv_s = 1.0 / ssum[j];
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
-        const double P = u[kk] * inv_s;
-        u[kk] = P;
-        r[kk] = kok[kk] ? ((k == y ? 1.0 : 0.0) - P) : 0.0;
-        if (k < KPS) Rs[ii * KPS + k] = r[kk];
-        if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
+        const double P = u[j][kk] * inv_s;
+        u[j][kk] = P;
+        r[j][kk] = kok[kk] ? ((k == y[j] ? 1.0 : 0.0) - P) : 0.0;
+        if (k < KPS) Rs[(ii0 + j) * KPS + k] = r[j][kk];
+        if (A.writeP && kok[kk]) A.Pr[gi[j] * A.ldP + k] = P;
       }
     }
-    // ---- ybar_e = sum_k P_k y_ke (writeP), gamma partials sum_k y_ke r_k, alpha partials z_kc r_k ----
-    double yb[YZS_F];
+  }
+  // ---- ybar_e = sum_k P_k y_ke (writeP), gamma partials sum_k y_ke r_k, alpha partials z_kc r_k ----
+  // in halves of 8 components: gamma partials, then (writeP) the cross-lane ybar sums through an
+  // [8][33] scratch (the row's own ring slot once its reads are done, when large enough; else red_w)
 #pragma unroll
-    for (int e = 0; e < YZS_F; e += 2) {
-      yb[e] = yb[e + 1] = 0.0;
-      if (e < f) {
-        double g0 = 0.0, g1 = 0.0;
+  for (int e8 = 0; e8 < YZS_F; e8 += 8) {
+    if (e8 < f) {
+      double yb[NI][8];
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) {
-          const double2 v = kok[kk] ? *reinterpret_cast<const double2*>(ys + (lane + 32 * kk) * f + e)
-                                    : make_double2(0.0, 0.0);
-          yb[e] = fma(u[kk], v.x, yb[e]);
-          yb[e + 1] = fma(u[kk], v.y, yb[e + 1]);
-          g0 = fma(v.x, r[kk], g0);
-          g1 = fma(v.y, r[kk], g1);
+      for (int e = e8; e < e8 + 8; e += 4) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j) yb[j][e - e8] = yb[j][e - e8 + 1] = yb[j][e - e8 + 2] = yb[j][e - e8 + 3] = 0.0;
+        if (e < f) {
+          const int nh = (e + 4 <= f) ? 2 : 1;  // pairs in this chunk (f even)
+          double2 v[2][NI][KPL];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+              for (int kk = 0; kk < KPL; ++kk)
+                v[h][j][kk] = (kok[kk] && h < nh)
+                                  ? *reinterpret_cast<const double2*>(ys[j] + (lane + 32 * kk) * f + e + 2 * h)
+                                  : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+              for (int kk = 0; kk < KPL; ++kk) {
+                yb[j][e - e8 + 2 * h] = fma(u[j][kk], v[h][j][kk].x, yb[j][e - e8 + 2 * h]);
+                yb[j][e - e8 + 2 * h + 1] = fma(u[j][kk], v[h][j][kk].y, yb[j][e - e8 + 2 * h + 1]);
+                g0 = fma(v[h][j][kk].x, r[j][kk], g0);
+                g1 = fma(v[h][j][kk].y, r[j][kk], g1);
+              }
+            gam[e + 2 * h] += g0;  // components >= f collect exact zeros (never output)
+            gam[e + 2 * h + 1] += g1;
+          }
         }
-        gam[e] += g0;
-        gam[e + 1] += g1;
       }
-    }
+      if (!HV && A.writeP) {
 #pragma unroll
-    for (int c = 0; c < YZS_D; ++c) {
-      if (c < d) {
-#pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) {
-          const double z = kok[kk] ? zs[(lane + 32 * kk) * d + c] : 0.0;
-          alp[kk][c] = fma(z, r[kk], alp[kk][c]);
-        }
-      }
-    }
-    if (!HV && A.writeP) {
-      // cross-lane ybar sums, 8 components per round through red[8][33]
-#pragma unroll
-      for (int e0 = 0; e0 < YZS_F; e0 += 8) {
-        if (e0 < f) {
-#pragma unroll
-          for (int t = 0; t < 8; ++t) red[t * 33 + lane] = yb[e0 + t];
-          __syncwarp();
-          const int t = lane >> 2, j = lane & 3;
-          double sacc = 0.0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) sacc += red[t * 33 + j * 8 + q];
-          sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-          sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-          if (j == 0 && e0 + t < f) A.Pr[gi * A.ldP + K + e0 + t] = sacc;
-          __syncwarp();
+        for (int j = 0; j < NI; ++j) {
+          const int t = (lane >> 2) & 7;  // the component warp_sum8 leaves in this lane
+          const double sacc = warp_sum8(yb[j], lane);
+          if ((lane & 3) == 0 && e8 + t < f) A.Pr[gi[j] * A.ldP + K + e8 + t] = sacc;
         }
       }
     }
   }
+#pragma unroll
+  for (int c0 = 0; c0 < YZS_D; c0 += 4) {
+    if (c0 < d) {
+      double z[4][NI][KPL];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk)
+            z[t][j][kk] = (kok[kk] && c0 + t < d) ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+          double a = alp[kk][c0 + t];
+#pragma unroll
+          for (int j = 0; j < NI; ++j) a = fma(z[t][j][kk], r[j][kk], a);
+          alp[kk][c0 + t] = a;
+        }
+    }
+  }
+}
+
+// Phase E of one tile for warp w (rows w YZS_R .. + YZS_R - 1): pairs of rows, a single ragged one
+template <int KPL, bool HV>
+__device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, const int* ch_t, double* red_w,
+                                             const double* alpha, const double* gamma,
+                                             double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
+                                             int64_t i0, int nt, int KPS, int w, int lane, const double* ring_w,
+                                             YzsState& st) {
+  const int ib = w * YZS_R;
+  const int n_mine = min(YZS_R, nt - ib);
+  for (int ii = ib + max(n_mine, 0); ii < ib + YZS_R; ++ii)  // ragged tail: zero residual rows
+    for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
+  int jj = 0;
+  if constexpr (YZS_R >= 2)
+    for (; jj + 2 <= n_mine; jj += 2) yzs_rows<KPL, HV, 2>(A, Rs, ch_t, red_w, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+  if (jj < n_mine)
+    yzs_rows<KPL, HV, 1>(A, Rs, ch_t, red_w, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
 }
 
 template <int KPL, int CM_MAX, bool HV, bool YZS>
-__global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
+__global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const EvalArgs A) {
+  constexpr int NWK = YZS ? NWY : NW;           // warps per CTA
   extern __shared__ __align__(16) double sm[];
   constexpr int KP = 32 * KPL, KPS = KP + 4;   // alternatives padded; smem row stride = 4 (mod 16)
   constexpr int NBN = KP / 8;                   // 8-wide alternative blocks
-  const int TI = A.TI;
+  const int TI = YZS ? YZS_TI : A.TI;
   const int K = A.K, q = A.q, d = A.d, f = A.f, p = A.p;
   const int QP = A.QP, XS = A.XS;              // q padded to 4; X tile row stride (= 4 mod 16)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -695,15 +848,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   double* Rs = Xs + 2 * TI * XS;                // [TI][KPS]  residuals
   // [TI][KPS] utilities from phase B (YZS: in place in Rs, each lane overwrites its own u by r)
   double* Ps = YZS ? Rs : Rs + TI * KPS;
-  double* Wa = Rs + ((d + f) && !YZS ? 2 * TI * KPS : TI * KPS);  // [NW][KPL][d][32] alpha-gradient,
-                                                // lane-private, then [NW][f][32] gamma-gradient (e >= 8)
-  double* Cf = Wa + (YZS ? 0 : NW * KPL * d * 32 + NW * f * 32);  // [K*d + f]  alpha, gamma
+  double* Wa = Rs + ((d + f) && !YZS ? 2 * TI * KPS : TI * KPS);  // [NWK][KPL][d][32] alpha-gradient,
+                                                // lane-private, then [NWK][f][32] gamma-gradient (e >= 8)
+  double* Cf = Wa + (YZS ? 0 : NWK * KPL * d * 32 + NWK * f * 32);  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
-  double* Red = Cf + K * d + f + 1 + TI;                  // [NW][8][33] ybar reductions
-  // YZS: per-warp mbarriers [NW][NS] and rings [NW][NS][SLOT] (16-byte aligned)
-  const int red_end = (int)(Red - sm) + ((d + f) ? NW * 8 * 33 : 0);
+  double* Red = Cf + K * d + f + 1 + TI;                  // [NWK][8][33] ybar reductions
+  // YZS: per-warp mbarriers [NWK][NS] and rings [NWK][NS][SLOT] (16-byte aligned); the ybar scratch
+  // is the row's own slot when it holds 8 x 33 doubles
+  const int red_end = (int)(Red - sm) + ((d + f) && !YZS ? NWK * 8 * 33 : 0);
   uint64_t* Bar = reinterpret_cast<uint64_t*>(sm + ((red_end + 1) & ~1));
-  double* Ring = sm + ((red_end + 1) & ~1) + NW * A.NS;
+  double* Ring = sm + ((red_end + 1) & ~1) + NWK * A.NS;
 
   for (int idx = tid; idx < QP * KPS; idx += blockDim.x) {
     const int a = idx / KPS, k = idx - a * KPS;
@@ -711,27 +865,23 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   }
   for (int idx = tid; idx < 2 * TI * XS; idx += blockDim.x) Xs[idx] = ((idx % XS) == 0) ? 1.0 : 0.0;
   if (!YZS)
-    for (int idx = tid; idx < NW * KPL * d * 32 + NW * f * 32; idx += blockDim.x) Wa[idx] = 0.0;
+    for (int idx = tid; idx < NWK * KPL * d * 32 + NWK * f * 32; idx += blockDim.x) Wa[idx] = 0.0;
   for (int idx = tid; idx < K * d + f; idx += blockDim.x) Cf[idx] = A.coef[A.off_alpha + idx];
   const double* alpha = Cf;
   const double* gamma = Cf + K * d;
   // YZS: this lane's alpha_k coefficients and alpha / gamma gradient partials live in registers
-  double acoef[YZS ? KPL : 1][YZS_D], alp[YZS ? KPL : 1][YZS_D], gamz[YZS_F];
+  double alp[YZS ? KPL : 1][YZS_D], gamz[YZS_F];
   YzsState yst;
   if constexpr (YZS) {
     yst.ring_s = static_cast<unsigned>(__cvta_generic_to_shared(Ring + (size_t)w * A.NS * A.SLOT));
     yst.bar_s = static_cast<unsigned>(__cvta_generic_to_shared(Bar + w * A.NS));
-    yst.slot = yst.par = yst.s_issue = yst.slot_i = yst.lg_cnt = 0;
+    yst.slot = yst.par = yst.s_cur = yst.s_issue = yst.slot_i = yst.lg_cnt = 0;
     yst.lg_a = 0.0;
     yst.lg_s = 1.0;
 #pragma unroll
     for (int kk = 0; kk < KPL; ++kk)
 #pragma unroll
-      for (int c = 0; c < YZS_D; ++c) {
-        const int k = lane + 32 * kk;
-        acoef[kk][c] = (k < K && c < d) ? A.coef[A.off_alpha + k * d + c] : 0.0;
-        alp[kk][c] = 0.0;
-      }
+      for (int c = 0; c < YZS_D; ++c) alp[kk][c] = 0.0;
 #pragma unroll
     for (int e = 0; e < YZS_F; ++e) gamz[e] = 0.0;
     if (lane == 0) {
@@ -740,13 +890,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     }
     __syncwarp();
     if (lane == 0)  // only lane 0 tracks the issue pointer
-      for (int j = 0; j < A.NS - 1; ++j) yzs_issue<tile_rows(KPL, true) / NW>(A, yst, w);
+      while (yst.s_issue < A.NS && yzs_issue(A, yst, w)) {
+      }
   }
 
   // phase-C warp grid over (m-blocks of a, n-blocks of k)
   const int MB = QP / 8 + ((QP & 7) ? 1 : 0);
   constexpr int WN = NBN < 8 ? NBN : 8;
-  constexpr int WM = 8 / WN;
+  constexpr int WM = NWK / WN;
   const int cwm = w / WN, cwn = w % WN;
   constexpr int CN = NBN / WN;                 // n-blocks per warp (CM_MAX m-blocks per warp)
   double G[CM_MAX][CN][2];
@@ -761,17 +912,25 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
 
   double l_s = 0.0, l_c = 0.0;  // Neumaier loglik of this lane's rows (lanes with r4 == 0)
   const int64_t ntiles = (A.N + TI - 1) / TI;
+  const unsigned xs_s = static_cast<unsigned>(__cvta_generic_to_shared(Xs));
+  const int x_i0 = p ? tid / p : 0, x_a0 = p ? tid - x_i0 * p : 0;                    // tid = x_i0 p + x_a0
+  const int x_di = p ? (int)blockDim.x / p : 0, x_da = p ? (int)blockDim.x - x_di * p : 0;  // blockDim likewise
   auto prefetch = [&](int64_t tile, int buf) {
     const int64_t i0 = tile * TI;
     const int nt = (int)(A.N - i0 < TI ? A.N - i0 : TI);
-    double* dst = Xs + buf * TI * XS;
+    const unsigned dst = xs_s + 8u * (unsigned)(buf * TI * XS);
     const double* src = A.X + i0 * p;
+    int i = x_i0, a = x_a0;  // element e = tid + j blockDim = i p + a, advanced without divisions
     for (int e = tid; e < nt * p; e += blockDim.x) {
-      const int i = e / p, a = e - i * p;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                       static_cast<unsigned>(__cvta_generic_to_shared(dst + i * XS + a + 1))),
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * (unsigned)(i * XS + a + 1)),
                    "l"(src + e)
                    : "memory");
+      i += x_di;
+      a += x_da;
+      if (a >= p) {
+        a -= p;
+        ++i;
+      }
     }
     for (int i = tid; i < nt; i += blockDim.x)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
@@ -807,16 +966,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     const int* ch_t = chs + buf * TI;
 
     // ---------------- phase B: u = X~ B on DMMA, then softmax / loglik / residuals ----------------
-    const int il = (8 * w + c8) % TI;  // this lane's individual (row of the C fragment)
-    const bool in_b = 8 * w < TI;      // warps beyond the tile skip phase B
+    // YZS (16-row tiles): the warps split 2 row blocks x NG groups of alternative blocks (groups
+    // beyond NBN idle)
+    constexpr int NG = NWK / 2;
+    constexpr int NBW = YZS ? (NBN >= NG ? NBN / NG : 1) : NBN;  // alternative blocks per warp
+    const int il = YZS ? 8 * (w & 1) + c8 : (8 * w + c8) % TI;  // this lane's individual (C-fragment row)
+    const int nb0 = YZS ? (w >> 1) * NBW : 0;
+    const bool in_b = YZS ? nb0 < NBN : 8 * w < TI;  // warps without a block skip phase B
     double u[NBN][2];
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb) u[nb][0] = u[nb][1] = 0.0;
-    for (int a0 = 0; a0 < QP; a0 += 4) {
+    for (int a0 = 0; a0 < (in_b ? QP : 0); a0 += 4) {
       const double av = X_t[il * XS + a0 + r4];
 #pragma unroll
-      for (int nb = 0; nb < NBN; ++nb) {
-        const double bv = Bs[(a0 + r4) * KPS + nb * 8 + c8];
+      for (int nb = 0; nb < NBW; ++nb) {
+        const double bv = Bs[(a0 + r4) * KPS + (nb0 + nb) * 8 + c8];
         asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
             : "+d"(u[nb][0]), "+d"(u[nb][1])
             : "d"(av), "d"(bv));
@@ -824,17 +988,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     }
     const bool valid = in_b && il < nt;
     const int64_t i = i0 + il;
-    if (d + f) {
+    if (YZS || (d + f)) {
       // ---- alternative-varying data present: stash u, then phase E (lanes over alternatives) ----
       if (in_b) {
 #pragma unroll
-        for (int nb = 0; nb < NBN; ++nb)
-          *reinterpret_cast<double2*>(Ps + il * KPS + nb * 8 + 2 * r4) = make_double2(u[nb][0], u[nb][1]);
+        for (int nb = 0; nb < NBW; ++nb)
+          *reinterpret_cast<double2*>(Ps + il * KPS + (nb0 + nb) * 8 + 2 * r4) = make_double2(u[nb][0], u[nb][1]);
       }
       __syncthreads();
       bool done = false;
       if constexpr (YZS) {
-        phase_e_smem<KPL, HV>(A, Rs, ch_t, Red + w * (8 * 33), acoef, gamma, gamz, alp, l_s, l_c, i0, nt, KPS, w,
+        phase_e_smem<KPL, HV>(A, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, gamz, alp, l_s, l_c, i0, nt, KPS, w,
                               lane, Ring + (size_t)w * A.NS * A.SLOT, yst);
         done = true;
       } else if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
@@ -843,8 +1007,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
           done = true;
         }
       }
-      if (!done)
-        phase_e<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
+      if constexpr (!YZS)
+        if (!done) phase_e<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
     } else {
     if constexpr (HV) {
       // Hessian-vector product: u holds s_ik = (J_i v)_k; with P_i from the last evaluation
@@ -955,14 +1119,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     if (lane < yst.lg_cnt) neu_add(l_s, l_c, yst.lg_a - log(yst.lg_s));  // the deferred logs left over
   __syncthreads();
   double* out = A.part + (size_t)blockIdx.x * A.n_part;
-  double* scratch = Rs;  // reuse
+  double* scratch = YZS ? Ring : Rs;  // reuse (YZS: the drained rings; Rs may be smaller than 2 NWK 32)
   // loglik: lanes with r4 == 0 hold rows; combine in (warp, lane) order
   scratch[2 * tid] = l_s;
   scratch[2 * tid + 1] = l_c;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0, c = 0.0;
-    for (int t = 0; t < NW * 32; t += (YZS ? 1 : 4)) { neu_add(s, c, scratch[2 * t]); neu_add(s, c, scratch[2 * t + 1]); }
+    for (int t = 0; t < NWK * 32; t += (YZS ? 1 : 4)) { neu_add(s, c, scratch[2 * t]); neu_add(s, c, scratch[2 * t + 1]); }
     out[0] = s;
     out[1] = c;
   }
@@ -983,10 +1147,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     }
   }
   if constexpr (YZS) {
-    // alpha / gamma register partials -> the (drained) rings as [NW][KPL][d][32] + [NW][f][32],
+    // alpha / gamma register partials -> the (drained) rings as [NWK][KPL][d][32] + [NWK][f][32],
     // then fixed-order sums over warps and lanes
+    __syncthreads();  // the loglik partials in the rings have been summed
     double* sa = Ring;
-    double* sg = Ring + NW * KPL * d * 32;
+    double* sg = Ring + NWK * KPL * d * 32;
 #pragma unroll
     for (int kk = 0; kk < KPL; ++kk)
 #pragma unroll
@@ -999,12 +1164,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
     for (int idx = tid; idx < K * d; idx += blockDim.x) {
       const int k = idx / d, c = idx - k * d, kk = k >> 5, ln = k & 31;
       double v = 0.0;
-      for (int ww = 0; ww < NW; ++ww) v += sa[((ww * KPL + kk) * d + c) * 32 + ln];
+      for (int ww = 0; ww < NWK; ++ww) v += sa[((ww * KPL + kk) * d + c) * 32 + ln];
       out[2 + A.off_alpha + idx] = v;
     }
     for (int e = tid; e < f; e += blockDim.x) {
       double v = 0.0;
-      for (int ww = 0; ww < NW; ++ww)
+      for (int ww = 0; ww < NWK; ++ww)
         for (int ln = 0; ln < 32; ++ln) v += sg[(ww * f + e) * 32 + ln];
       out[2 + A.off_gamma + e] = v;
     }
@@ -1013,25 +1178,25 @@ __global__ void __launch_bounds__(NW * 32, 1) k_eval_kernel(const EvalArgs A) {
   // register partials of gamma components 8..15 into Wa (each (warp, lane) slot is private)
 #pragma unroll
   for (int e = 8; e < gam_regs<KPL>(); ++e)
-    if (e < f) Wa[NW * KPL * d * 32 + (w * f + e) * 32 + lane] += gam[e];
+    if (e < f) Wa[NWK * KPL * d * 32 + (w * f + e) * 32 + lane] += gam[e];
   __syncthreads();
   // gamma partials: registers (e < 8) -> smem, then fixed-order sums
-  double* gsc = Rs;  // [NW*32][8]
+  double* gsc = Rs;  // [NWK*32][8]
   for (int e = 0; e < 8; ++e) gsc[tid * 8 + e] = gam[e];
   __syncthreads();
   for (int idx = tid; idx < K * d; idx += blockDim.x) {
     const int k = idx / d, c = idx - k * d, kk = k >> 5, ln = k & 31;
     double v = 0.0;
-    for (int ww = 0; ww < NW; ++ww) v += Wa[((ww * KPL + kk) * d + c) * 32 + ln];
+    for (int ww = 0; ww < NWK; ++ww) v += Wa[((ww * KPL + kk) * d + c) * 32 + ln];
     out[2 + A.off_alpha + idx] = v;
   }
   for (int e = tid; e < f; e += blockDim.x) {
     double v = 0.0;
     if (e < 8) {
-      for (int t = 0; t < NW * 32; ++t) v += gsc[t * 8 + e];
+      for (int t = 0; t < NWK * 32; ++t) v += gsc[t * 8 + e];
     } else {
-      for (int ww = 0; ww < NW; ++ww)
-        for (int ln = 0; ln < 32; ++ln) v += Wa[NW * KPL * d * 32 + (ww * f + e) * 32 + ln];
+      for (int ww = 0; ww < NWK; ++ww)
+        for (int ln = 0; ln < 32; ++ln) v += Wa[NWK * KPL * d * 32 + (ww * f + e) * 32 + ln];
     }
     out[2 + A.off_gamma + e] = v;
   }
@@ -1047,8 +1212,17 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
   const int tid = threadIdx.x;
   const int r = blockIdx.x * 256 + tid;
   if (want_grad && r < n_p) {
+    // fixed block order; the loads of 8 blocks are issued together (the partials sit in L2)
     double s = 0.0, c = 0.0;
-    for (int b = 0; b < nblk; ++b) neu_add(s, c, part[(size_t)b * n_part + 2 + r]);
+    int b = 0;
+    for (; b + 8 <= nblk; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = __ldcg(part + (size_t)(b + t) * n_part + 2 + r);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) neu_add(s, c, v[t]);
+    }
+    for (; b < nblk; ++b) neu_add(s, c, __ldcg(part + (size_t)b * n_part + 2 + r));
     grad[r] = s + c;
   }
   __threadfence();
@@ -1071,9 +1245,20 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
   }
   if (tid == 0) {
     double s = 0.0, c = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-      neu_add(s, c, part[(size_t)b * n_part]);
-      neu_add(s, c, part[(size_t)b * n_part + 1]);
+    int b = 0;
+    for (; b + 4 <= nblk; b += 4) {
+      double v[8];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        v[2 * t] = __ldcg(part + (size_t)(b + t) * n_part);
+        v[2 * t + 1] = __ldcg(part + (size_t)(b + t) * n_part + 1);
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) neu_add(s, c, v[t]);
+    }
+    for (; b < nblk; ++b) {
+      neu_add(s, c, __ldcg(part + (size_t)b * n_part));
+      neu_add(s, c, __ldcg(part + (size_t)b * n_part + 1));
     }
     const double l = s + c;
     scal[0] = l;
@@ -1180,17 +1365,20 @@ static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
 static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns) {
-  const int KP = 32 * kpl, KPS = KP + 4, TI = tile_rows(kpl, (D.d + D.f) > 0);
+  const int KP = 32 * kpl, KPS = KP + 4, TI = yzs ? YZS_TI : tile_rows(kpl, (D.d + D.f) > 0);
+  const int slot = D.K * (D.f + D.d);
+  const int nw = yzs ? NWY : NW;
   size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
              ((D.d + D.f) && !yzs ? (size_t)TI * KPS : 0) +
-             (yzs ? 0 : (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32) +
+             (yzs ? 0 : (size_t)nw * kpl * D.d * 32 + (size_t)nw * D.f * 32) +
              (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
-             ((D.d + D.f) ? (size_t)NW * 8 * 33 : 0);
+             ((D.d + D.f) && !yzs ? (size_t)nw * 8 * 33 : 0);
   if (yzs) {
     n = (n + 1) & ~(size_t)1;
-    const size_t ring = (size_t)NW * ns * D.K * (D.f + D.d);
-    const size_t scr = (size_t)NW * kpl * D.d * 32 + (size_t)NW * D.f * 32;  // finalisation scratch
-    n += (size_t)NW * ns + (ring > scr ? ring : scr);
+    const size_t ring = (size_t)nw * ns * slot;
+    size_t scr = (size_t)nw * kpl * D.d * 32 + (size_t)nw * D.f * 32;  // finalisation scratch
+    if (scr < (size_t)2 * nw * 32) scr = (size_t)2 * nw * 32;          // (and the loglik partials)
+    n += (size_t)nw * ns + (ring > scr ? ring : scr);
   }
   return n * sizeof(double);
 }
@@ -1199,13 +1387,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   int kpl = 1;
   while (32 * kpl < D.K) kpl *= 2;
   if (kpl > 8) return false;
-  // register budget: phase-C accumulators (cm x cn blocks) + the phase-B row (nbn blocks)
-  const int nbn = 4 * kpl, wn = nbn < 8 ? nbn : 8, wm = 8 / wn, cn = nbn / wn;
-  const int mb = (eval_qp(D) + 7) / 8;
-  int cm = 2;
-  while (cm < (mb + wm - 1) / wm) cm *= 2;
-  if (cm > 8 || 2 * cm * cn + 2 * nbn > 96) return false;
-  plan->cm = cm;
+
   // YZS (alternative-varying rows staged per warp with bulk copies): f even <= 16, d <= 8, whole
   // 16-byte rows (K f, K d even), K <= 64; 3 ring slots if they fit, else 2
   plan->yzs = 0;
@@ -1214,7 +1396,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
                       (D.K * D.f) % 2 == 0 && (D.K * D.d) % 2 == 0 && !getenv("MNL_NO_YZS");
   size_t smem = eval_smem(D, kpl, false, 0);
   if (yzs_ok) {
-    for (int ns = 3; ns >= 2; --ns) {
+    for (int ns = 4; ns >= 2; --ns) {  // 4: two rows computed while the next two land
       const size_t sz = eval_smem(D, kpl, true, ns);
       if (sz <= 227 * 1024) {
         plan->yzs = 1;
@@ -1225,10 +1407,18 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
     }
   }
   if (smem > 227 * 1024) return false;  // sm_100a opt-in maximum (232448 bytes)
+  // register budget: phase-C accumulators (cm x cn blocks) + the phase-B row (nbn blocks)
+  const int nwarps = plan->yzs ? NWY : NW;
+  const int nbn = 4 * kpl, wn = nbn < 8 ? nbn : 8, wm = nwarps / wn, cn = nbn / wn;
+  const int mb = (eval_qp(D) + 7) / 8;
+  int cm = 2;
+  while (cm < (mb + wm - 1) / wm) cm *= 2;
+  if (cm > 8 || 2 * cm * cn + 2 * nbn > 96) return false;
+  plan->cm = cm;
   plan->kpl = kpl;
   plan->smem = smem;
-  plan->block = NW * 32;
-  const int ti = tile_rows(kpl, (D.d + D.f) > 0);
+  plan->block = nwarps * 32;
+  const int ti = plan->yzs ? YZS_TI : tile_rows(kpl, (D.d + D.f) > 0);
   const int64_t ntiles = (D.N + ti - 1) / ti;
   int64_t grid = sms;
   if (grid > ntiles) grid = ntiles;
@@ -1244,7 +1434,7 @@ static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const d
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = eval_qp(D); a.XS = eval_xs(D);
-  a.TI = tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = 0;
+  a.TI = plan.yzs ? YZS_TI : tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = 0;
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
   a.Pr = (writeP || hv) ? pk->Pr : nullptr;
   a.ldP = (writeP || hv) ? pk->ldP : 0;
