@@ -163,6 +163,25 @@ int mnl_hessvec(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
                 const double* X, const double* Y, const double* Z, const int32_t* choice,
                 const double* coef, const double* v, double* hv, void* stream);
 
+/* Standard errors at `coef` (the paper's summary statistics):
+ *   se_j = sqrt( [(-H)^{-1}]_jj ),  H the Hessian of P:462-476 at coef
+ * (the inverse observed information; at the MLE the usual asymptotic standard errors).
+ *   se  dev [n_p] out
+ * Forms H, factors -H = L L^T (as the Newton step does) and sums the squares of the columns of
+ * L^{-1} (blocked triangular inverse on DMMA, one CTA per 64-column block).
+ * Errors: as mnl_eval, plus MNL_ERR_NOT_SPD when -H is not positive definite (singular design). */
+int mnl_std_errors(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                   const double* X, const double* Y, const double* Z, const int32_t* choice,
+                   const double* coef, double* se, void* stream);
+
+/* Choice probabilities at `coef` (Eqs. "probability" / "base probability"):
+ *   P  dev [N][K] out, row-major, 16-byte aligned; P[i][k] = e^{U_ik} / sum_l e^{U_il}
+ * Same X, Y, Z conventions as mnl_eval; no choices are needed. Errors: MNL_ERR_ARG, MNL_ERR_CUDA,
+ * MNL_ERR_NONFINITE. */
+int mnl_predict(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                const double* X, const double* Y, const double* Z, const double* coef, double* P,
+                void* stream);
+
 /* Host-buffer variants: every pointer is HOST memory (pinned or pageable). The call copies the
  * inputs to the device, runs the same path and copies the outputs back, all inside the call. */
 int mnl_eval_host(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,

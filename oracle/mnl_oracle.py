@@ -42,7 +42,8 @@ is a library routine (numpy.linalg.cholesky / LAPACK).
 Pins (tests/test_oracle_pins.py): closed forms at theta=0 (P:874 printed value),
 K=2 textbook logistic regression, central finite differences, the
 textbook dense X~^T W~ X~ of P:383-403, the paper's block formula
-written independently, intercept-only closed-form MLE, invariants.
+written independently, intercept-only closed-form MLE, invariants; standard
+errors against the intercept-only closed-form variance (1/N)(1/p_k + 1/p_0).
 """
 from __future__ import annotations
 
@@ -271,6 +272,18 @@ def hessvec(D: Data, theta, v, P: np.ndarray | None = None) -> np.ndarray:
     for r, (ks, vals) in enumerate(cols):
         out[r] = -np.sum(vals * W[:, ks])
     return out
+
+
+def std_errors(D: Data, theta) -> np.ndarray:
+    """se_j = sqrt([(-H)^{-1}]_jj) at theta: the square roots of the diagonal of the inverse observed
+    information (the paper's estimation summary). numpy.linalg.inv is the library step."""
+    H = hessian(D, theta)
+    return np.sqrt(np.diag(np.linalg.inv(-H)))
+
+
+def predict(D: Data, theta) -> np.ndarray:
+    """P[N, K]: the choice probabilities of Eqs. "probability" / "base probability"."""
+    return probabilities(utilities(D, np.asarray(theta, dtype=np.float64)))
 
 
 def mnl_eval(D: Data, theta, want_grad=True, want_hess=True):

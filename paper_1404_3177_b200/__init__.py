@@ -22,7 +22,8 @@ MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_
 
 EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex", "mnl_eval_host",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
-            "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec")
+            "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec",
+            "mnl_std_errors", "mnl_predict")
 
 MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
 MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
@@ -85,6 +86,10 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_opts.restype = ctypes.c_int
     lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_hessvec.restype = ctypes.c_int
+    lib.mnl_std_errors.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V]
+    lib.mnl_std_errors.restype = ctypes.c_int
+    lib.mnl_predict.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V]
+    lib.mnl_predict.restype = ctypes.c_int
     lib.mnl_eval_host.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_eval_host.restype = ctypes.c_int
     lib.mnl_newton_fit_host.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, D, I32, V,
@@ -244,6 +249,30 @@ def mnl_hessvec(prob: Problem, coef, v, stream=None):
     if rc != MNL_OK:
         raise MnlError(rc, "mnl_hessvec")
     return hv
+
+
+def mnl_std_errors(prob: Problem, coef, stream=None):
+    """sqrt(diag((-H)^{-1})) at coef (CUDA float64 [n_p]); the asymptotic standard errors at the MLE."""
+    torch = _torch()
+    se = torch.empty(prob.n_p, dtype=torch.float64, device=prob.choice.device)
+    X, Y, Z, ch = prob.ptrs()
+    rc = load().mnl_std_errors(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, ch, coef.data_ptr(), se.data_ptr(),
+                               _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_std_errors")
+    return se
+
+
+def mnl_predict(prob: Problem, coef, stream=None):
+    """Choice probabilities P[N, K] at coef (CUDA float64 [n_p])."""
+    torch = _torch()
+    P = torch.empty(prob.N, prob.K, dtype=torch.float64, device=prob.choice.device)
+    X, Y, Z, _ = prob.ptrs()
+    rc = load().mnl_predict(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, coef.data_ptr(), P.data_ptr(),
+                            _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_predict")
+    return P
 
 
 def mnl_cholesky(A, stream=None):

@@ -100,6 +100,9 @@ cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t s
 // panels, backward solve as one wavefront kernel). x may alias b.
 cudaError_t launch_cholesky_solve_fused(int n, double* A, int lda, int* info, const double* b, double* x,
                                         cudaStream_t st);
+// se_j = sqrt([(L L^T)^{-1}]_jj) for the factor L in the lower triangle of L (lda); the strict upper
+// triangle of L is overwritten (workspace for the blocks of L^{-1}).
+cudaError_t launch_inv_diag_sqrt(int n, double* L, int lda, double* se, cudaStream_t st);
 // x = (L L^T)^{-1} b ; x may alias b.
 cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, double* x,
                               cudaStream_t st);

@@ -698,6 +698,130 @@ cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t
   return cudaGetLastError();
 }
 
+// ---- diag((L L^T)^{-1}) for standard errors ---------------------
+// CTA J owns block column J of W = L^{-1}: W_JJ = Linv[J]; for I = J+1 .. : W_IJ = -Linv[I]
+// sum_{K=J}^{I-1} L_IK W_KJ (DMMA 64x64 tiles). The finished blocks W_KJ are kept, transposed, in
+// the (unused) strict upper triangle of A at block (J, K); columns of A^{-1} = W^T W have
+// diag_c = sum_r W_rc^2, summed in a fixed order (rows of a tile by shuffles, warps via smem, I
+// ascending). Block columns are independent; the first one carries the longest chain.
+__device__ __forceinline__ void tile_acc_xyT(const double (*Xs)[LDS], const double (*Ys)[LDS], double acc[2][4][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wr = (w >> 1) * 16, wc = (w & 1) * 32;
+  const int lr = lane >> 2, lk = lane & 3;
+#pragma unroll 4
+  for (int k0 = 0; k0 < NB; k0 += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) af[a] = Xs[wr + a * 8 + lr][k0 + lk];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bf[b] = Ys[wc + b * 8 + lr][k0 + lk];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_inv_diag(int n, double* A, int lda, const double* Linv, double* se) {
+  extern __shared__ __align__(16) double dsm[];
+  double(*Xs)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
+  double(*Ys)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + NB * LDS);
+  __shared__ double colw[4][NB];
+  const int nblk = (n + NB - 1) / NB;
+  const int J = blockIdx.x, j0 = J * NB, jb = min(NB, n - j0);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
+  double csum[4][2];  // this thread's 8 columns: sum of squares over rows (its lr == 0 lanes after shuffles)
+#pragma unroll
+  for (int b = 0; b < 4; ++b) csum[b][0] = csum[b][1] = 0.0;
+  auto add_squares = [&](const double (&v)[2][4][2]) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double t = v[0][b][h] * v[0][b][h] + v[1][b][h] * v[1][b][h];
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 16);
+        csum[b][h] += t;
+      }
+  };
+  // W_JJ = Linv[J] (zero beyond jb)
+  {
+    double v[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          v[a][b][h] = (wr + a * 8 + lr < jb && wc + b * 8 + 2 * lk + h < jb)
+                           ? __ldg(Linv + (size_t)J * NB * NB + (wr + a * 8 + lr) * NB + wc + b * 8 + 2 * lk + h)
+                           : 0.0;
+    add_squares(v);
+  }
+  for (int I = J + 1; I < nblk; ++I) {
+    const int i0 = I * NB, ib = min(NB, n - i0);
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int Kb = J; Kb < I; ++Kb) {
+      const int k0 = Kb * NB, kb = min(NB, n - k0);
+      __syncthreads();
+      load_tile(Xs, A, lda, i0, k0, ib, kb);  // L_IK
+      if (Kb == J) {                          // W_JJ^T from Linv[J]
+        for (int e = tid; e < NB * NB; e += 256) {
+          const int r = e >> 6, c = e & 63;
+          Ys[c][r] = (r < jb && c < jb) ? __ldg(Linv + (size_t)J * NB * NB + e) : 0.0;
+        }
+      } else {
+        load_tile(Ys, A, lda, j0, k0, jb, kb);  // W_KJ^T, stored transposed at block (J, K)
+      }
+      __syncthreads();
+      tile_acc_xyT(Xs, Ys, acc);
+    }
+    // W_IJ = -Linv[I] T, T = acc: Xs = Linv[I], Ys = T^T
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) Ys[wc + b * 8 + 2 * lk + h][wr + a * 8 + lr] = acc[a][b][h];
+    for (int e = tid; e < NB * NB; e += 256)
+      Xs[e >> 6][e & 63] = ((e >> 6) < ib && (e & 63) < ib) ? __ldg(Linv + (size_t)I * NB * NB + e) : 0.0;
+    __syncthreads();
+    double wv[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) wv[a][b][0] = wv[a][b][1] = 0.0;
+    tile_acc_xyT(Xs, Ys, wv);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wr + a * 8 + lr, c = wc + b * 8 + 2 * lk + h;
+          wv[a][b][h] = (r < ib && c < jb) ? -wv[a][b][h] : 0.0;
+          if (r < ib && c < jb) A[(int64_t)(j0 + c) * lda + i0 + r] = wv[a][b][h];  // W_IJ^T at block (J, I)
+        }
+    add_squares(wv);
+  }
+  // combine the four row-warps of each column in a fixed order
+  if (lr == 0) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) colw[w >> 1][wc + b * 8 + 2 * lk + h] = csum[b][h];
+  }
+  __syncthreads();
+  if (tid < jb) se[j0 + tid] = sqrt(((colw[0][tid] + colw[1][tid]) + colw[2][tid]) + colw[3][tid]);
+}
+
 }  // namespace
 
 cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t st) {
@@ -710,6 +834,25 @@ cudaError_t launch_cholesky_solve_fused(int n, double* A, int lda, int* info, co
   cudaError_t e = factor(n, A, lda, info, x, st);
   if (e != cudaSuccess) return e;
   return launch_wave(n, A, lda, x, 1, st);
+}
+
+cudaError_t launch_inv_diag_sqrt(int n, double* L, int lda, double* se, cudaStream_t st) {
+  set_attrs();
+  if (!ensure_work(n)) return cudaErrorMemoryAllocation;
+  if (g_cw.factor != L || g_cw.factor_n != n) {  // factor from elsewhere: build its Linv blocks
+    k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, g_cw.Linv);
+    count_launch();
+    g_cw.factor = L;
+    g_cw.factor_n = n;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
+    attr = true;
+  }
+  k_inv_diag<<<(n + NB - 1) / NB, 256, kDyn, st>>>(n, L, lda, g_cw.Linv, se);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, double* x, cudaStream_t st) {

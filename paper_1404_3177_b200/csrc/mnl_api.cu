@@ -59,6 +59,8 @@ struct Workspace {
   // host-mode device copies
   double *hX = nullptr, *hY = nullptr, *hZ = nullptr, *hcoef = nullptr, *hout = nullptr, *hH = nullptr;
   int32_t* hch = nullptr;
+  int32_t* zch = nullptr;  // all-zero choices for mnl_predict
+  size_t czch = 0;
   size_t chX = 0, chY = 0, chZ = 0, chcoef = 0, chout = 0, chH = 0, chch = 0;
   cudaStream_t hstream = nullptr;
 };
@@ -446,6 +448,66 @@ int mnl_hessvec(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const dou
   return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
 }
 
+int mnl_std_errors(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
+                   const double* Z, const int32_t* choice, const double* coef, double* se, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_launches = 0;
+  Dims D;
+  if (!dims_of(N, K, p, f, d, &D) || !check_inputs(D, X, Y, Z, choice) || !coef || !se) return MNL_ERR_ARG;
+  Workspace& W = g_ws;
+  int rc = init_device(W);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  EvalPlan ep;
+  if (!eval_plan(D, &ep, W.sms)) return MNL_ERR_ARG;
+  Packed pk{};
+  if (!ensure_packed(W, D, &pk)) return MNL_ERR_CUDA;
+  if (launch_pack(D, pk, X, Z, st) != cudaSuccess) return MNL_ERR_CUDA;
+  if (W.hp) hess_plan_design_changed(W.hp);
+  double scal[3];
+  rc = run_eval(W, D, ep, X, Y, Z, choice, coef, &pk, true, nullptr, nullptr, scal, st);  // P_i at coef
+  if (rc) return rc;
+  if (!std::isfinite(scal[0])) return MNL_ERR_NONFINITE;
+  HessPlan* hp = get_hess_plan(W, D, pk);
+  const int n = D.n_p;
+  if (!hp || !grow(&W.A, &W.cA, (size_t)n * n)) return MNL_ERR_CUDA;
+  if (launch_hessian(hp, D, pk, Y, W.A, n, -1.0, st) != cudaSuccess) return MNL_ERR_CUDA;  // A = -H
+  if (launch_cholesky(n, W.A, n, W.info, st) != cudaSuccess) return MNL_ERR_CUDA;
+  int info = 0;
+  cudaMemcpyAsync(&info, W.info, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return MNL_ERR_CUDA;
+  if (info) return MNL_ERR_NOT_SPD;
+  if (launch_inv_diag_sqrt(n, W.A, n, se, st) != cudaSuccess) return MNL_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
+}
+
+int mnl_predict(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
+                const double* Z, const double* coef, double* P, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_launches = 0;
+  Dims D;
+  if (!dims_of(N, K, p, f, d, &D) || !coef || !P || !aligned16(P)) return MNL_ERR_ARG;
+  Workspace& W = g_ws;
+  int rc = init_device(W);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!grow(&W.zch, &W.czch, (size_t)N)) return MNL_ERR_CUDA;  // pass 1 reads a choice per row
+  cudaMemsetAsync(W.zch, 0, (size_t)N * sizeof(int32_t), st);
+  if (!check_inputs(D, X, Y, Z, W.zch)) return MNL_ERR_ARG;
+  EvalPlan ep;
+  if (!eval_plan(D, &ep, W.sms)) return MNL_ERR_ARG;
+  Packed pk{};
+  if (!ensure_packed(W, D, &pk)) return MNL_ERR_CUDA;
+  double scal[3];
+  rc = run_eval(W, D, ep, X, Y, Z, W.zch, coef, &pk, true, nullptr, nullptr, scal, st);
+  if (rc) return rc;
+  if (!std::isfinite(scal[0])) return MNL_ERR_NONFINITE;
+  if (cudaMemcpy2DAsync(P, (size_t)K * sizeof(double), pk.Pr, (size_t)pk.ldP * sizeof(double),
+                        (size_t)K * sizeof(double), (size_t)N, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return MNL_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
+}
+
 int mnl_newton_fit(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
                    const double* Z, const int32_t* choice, const double* coef0, double tol, int32_t max_iter,
                    double* coef, int32_t* iters, double* loglik, void* stream) {
@@ -551,6 +613,7 @@ void mnl_release(void) {
   cudaFree(W.info);
   cudaFree(W.counter);
   cudaFree(W.hch);
+  cudaFree(W.zch);
   if (W.hstream) cudaStreamDestroy(W.hstream);
   W = Workspace();
 }

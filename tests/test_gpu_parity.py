@@ -401,3 +401,42 @@ def test_cg_fit_reaches_golden_mle(cfg):
     ref = np.array(g["coef"])
     assert np.linalg.norm(coef - ref) <= 1e-8 * np.linalg.norm(ref)
     assert abs(r.loglik - g["loglik"]) <= 1e-10 * abs(g["loglik"])
+
+
+# --- standard errors and prediction ------------------------------------
+# se_j = sqrt([(-H)^{-1}]_jj): the inversion amplifies H's relative rounding (<= 1e-9 by the
+# Hessian tolerance) by at most the condition number of -H on these well-conditioned problems;
+# the bound used is 1e-8 relative per entry.
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c3", (300, 7, 4, 2, 3), (2000, 12, 9, 0, 2)],
+                         ids=["c1", "c2", "c3", "ragged-mixed", "ragged-Z"])
+def test_std_errors_parity(case):
+    prob = datagen.make(case) if isinstance(case, str) else datagen.custom(*case, seed=23, coef_sd=0.4,
+                                                                         require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    th = prob.theta_true
+    se_o = O.std_errors(D, th)
+    se = M.mnl_std_errors(dp, dev(th)).cpu().numpy()
+    assert np.max(np.abs(se - se_o) / se_o) <= 1e-8, np.max(np.abs(se - se_o) / se_o)
+
+
+def test_std_errors_intercept_only_closed_form():
+    prob = datagen.custom(5000, 9, 0, seed=45, coef_sd=0.6)
+    dp = device_problem(prob)
+    n = np.bincount(prob.choice, minlength=9).astype(float)
+    se = M.mnl_std_errors(dp, dev(np.log(n[1:] / n[0]))).cpu().numpy()
+    ph = n / prob.spec.N
+    assert np.allclose(se, np.sqrt((1.0 / ph[1:] + 1.0 / ph[0]) / prob.spec.N), rtol=1e-11, atol=0)
+
+
+@pytest.mark.parametrize("case", ["c1", "c5", (77, 9, 3, 4, 2), (333, 100, 5, 0, 0), (50, 3, 2, 3, 1)],
+                         ids=["c1", "c5", "yzs-ragged", "K100", "odd-f"])
+def test_predict_parity(case):
+    prob = datagen.make(case) if isinstance(case, str) else datagen.custom(*case, seed=29, coef_sd=0.4,
+                                                                         require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    P = M.mnl_predict(dp, dev(prob.theta_true)).cpu().numpy()
+    P_o = O.predict(D, prob.theta_true)
+    assert np.max(np.abs(P - P_o)) <= 1e-13

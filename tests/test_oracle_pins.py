@@ -388,3 +388,40 @@ def test_newton_cg_with_exhaustive_cg_is_the_newton_step():
     assert cg.iters == exact.iters
     assert [h["halvings"] for h in cg.history] == [h["halvings"] for h in exact.history]
     assert np.linalg.norm(cg.coef - exact.coef) <= 1e-10 * np.linalg.norm(exact.coef)
+
+
+# --- standard errors and prediction ----------------
+
+def test_std_errors_intercept_only_closed_form():
+    # At the intercept-only MLE p_k = n_k / N and -H = N (diag(p) - p p^T) over k = 1..K-1, whose
+    # inverse is (1/N)(diag(1/p_k) + (1/p_0) 1 1^T): se_k^2 = (1/N)(1/p_k + 1/p_0).
+    pr = datagen.custom(700, 6, 0, seed=41, coef_sd=0.7)
+    D = data_of(pr)
+    n = np.bincount(D.choice, minlength=D.K).astype(float)
+    th = np.log(n[1:] / n[0])
+    se = O.std_errors(D, th)
+    ph = n / D.N
+    assert np.allclose(se, np.sqrt((1.0 / ph[1:] + 1.0 / ph[0]) / D.N), rtol=1e-12, atol=0)
+
+
+def test_std_errors_K2_equal_logistic_regression():
+    # K = 2: the inverse information of binary logistic regression on the textbook design
+    pr = datagen.custom(300, 2, 2, f=1, d=1, seed=43, coef_sd=0.6)
+    D = data_of(pr)
+    th = datagen.draw(D.n_p, 13, 1, datagen.NORMAL, 0.4)
+    W = np.hstack([np.ones((D.N, 1)), D.X, -D.Z[:, 0, :], D.Z[:, 1, :], D.Y[:, 1, :] - D.Y[:, 0, :]])
+    s = expit(W @ th)
+    info = (W.T * (s * (1 - s))) @ W
+    assert np.allclose(O.std_errors(D, th), np.sqrt(np.diag(np.linalg.inv(info))), rtol=1e-11, atol=0)
+
+
+def test_predict_rows_uniform_and_logistic():
+    pr = tiny(N=120, K=5)
+    D = data_of(pr)
+    assert np.allclose(O.predict(D, np.zeros(D.n_p)), 1.0 / D.K, rtol=0, atol=1e-15)
+    P = O.predict(D, pr.theta_true)
+    assert np.allclose(P.sum(axis=1), 1.0, rtol=0, atol=1e-14) and P.min() > 0
+    pr2 = datagen.custom(100, 2, 3, f=1, d=1, seed=44, coef_sd=0.6)
+    D2 = data_of(pr2)
+    W = np.hstack([np.ones((D2.N, 1)), D2.X, -D2.Z[:, 0, :], D2.Z[:, 1, :], D2.Y[:, 1, :] - D2.Y[:, 0, :]])
+    assert np.allclose(O.predict(D2, pr2.theta_true)[:, 1], expit(W @ pr2.theta_true), rtol=1e-13, atol=0)

@@ -28,6 +28,13 @@ def main():
         if mode in ("fit", "fitcg"):
             f = M.mnl_newton_fit(dp, tol=1e-6, method="cg" if mode == "fitcg" else "newton")
             print(cfg, mode, f.iters, f.loglik, f.stats, flush=True)
+        elif mode == "se":
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            se = M.mnl_std_errors(dp, th)
+            e1.record()
+            torch.cuda.synchronize()
+            print(cfg, "std_errors ms %.3f" % e0.elapsed_time(e1), "se[:3]", se[:3].tolist(), flush=True)
         elif mode == "hv":
             v = th.clone()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
