@@ -452,6 +452,44 @@ def full_fit_extra(cfg: str, seed: int):
             "grad_norm": f.stats["grad_norm"]}
 
 
+def pass1_extra(cfg: str, seed: int, reps: int = 20):
+    """Pass 1 (a1-a4: utilities, softmax, loglik, gradient; no Hessian, no P write) of `cfg` at
+    theta_true: the kernel's device time (CUDA events around the launch, inside the library) and
+    its algorithmic HBM bytes 8N(p + K(f + d)) + 4N (X, Y, Z, choice read once) against the HBM
+    peak; plus the truncated-Newton (CG) fit of the same config."""
+    import torch
+    import paper_1404_3177_b200 as M
+    prob = datagen.make(cfg, seed=seed)
+    s = prob.spec
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dp = M.problem(torch.from_numpy(prob.X).to(dev), torch.from_numpy(prob.Y).to(dev) if s.f else None,
+                   torch.from_numpy(prob.Z).to(dev) if s.d else None,
+                   torch.from_numpy(prob.choice.astype(np.int32)).to(dev), K=s.K)
+    th = torch.from_numpy(prob.theta_true).to(dev)
+    for _ in range(3):
+        M.mnl_eval(dp, th, grad=True, hess=False)
+    ts = []
+    for _ in range(reps):
+        M.mnl_eval(dp, th, grad=True, hess=False)
+        ts.append(M.last_eval_ms())
+    ms = float(np.median(ts))
+    nbytes = 8 * s.N * (s.p + s.K * (s.f + s.d)) + 4 * s.N
+    peaks, _ = load_peaks()
+    hbm = float(peaks.get("hbm_gbs") or 6542.1)  # measured copy bandwidth (MEASURED_PEAKS.json)
+    gbs = nbytes / (ms / 1e3) / 1e9
+    M.mnl_newton_fit(dp, tol=1e-6, method="cg")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f = M.mnl_newton_fit(dp, tol=1e-6, method="cg")
+    t_cg = time.perf_counter() - t0
+    return {"config": f"{cfg}: N={s.N} K={s.K} p={s.p} f={s.f} d={s.d} n_p={s.n_params}",
+            "pass1_roofline": {"kernel": "k_eval_kernel (fused a1-a4 pass, gradient, no Hessian)", "bound": "hbm",
+                               "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                               "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": ms},
+            "cg_fit": {"fit_s": t_cg, "iters": f.iters, "cg_iters": f.stats["cg_iters"], "status": f.status,
+                       "grad_norm": f.stats["grad_norm"], "loglik": f.loglik}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -478,6 +516,7 @@ def main():
     single = res.get("n_gpus", 1) == 1 and "data-parallel" not in res["config"]["parallelism"]
     if single and not args.no_extra and args.config != "c5":
         res["extra_full_fit"] = full_fit_extra("c5", args.seed)
+        res["extra_full_fit"].update(pass1_extra("c5", args.seed))
     if not args.no_cpu_baseline and single:
         res["cpu_baseline"] = cpu_baseline(prob, args.oracle_sample)
     print(json.dumps(res), flush=True)

@@ -207,6 +207,10 @@ int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, v
  * (weights every evaluation, design products once per packed design; 0 when generated in-kernel). */
 int mnl_last_hessian_times(double out[7]);
 
+/* Device time (ms, CUDA events on the call's stream) of the last pass-1 kernel (a1-a4, the fused
+ * utility / softmax / loglik / gradient pass) launched by any call. */
+int mnl_last_eval_ms(double* ms);
+
 /* Kernel launches made by the last call on this thread (for the bench's gpu_launches). */
 int64_t mnl_last_launch_count(void);
 

@@ -23,7 +23,7 @@ MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_
 EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex", "mnl_eval_host",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
             "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec",
-            "mnl_std_errors", "mnl_predict")
+            "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms")
 
 MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
 MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
@@ -86,6 +86,8 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_opts.restype = ctypes.c_int
     lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_hessvec.restype = ctypes.c_int
+    lib.mnl_last_eval_ms.argtypes = [ctypes.POINTER(D)]
+    lib.mnl_last_eval_ms.restype = ctypes.c_int
     lib.mnl_std_errors.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V]
     lib.mnl_std_errors.restype = ctypes.c_int
     lib.mnl_predict.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V]
@@ -122,6 +124,15 @@ def num_params(K: int, p: int, f: int = 0, d: int = 0) -> int:
 def last_launch_count() -> int:
     """Kernel launches made by the last library call (counted by the library)."""
     return int(load().mnl_last_launch_count())
+
+
+def last_eval_ms() -> float:
+    """Device time (ms) of the last pass-1 kernel."""
+    v = ctypes.c_double(0.0)
+    rc = load().mnl_last_eval_ms(ctypes.byref(v))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_last_eval_ms")
+    return v.value
 
 
 def last_hessian_times() -> dict:

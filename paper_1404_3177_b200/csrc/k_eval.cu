@@ -1215,12 +1215,12 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
     // fixed block order; the loads of 8 blocks are issued together (the partials sit in L2)
     double s = 0.0, c = 0.0;
     int b = 0;
-    for (; b + 8 <= nblk; b += 8) {
-      double v[8];
+    for (; b + 16 <= nblk; b += 16) {
+      double v[16];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = __ldcg(part + (size_t)(b + t) * n_part + 2 + r);
+      for (int t = 0; t < 16; ++t) v[t] = __ldcg(part + (size_t)(b + t) * n_part + 2 + r);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) neu_add(s, c, v[t]);
+      for (int t = 0; t < 16; ++t) neu_add(s, c, v[t]);
     }
     for (; b < nblk; ++b) neu_add(s, c, __ldcg(part + (size_t)b * n_part + 2 + r));
     grad[r] = s + c;
@@ -1243,23 +1243,24 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
     if (tid < o) red[tid] += red[tid + o];
     __syncthreads();
   }
-  if (tid == 0) {
-    double s = 0.0, c = 0.0;
-    int b = 0;
-    for (; b + 4 <= nblk; b += 4) {
-      double v[8];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        v[2 * t] = __ldcg(part + (size_t)(b + t) * n_part);
-        v[2 * t + 1] = __ldcg(part + (size_t)(b + t) * n_part + 1);
-      }
-#pragma unroll
-      for (int t = 0; t < 8; ++t) neu_add(s, c, v[t]);
-    }
-    for (; b < nblk; ++b) {
+  double s = 0.0, c = 0.0;
+  if (tid < 32) {
+    // loglik: lane l sums blocks l, l + 32, ... (Neumaier), then lane 0 folds the 32 lane sums in
+    // lane order (fixed order: deterministic)
+    for (int b = tid; b < nblk; b += 32) {
       neu_add(s, c, __ldcg(part + (size_t)b * n_part));
       neu_add(s, c, __ldcg(part + (size_t)b * n_part + 1));
     }
+    double S = 0.0, C = 0.0;
+    for (int l = 0; l < 32; ++l) {
+      const double sl = __shfl_sync(0xffffffffu, s, l), cl = __shfl_sync(0xffffffffu, c, l);
+      neu_add(S, C, sl);
+      neu_add(S, C, cl);
+    }
+    s = S;
+    c = C;
+  }
+  if (tid == 0) {
     const double l = s + c;
     scal[0] = l;
     scal[1] = red[0];

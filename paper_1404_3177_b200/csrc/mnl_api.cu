@@ -63,6 +63,7 @@ struct Workspace {
   size_t czch = 0;
   size_t chX = 0, chY = 0, chZ = 0, chcoef = 0, chout = 0, chH = 0, chch = 0;
   cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_eval[2] = {nullptr, nullptr};  // around the last pass-1 kernel
 };
 
 Workspace g_ws;
@@ -135,8 +136,14 @@ int run_eval(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X, c
              double* loglik_dev, double* scal_h, cudaStream_t st) {
   if (!grow(&W.part, &W.cpart, (size_t)ep.grid * ep.n_part)) return MNL_ERR_CUDA;
   cudaMemsetAsync(W.err, 0, sizeof(int), st);
+  if (!W.ev_eval[0]) {
+    cudaEventCreate(&W.ev_eval[0]);
+    cudaEventCreate(&W.ev_eval[1]);
+  }
+  cudaEventRecord(W.ev_eval[0], st);
   cudaError_t e = launch_eval(D, ep, X, Y, Z, choice, coef, pk, grad != nullptr, writeP, W.part, W.err, st);
   if (e != cudaSuccess) return MNL_ERR_CUDA;
+  cudaEventRecord(W.ev_eval[1], st);
   e = launch_eval_finalize(D, ep, W.part, grad != nullptr, grad, loglik_dev, W.scal, W.err, W.counter, st);
   if (e != cudaSuccess) return MNL_ERR_CUDA;
   if (cudaMemcpyAsync(scal_h, W.scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -390,6 +397,17 @@ const char* mnl_status_string(int code) {
 
 int64_t mnl_last_launch_count(void) { return g_launches; }
 
+int mnl_last_eval_ms(double* ms) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!ms || !g_ws.ev_eval[0]) return MNL_ERR_ARG;
+  float t = 0.f;
+  if (cudaEventSynchronize(g_ws.ev_eval[1]) != cudaSuccess ||
+      cudaEventElapsedTime(&t, g_ws.ev_eval[0], g_ws.ev_eval[1]) != cudaSuccess)
+    return MNL_ERR_CUDA;
+  *ms = t;
+  return MNL_OK;
+}
+
 int mnl_last_hessian_times(double out[7]) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!out) return MNL_ERR_ARG;
@@ -615,6 +633,8 @@ void mnl_release(void) {
   cudaFree(W.hch);
   cudaFree(W.zch);
   if (W.hstream) cudaStreamDestroy(W.hstream);
+  for (cudaEvent_t ev : W.ev_eval)
+    if (ev) cudaEventDestroy(ev);
   W = Workspace();
 }
 
