@@ -78,6 +78,18 @@ int mnl_eval(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
              const double* X, const double* Y, const double* Z, const int32_t* choice,
              const double* coef, double* loglik, double* grad, double* hess, void* stream);
 
+/* Asynchronous mnl_eval: enqueues the same kernels on `stream` and returns without synchronising.
+ *   status  dev int32 [1] out, written on the stream after the pass: MNL_OK, MNL_ERR_ARG (a choice
+ *           outside [0, K)) or MNL_ERR_NONFINITE (non-finite loglik)
+ * Host-side argument errors (sizes, NULL pointers, misalignment) are returned immediately; the
+ * return value MNL_OK means "enqueued". The first call for a problem shape allocates library
+ * scratch (which synchronises); later calls of the same shape launch only. The scratch is shared:
+ * calls on different streams must not overlap in time. */
+int mnl_eval_async(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                   const double* X, const double* Y, const double* Z, const int32_t* choice,
+                   const double* coef, double* loglik, double* grad, double* hess, int32_t* status,
+                   void* stream);
+
 /* Newton-Raphson maximum-likelihood fit.
  *   coef0   dev [n_p] start, or NULL => zeros (reading R9)
  *   tol     ||grad||_2 threshold (gtol; reading R10), > 0

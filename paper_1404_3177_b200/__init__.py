@@ -23,7 +23,7 @@ MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_
 EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex", "mnl_eval_host",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
             "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec",
-            "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms")
+            "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms", "mnl_eval_async")
 
 MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
 MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
@@ -86,6 +86,8 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_opts.restype = ctypes.c_int
     lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_hessvec.restype = ctypes.c_int
+    lib.mnl_eval_async.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V, V, V]
+    lib.mnl_eval_async.restype = ctypes.c_int
     lib.mnl_last_eval_ms.argtypes = [ctypes.POINTER(D)]
     lib.mnl_last_eval_ms.restype = ctypes.c_int
     lib.mnl_std_errors.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V]
@@ -217,6 +219,24 @@ def mnl_eval(prob: Problem, coef, grad: bool = True, hess: bool = False, stream=
     if rc != MNL_OK:
         raise MnlError(rc, "mnl_eval")
     return ll, g, H
+
+
+def mnl_eval_async(prob: Problem, coef, grad: bool = True, hess: bool = False, stream=None):
+    """Enqueue an evaluation without synchronising: returns (loglik[1], grad | None, hess | None,
+    status[1] int32) device tensors, valid once the stream has passed the work."""
+    torch = _torch()
+    dev = prob.choice.device
+    ll = torch.empty(1, dtype=torch.float64, device=dev)
+    st = torch.empty(1, dtype=torch.int32, device=dev)
+    g = torch.empty(prob.n_p, dtype=torch.float64, device=dev) if grad else None
+    H = torch.empty(prob.n_p, prob.n_p, dtype=torch.float64, device=dev) if hess else None
+    X, Y, Z, ch = prob.ptrs()
+    rc = load().mnl_eval_async(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, ch, coef.data_ptr(), ll.data_ptr(),
+                               g.data_ptr() if grad else None, H.data_ptr() if hess else None, st.data_ptr(),
+                               _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_eval_async")
+    return ll, g, H, st
 
 
 @dataclass

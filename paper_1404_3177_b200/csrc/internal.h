@@ -59,7 +59,8 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
                         const Packed* pk, bool want_grad, bool writeP, double* part, int* err,
                         cudaStream_t st);
 // Fixed-order reduction of the CTA partials -> loglik, grad (optional); scal[0] = l,
-// scal[1] = ||g||^2, scal[2] = err flag (as double). `counter` is a zeroed int.
+// scal[1] = ||g||^2, scal[2] = err flag (as double), *status_out (if given) = the mnl_status of the
+// evaluation (MNL_ERR_ARG for a bad choice, MNL_ERR_NONFINITE). `counter` is a zeroed int.
 // Hessian-vector product pass: part receives H v (gradient slots) from P_i in pk->Pr (written by the
 // last evaluation with writeP) and s_i = J_i v.
 cudaError_t launch_hessvec(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
@@ -73,7 +74,8 @@ cudaError_t launch_cg_update(int n, double alpha, const double* p, const double*
 cudaError_t launch_cg_dir(int n, double beta, const double* r, double* p, cudaStream_t st);
 cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const double* part,
                                  bool want_grad, double* grad, double* loglik_out, double* scal,
-                                 const int* err, unsigned* counter, cudaStream_t st);
+                                 const int* err, unsigned* counter, cudaStream_t st,
+                                 int* status_out = nullptr);
 cudaError_t launch_pack(const Dims& D, const Packed& pk, const double* X, const double* Z,
                         cudaStream_t st);
 cudaError_t launch_axpy_pow2(int n, const double* theta, const double* delta, int j,

@@ -1206,7 +1206,7 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
                                                       int nblk, int n_p, int want_grad,
                                                       double* grad, double* loglik_out,
                                                       double* scal, const int* err,
-                                                      unsigned* counter) {
+                                                      unsigned* counter, int* status_out) {
   __shared__ double red[256];
   __shared__ bool last;
   const int tid = threadIdx.x;
@@ -1266,6 +1266,7 @@ __global__ void __launch_bounds__(256) k_eval_finalize(const double* __restrict_
     scal[1] = red[0];
     scal[2] = (double)(*err);
     if (loglik_out) *loglik_out = l;
+    if (status_out) *status_out = *err ? 1 /* MNL_ERR_ARG */ : (isfinite(l) ? 0 : 5 /* MNL_ERR_NONFINITE */);
     *counter = 0u;
   }
 }
@@ -1507,10 +1508,10 @@ cudaError_t launch_cg_dir(int n, double beta, const double* r, double* p, cudaSt
 
 cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const double* part,
                                  bool want_grad, double* grad, double* loglik_out, double* scal,
-                                 const int* err, unsigned* counter, cudaStream_t st) {
+                                 const int* err, unsigned* counter, cudaStream_t st, int* status_out) {
   int blocks = want_grad ? (D.n_p + 255) / 256 : 1;
   k_eval_finalize<<<blocks, 256, 0, st>>>(part, plan.n_part, plan.grid, D.n_p, want_grad, grad,
-                                          loglik_out, scal, err, counter);
+                                          loglik_out, scal, err, counter, status_out);
   count_launch();
   return cudaGetLastError();
 }

@@ -466,6 +466,41 @@ int mnl_hessvec(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const dou
   return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
 }
 
+int mnl_eval_async(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
+                   const double* Z, const int32_t* choice, const double* coef, double* loglik, double* grad,
+                   double* hess, int32_t* status, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_launches = 0;
+  Dims D;
+  if (!dims_of(N, K, p, f, d, &D) || !check_inputs(D, X, Y, Z, choice) || !coef || !loglik || !status)
+    return MNL_ERR_ARG;
+  Workspace& W = g_ws;
+  int rc = init_device(W);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  EvalPlan ep;
+  if (!eval_plan(D, &ep, W.sms)) return MNL_ERR_ARG;
+  Packed pk{};
+  const bool want_h = hess != nullptr;
+  if (want_h) {
+    if (!ensure_packed(W, D, &pk)) return MNL_ERR_CUDA;
+    if (launch_pack(D, pk, X, Z, st) != cudaSuccess) return MNL_ERR_CUDA;
+    if (W.hp) hess_plan_design_changed(W.hp);
+  }
+  if (!grow(&W.part, &W.cpart, (size_t)ep.grid * ep.n_part)) return MNL_ERR_CUDA;
+  HessPlan* hp = want_h ? get_hess_plan(W, D, pk) : nullptr;  // (first use of a shape allocates)
+  if (want_h && !hp) return MNL_ERR_CUDA;
+  cudaMemsetAsync(W.err, 0, sizeof(int), st);
+  if (launch_eval(D, ep, X, Y, Z, choice, coef, want_h ? &pk : nullptr, grad != nullptr, want_h, W.part, W.err, st) !=
+      cudaSuccess)
+    return MNL_ERR_CUDA;
+  if (launch_eval_finalize(D, ep, W.part, grad != nullptr, grad, loglik, W.scal, W.err, W.counter, st, status) !=
+      cudaSuccess)
+    return MNL_ERR_CUDA;
+  if (want_h && launch_hessian(hp, D, pk, Y, hess, D.n_p, +1.0, st) != cudaSuccess) return MNL_ERR_CUDA;
+  return MNL_OK;
+}
+
 int mnl_std_errors(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const double* X, const double* Y,
                    const double* Z, const int32_t* choice, const double* coef, double* se, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);

@@ -116,7 +116,8 @@ def test_eval_yz_paths(mode):
     if mode != "default":
         os.environ[mode] = "1"
     try:
-        for N, K, p, f, d in [(1000, 4, 3, 2, 1), (333, 50, 5, 10, 5), (2049, 6, 17, 2, 3), (65, 20, 0, 4, 0)]:
+        for N, K, p, f, d in [(1000, 4, 3, 2, 1), (333, 50, 5, 10, 5), (2049, 6, 17, 2, 3), (65, 20, 0, 4, 0),
+                              (1, 4, 2, 2, 1), (3, 6, 0, 2, 2), (17, 64, 1, 16, 8), (40, 33, 2, 6, 7)]:
             prob = datagen.custom(N, K, p, f, d, seed=7, coef_sd=0.3, require_all_classes=False)
             D = oracle_data(prob)
             dp = device_problem(prob)
@@ -440,3 +441,25 @@ def test_predict_parity(case):
     P = M.mnl_predict(dp, dev(prob.theta_true)).cpu().numpy()
     P_o = O.predict(D, prob.theta_true)
     assert np.max(np.abs(P - P_o)) <= 1e-13
+
+
+def test_eval_async_matches_sync_and_reports_status():
+    """mnl_eval_async enqueues the same kernels (identical results) and reports errors on device."""
+    for case in ["c1", (500, 9, 4, 2, 3), (300, 20, 6, 0, 0)]:
+        prob = datagen.make(case) if isinstance(case, str) else datagen.custom(*case, seed=37, coef_sd=0.4,
+                                                                             require_all_classes=False)
+        dp = device_problem(prob)
+        th = dev(datagen.perturbed_theta(prob, 0.2))
+        l0, g0, H0 = M.mnl_eval(dp, th, grad=True, hess=True)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            l1, g1, H1, st = M.mnl_eval_async(dp, th, grad=True, hess=True, stream=s)
+        s.synchronize()
+        assert int(st.item()) == M.MNL_OK
+        assert torch.equal(l0, l1) and torch.equal(g0, g1) and torch.equal(H0, H1)
+    bad = dp.choice.clone()
+    bad[7] = prob.spec.K
+    dbad = M.problem(dp.X, dp.Y, dp.Z, bad, K=prob.spec.K)
+    _, _, _, st = M.mnl_eval_async(dbad, th, grad=True, hess=False)
+    torch.cuda.synchronize()
+    assert int(st.item()) == M.MNL_ERR_ARG
