@@ -186,9 +186,22 @@ def run_dp(args):
         dist.all_reduce(t)
 
     theta0 = torch.zeros(spec.n_params, dtype=torch.float64, device=dev)
+    pk_inner = DP.cuda_packer()
+
+    def pack(H):
+        v = pk_inner[0](H)
+        launches[0] += M.last_launch_count()
+        return v
+
+    def unpack(v, n):
+        H = pk_inner[1](v, n)
+        launches[0] += M.last_launch_count()
+        return H
+
+    packer = (pack, unpack)
 
     def step():
-        return DP.newton_fit_dp(evaluate, all_reduce, solve, theta0, tol=1e-300, max_iter=1)
+        return DP.newton_fit_dp(evaluate, all_reduce, solve, theta0, tol=1e-300, max_iter=1, packer=packer)
 
     for _ in range(args.warmup):
         step()
@@ -249,7 +262,8 @@ def run_dp(args):
             "config": {"workload": f"{args.config}: N={spec.N} K={spec.K} p={spec.p} f={spec.f} d={spec.d} "
                                    f"n_p={spec.n_params}, one Newton iteration from theta=0 per step",
                        "l2": "inputs larger than L2 (no flush)",
-                       "parallelism": f"data-parallel over individuals, {ws} ranks, NCCL all-reduce of (l, g, H)"},
+                       "parallelism": f"data-parallel over individuals, {ws} ranks, one NCCL all-reduce of "
+                                      f"(l, g, packed upper triangle of H)"},
             "s_per_newton_iter": ms / args.steps / 1e3,
             "roofline": roof,
             "gpu_launches": int(launches[0]),

@@ -211,6 +211,13 @@ int mnl_cholesky(int32_t n, double* A, void* stream);
 /* Solve (L L^T) x = b given the factor from mnl_cholesky; b and x dev [n], may alias. */
 int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, void* stream);
 
+/* Packed upper triangle of a symmetric dev [n][n] row-major matrix: packed[off(i) + j - i] =
+ * H[i][j] for j >= i, off(i) = i n - i (i - 1) / 2 (n (n + 1) / 2 doubles), and back (both
+ * triangles written, exactly symmetric). The data-parallel fit all-reduces [l, g, packed H] in one
+ * collective (half the bytes of the full matrix). */
+int mnl_sym_pack(int32_t n, const double* H, double* packed, void* stream);
+int mnl_sym_unpack(int32_t n, const double* packed, double* H, void* stream);
+
 /* Device times (ms, CUDA events on the call's stream) of the last Hessian assembly:
  * out[0] beta-beta DMMA GEMM over whole 128-column tiles (J1), out[1] its split-N reduction,
  * out[2] the narrow tail GEMM of the remaining vech columns (J1b; 0 if none), out[3] its reduction,

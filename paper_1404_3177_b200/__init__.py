@@ -23,7 +23,8 @@ MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_
 EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex", "mnl_eval_host",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
             "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec",
-            "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms", "mnl_eval_async")
+            "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms", "mnl_eval_async", "mnl_sym_pack",
+            "mnl_sym_unpack")
 
 MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
 MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
@@ -86,6 +87,10 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_opts.restype = ctypes.c_int
     lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_hessvec.restype = ctypes.c_int
+    lib.mnl_sym_pack.argtypes = [I32, V, V, V]
+    lib.mnl_sym_pack.restype = ctypes.c_int
+    lib.mnl_sym_unpack.argtypes = [I32, V, V, V]
+    lib.mnl_sym_unpack.restype = ctypes.c_int
     lib.mnl_eval_async.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V, V, V]
     lib.mnl_eval_async.restype = ctypes.c_int
     lib.mnl_last_eval_ms.argtypes = [ctypes.POINTER(D)]
@@ -304,6 +309,29 @@ def mnl_predict(prob: Problem, coef, stream=None):
     if rc != MNL_OK:
         raise MnlError(rc, "mnl_predict")
     return P
+
+
+def mnl_sym_pack(H, out=None, stream=None):
+    """Upper triangle of the symmetric CUDA float64 [n, n] H, packed row by row (n(n+1)/2)."""
+    torch = _torch()
+    n = H.shape[0]
+    if out is None:
+        out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=H.device)
+    rc = load().mnl_sym_pack(n, H.data_ptr(), out.data_ptr(), _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_sym_pack")
+    return out
+
+
+def mnl_sym_unpack(packed, n: int, out=None, stream=None):
+    """The symmetric [n, n] matrix from its packed upper triangle (both triangles written)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(n, n, dtype=torch.float64, device=packed.device)
+    rc = load().mnl_sym_unpack(n, packed.data_ptr(), out.data_ptr(), _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_sym_unpack")
+    return out
 
 
 def mnl_cholesky(A, stream=None):

@@ -95,6 +95,10 @@ void hess_plan_design_changed(HessPlan* hp);
 // Phase times of the last launch_hessian (valid once the stream has passed it).
 void hess_last_times(HessPlan* hp, double out[7]);
 
+// Packed upper triangle of a symmetric dev [n][n] matrix (row i: columns i..n-1) and back (mirrored).
+cudaError_t launch_sym_pack(int n, const double* H, double* out, cudaStream_t st);
+cudaError_t launch_sym_unpack(int n, const double* in, double* H, cudaStream_t st);
+
 // ---- k_chol.cu -------------------------------------------------------------------------
 // In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.
 cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t st);

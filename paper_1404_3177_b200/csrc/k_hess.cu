@@ -1292,4 +1292,34 @@ void hess_last_times(HessPlan* hp, double out[7]) {
   }
 }
 
+// ---- packed upper triangle (the data-parallel exchange) -----------------------
+// Row i of the upper triangle (columns i..n-1) starts at off(i) = i n - i (i - 1) / 2. One CTA per
+// row; pack reads H[i][i..] and writes contiguously (coalesced both sides); unpack writes the
+// row and mirrors it into column i (exactly symmetric result).
+__global__ void k_sym_pack(int n, const double* __restrict__ H, double* __restrict__ out) {
+  const int64_t i = blockIdx.x;
+  const int64_t off = i * n - i * (i - 1) / 2;
+  for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) out[off + (j - i)] = H[i * n + j];
+}
+__global__ void k_sym_unpack(int n, const double* __restrict__ in, double* __restrict__ H) {
+  const int64_t i = blockIdx.x;
+  const int64_t off = i * n - i * (i - 1) / 2;
+  for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) {
+    const double v = in[off + (j - i)];
+    H[i * n + j] = v;
+    H[j * n + i] = v;
+  }
+}
+
+cudaError_t launch_sym_pack(int n, const double* H, double* out, cudaStream_t st) {
+  k_sym_pack<<<n, 256, 0, st>>>(n, H, out);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_sym_unpack(int n, const double* in, double* H, cudaStream_t st) {
+  k_sym_unpack<<<n, 256, 0, st>>>(n, in, H);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace mnl

@@ -654,6 +654,22 @@ int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, v
   return MNL_OK;
 }
 
+int mnl_sym_pack(int32_t n, const double* H, double* packed, void* stream) {
+  g_launches = 0;
+  if (n < 1 || !H || !packed) return MNL_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (launch_sym_pack(n, H, packed, st) != cudaSuccess) return MNL_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
+}
+
+int mnl_sym_unpack(int32_t n, const double* packed, double* H, void* stream) {
+  g_launches = 0;
+  if (n < 1 || !H || !packed) return MNL_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (launch_sym_unpack(n, packed, H, st) != cudaSuccess) return MNL_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? MNL_OK : MNL_ERR_CUDA;
+}
+
 void mnl_release(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   Workspace& W = g_ws;

@@ -2,7 +2,8 @@
 
 The log-likelihood, gradient and Hessian are sums over individuals, so
 each rank owns a contiguous slice of the individuals, evaluates its partial (l_r, g_r, H_r) with the
-single-GPU kernels, and ONE all-reduce (sum) per iteration forms (l, g, H) on every rank.  Every
+single-GPU kernels, and ONE all-reduce (sum) of [l, g, packed upper triangle of H] per iteration
+forms (l, g, H) on every rank.  Every
 rank then factors the same -H and takes the same step (all-reduce results are identical on all
 ranks), so the iterates stay bitwise identical without broadcasting the coefficients.  Each
 line-search trial needs one scalar all-reduce.
@@ -40,8 +41,37 @@ class DPFit:
     halvings: list = field(default_factory=list)
 
 
-def newton_fit_dp(evaluate, all_reduce, solve, theta0, tol: float = 1e-6, max_iter: int = 50) -> DPFit:
-    """Newton-Raphson with step halving on data sharded over ranks (identical on every rank)."""
+def torch_packer():
+    """(pack, unpack) of the upper triangle with torch indexing (host-logic tests on CPU)."""
+    import torch
+
+    cache = {}
+
+    def idx(n, dev):
+        if (n, dev) not in cache:
+            cache[(n, dev)] = torch.triu_indices(n, n, device=dev)
+        return cache[(n, dev)]
+
+    def pack(H):
+        iu = idx(H.shape[0], H.device)
+        return H[iu[0], iu[1]]
+
+    def unpack(v, n):
+        iu = idx(n, v.device)
+        H = torch.empty(n, n, dtype=v.dtype, device=v.device)
+        H[iu[0], iu[1]] = v
+        H[iu[1], iu[0]] = v
+        return H
+
+    return pack, unpack
+
+
+def newton_fit_dp(evaluate, all_reduce, solve, theta0, tol: float = 1e-6, max_iter: int = 50,
+                  packer=None) -> DPFit:
+    """Newton-Raphson with step halving on data sharded over ranks (identical on every rank).
+    With `packer` = (pack, unpack) the Hessian evaluation exchanges ONE buffer [l, g, upper
+    triangle of H] (n_p + 1 + n_p (n_p + 1) / 2 doubles, half the bytes of the full matrix);
+    without it, [l, g] and the full H in two all-reduces."""
     import torch
 
     theta = theta0.clone()
@@ -49,6 +79,11 @@ def newton_fit_dp(evaluate, all_reduce, solve, theta0, tol: float = 1e-6, max_it
 
     def reduced(th, want_hess):
         l, g, H = evaluate(th, True, want_hess)
+        n = g.shape[0]
+        if H is not None and packer is not None:
+            buf = torch.cat([l.reshape(1).to(g.dtype), g, packer[0](H)])
+            all_reduce(buf)
+            return float(buf[0].item()), buf[1:n + 1], packer[1](buf[n + 1:], n)
         lg = torch.cat([l.reshape(1).to(g.dtype), g])
         all_reduce(lg)
         if H is not None:
@@ -99,6 +134,16 @@ def cuda_evaluator(prob):
         return mnl_eval(prob, theta, grad=True, hess=want_hess)
 
     return evaluate
+
+
+def cuda_packer():
+    """(pack, unpack) with the library's kernels (mnl_sym_pack / mnl_sym_unpack)."""
+    from . import mnl_sym_pack, mnl_sym_unpack
+
+    def unpack(v, n):
+        return mnl_sym_unpack(v.contiguous(), n)
+
+    return (lambda H: mnl_sym_pack(H.contiguous())), unpack
 
 
 def cuda_solver():

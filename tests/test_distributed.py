@@ -23,7 +23,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, shape, start_scale, out_path):
+def _worker(rank, world, port, shape, start_scale, out_path, packed=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -48,7 +48,7 @@ def _worker(rank, world, port, shape, start_scale, out_path):
         return DP.MNL_OK, torch.cholesky_solve(g.reshape(-1, 1), L).reshape(-1)
 
     theta0 = torch.full((prob.spec.n_params,), start_scale, dtype=torch.float64)
-    fit = DP.newton_fit_dp(evaluate, all_reduce, solve, theta0, tol=1e-8)
+    fit = DP.newton_fit_dp(evaluate, all_reduce, solve, theta0, tol=1e-8, packer=DP.torch_packer() if packed else None)
     coefs = [torch.zeros_like(fit.coef) for _ in range(world)]
     dist.all_gather(coefs, fit.coef)
     if rank == 0:
@@ -57,10 +57,11 @@ def _worker(rank, world, port, shape, start_scale, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape,start", [((301, 4, 2, 1, 1), 0.0), ((250, 3, 3, 0, 2), 2.0)])
-def test_data_parallel_fit_equals_single_process_oracle(tmp_path, shape, start):
+@pytest.mark.parametrize("shape,start,packed", [((301, 4, 2, 1, 1), 0.0, True), ((250, 3, 3, 0, 2), 2.0, True),
+                                                ((301, 4, 2, 1, 1), 0.0, False)])
+def test_data_parallel_fit_equals_single_process_oracle(tmp_path, shape, start, packed):
     out = str(tmp_path / "fit.npz")
-    mp.spawn(_worker, args=(2, _free_port(), shape, start, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), shape, start, out, packed), nprocs=2, join=True)
     r = np.load(out)
     N, K, p, f, d = shape
     prob = datagen.custom(N, K, p, f, d, seed=51, coef_sd=0.5)
@@ -81,3 +82,12 @@ def test_shard_range_partitions():
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
             sizes = [b - a for a, b in parts]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_torch_packer_round_trip():
+    pack, unpack = DP.torch_packer()
+    A = torch.randn(7, 7, dtype=torch.float64)
+    S = A + A.T
+    v = pack(S)
+    assert v.numel() == 28 and torch.equal(v[:7], S[0]) and torch.equal(v[7:13], S[1, 1:])
+    assert torch.equal(unpack(v, 7), S)

@@ -463,3 +463,24 @@ def test_eval_async_matches_sync_and_reports_status():
     _, _, _, st = M.mnl_eval_async(dbad, th, grad=True, hess=False)
     torch.cuda.synchronize()
     assert int(st.item()) == M.MNL_ERR_ARG
+
+
+def test_sym_pack_round_trip_and_dp_driver_world1():
+    """Packed upper triangle (exact round trip) and the data-parallel driver at world size 1 with
+    the CUDA evaluator, solver and packer: the same fit as mnl_newton_fit."""
+    from paper_1404_3177_b200 import distributed as DP
+    n = 300
+    A = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    S = A + A.T
+    v = M.mnl_sym_pack(S)
+    iu = torch.triu_indices(n, n, device="cuda")
+    assert torch.equal(v, S[iu[0], iu[1]])
+    assert torch.equal(M.mnl_sym_unpack(v, n), S)
+    prob = datagen.custom(3000, 6, 5, 2, 1, seed=61, coef_sd=0.4)
+    dp = device_problem(prob)
+    ref = M.mnl_newton_fit(dp, tol=1e-8)
+    fit = DP.newton_fit_dp(DP.cuda_evaluator(dp), lambda t: None, DP.cuda_solver(),
+                           torch.zeros(prob.spec.n_params, dtype=torch.float64, device="cuda"), tol=1e-8,
+                           packer=DP.cuda_packer())
+    assert fit.status == M.MNL_OK and fit.iters == ref.iters
+    assert torch.linalg.norm(fit.coef - ref.coef) <= 1e-9 * torch.linalg.norm(ref.coef)

@@ -29,7 +29,7 @@ def flops_bytes(spec):
     nb, na = (K - 1) * q, K * d
     j2 = 2.0 * N * (nb + na + f) * (na + f) if (d + f) else 0.0
     ar = 2.0 * N * K * (q + d + f) * (d + f) if (d + f) else 0.0
-    pass1_bytes = 8.0 * N * (p + K * (f + d)) + 4.0 * N + 8.0 * N * (K + f)
+    pass1_bytes = 8.0 * N * (p + K * (f + d)) + 4.0 * N  # gradient pass: X, Y, Z, choice read once
     return j1 + j2 + ar, pass1_bytes
 
 
@@ -46,11 +46,8 @@ def gpu_row(cfg, reps=5):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p1, hs, ev = [], [], []
     for r in range(reps + 2):
-        e0.record()
         M.mnl_eval(dp, th, grad=True, hess=False)
-        e1.record()
-        torch.cuda.synchronize()
-        p1.append(e0.elapsed_time(e1))
+        p1.append(M.last_eval_ms())  # the pass-1 kernel's device time (events inside the library)
         e0.record()
         M.mnl_eval(dp, th, grad=True, hess=True)
         e1.record()
@@ -66,11 +63,22 @@ def gpu_row(cfg, reps=5):
         f = M.mnl_newton_fit(dp, tol=1e-6)
         fits.append((time.perf_counter() - t0, f))
     fit_s, f = sorted(fits, key=lambda x: x[0])[1]
+    M.mnl_newton_fit(dp, tol=1e-6, method="cg")
+    t0 = time.perf_counter()
+    fcg = M.mnl_newton_fit(dp, tol=1e-6, method="cg")
+    cg_s = time.perf_counter() - t0
+    fc = torch.from_numpy(np.ascontiguousarray(prob.theta_true)).to(dev)
+    M.mnl_std_errors(dp, fc)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    M.mnl_std_errors(dp, fc)
+    se_s = time.perf_counter() - t0
     F, B = flops_bytes(s)
     return dict(cfg=cfg, N=s.N, K=s.K, n_p=s.n_params, pass1_ms=p1, pass1_GBs=B / (p1 / 1e3) / 1e9,
                 hess_ms=hs, hess_evals_s=1e3 / hs, hess_tflops=F / (hs / 1e3) / 1e12, eval_with_hess_ms=ev,
                 fit_s=fit_s, iters=f.iters, halvings=f.stats["halvings"], s_per_iter=fit_s / max(f.iters, 1),
-                hess_ms_in_fit=f.stats["hess_ms"], chol_ms_in_fit=f.stats["chol_ms"], status=f.status)
+                hess_ms_in_fit=f.stats["hess_ms"], chol_ms_in_fit=f.stats["chol_ms"], status=f.status,
+                cg_fit_s=cg_s, cg_iters=fcg.iters, cg_inner=fcg.stats["cg_iters"], std_errors_s=se_s)
 
 
 def oracle_row(cfg, budget_s=60.0):
