@@ -484,3 +484,34 @@ def test_sym_pack_round_trip_and_dp_driver_world1():
                            packer=DP.cuda_packer())
     assert fit.status == M.MNL_OK and fit.iters == ref.iters
     assert torch.linalg.norm(fit.coef - ref.coef) <= 1e-9 * torch.linalg.norm(ref.coef)
+
+
+@pytest.mark.parametrize("shape", [(300, 4, 3, 2, 1), (200, 50, 5, 10, 5), (500, 100, 6, 0, 0), (90, 3, 2, 3, 1)],
+                         ids=["yzs", "yzs-K50", "x-only", "direct-yz"])
+def test_nonfinite_and_overflow_safety(shape):
+    """R12: utilities of order 1e3 stay finite (max-shifted softmax) and match the oracle; a NaN
+    coefficient or a NaN in the data reports MNL_ERR_NONFINITE (sync) / status 5 (async)."""
+    N, K, p, f, d = shape
+    prob = datagen.custom(N, K, p, f, d, seed=71, coef_sd=0.4, require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    big = prob.theta_true * 400.0
+    l_o, g_o, _ = O.mnl_eval(D, big, want_hess=False)
+    l, g, _ = gpu_eval(dp, big, hess=False)
+    assert np.isfinite(l) and abs(l - l_o) <= 1e-10 * abs(l_o)
+    assert np.linalg.norm(g - g_o) <= 1e-10 * np.linalg.norm(g_o)
+    bad = prob.theta_true.copy()
+    bad[0] = np.nan
+    with pytest.raises(M.MnlError) as ei:
+        M.mnl_eval(dp, dev(bad), grad=True, hess=False)
+    assert ei.value.code == M.MNL_ERR_NONFINITE
+    _, _, _, st = M.mnl_eval_async(dp, dev(bad), grad=True, hess=False)
+    torch.cuda.synchronize()
+    assert int(st.item()) == M.MNL_ERR_NONFINITE
+    if f:
+        Y = dp.Y.clone()
+        Y[N // 2, K // 2, 0] = float("nan")
+        dY = M.problem(dp.X, Y, dp.Z, dp.choice, K=K)
+        with pytest.raises(M.MnlError) as ei:
+            M.mnl_eval(dY, dev(prob.theta_true), grad=True, hess=False)
+        assert ei.value.code == M.MNL_ERR_NONFINITE
