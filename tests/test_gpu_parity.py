@@ -515,3 +515,19 @@ def test_nonfinite_and_overflow_safety(shape):
         with pytest.raises(M.MnlError) as ei:
             M.mnl_eval(dY, dev(prob.theta_true), grad=True, hess=False)
         assert ei.value.code == M.MNL_ERR_NONFINITE
+
+
+@pytest.mark.parametrize("cfg", ["c5", "c4"])
+def test_recovery_of_true_coefficients(cfg):
+    """north_star / SURVEY.md §8(c) statistical pin on the large draws: z_j = (theta_hat_j -
+    theta_true_j) / se_j with se = sqrt(diag((-H)^{-1})) at theta_hat (GPU fit + mnl_std_errors):
+    max |z| < 5.5 and RMS(z) in [0.9, 1.1] over all n_p coefficients."""
+    prob = datagen.make(cfg)
+    dp = device_problem(prob)
+    fit = M.mnl_newton_fit(dp, tol=1e-6)
+    assert fit.status == M.MNL_OK
+    se = M.mnl_std_errors(dp, fit.coef).cpu().numpy()
+    z = (fit.coef.cpu().numpy() - prob.theta_true) / se
+    rms = float(np.sqrt(np.mean(z ** 2)))
+    assert np.abs(z).max() < 5.5, np.abs(z).max()
+    assert 0.9 <= rms <= 1.1, rms
