@@ -10,15 +10,18 @@
 // and, for the Hessian pass, the probability rows Pr[i] = [P_i0..P_i,K-1, ybar_i] with
 // ybar_i = sum_k P_ik y_ik (the O(K) regrouping of the generic blocks).
 //
-// Layout: CTA = 8 warps, persistent over tiles of 64 individuals (X tiles prefetched with
+// Layout: CTA = 8 warps, persistent over tiles of individuals (X tiles prefetched with
 // cp.async, double-buffered).  The two dense contractions run on the FP64 tensor pipe
 // (mma.sync m8n8k4, SASS DMMA.8x8x4):
 //   phase B  U = X~ B   (warp w: individuals 8w..8w+7 x all alternatives; the C fragment gives
 //            each lane 2 alternatives per 8-block of one individual, so the row softmax is a
 //            local reduction plus two shuffles);
 //   phase C  G += X~^T R (the beta gradient; CTA-persistent accumulators in registers).
-// Phase D (only with Y or Z) folds the alpha/gamma gradients and ybar with lanes over
-// alternatives.  CTA partials are reduced in a fixed order by k_eval_finalize (deterministic).
+// Phase E (only with Y or Z) folds the alpha/gamma gradients and ybar with lanes over
+// alternatives. Three variants: YZS (16-row tiles; every warp bulk-copies the Y/Z rows of its own
+// individuals into a 2-4 slot shared-memory ring and computes them in pairs; see phase_e_smem),
+// the register path (direct L1 loads, values held in registers) and the general direct path.
+// CTA partials are reduced in a fixed order by k_eval_finalize (deterministic).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -537,7 +540,7 @@ constexpr int YZS_F = 16, YZS_D = 8;  // register capacity of the YZS path (gamm
 // (loads -> utilities -> max / sum shuffles -> exp -> gradient sums) interleave. Lane k holds
 // alternatives k + 32 kk. Reads its rows' staged Y [K][f] and Z [K][d] from the ring.
 template <int KPL, bool HV, int NI>
-__device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const int* ch_t, double* red_w,
+__device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const int* ch_t,
                                          const double* alpha, const double* gamma,
                                          double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
                                          int64_t i0, int ii0, int KPS, int w, int lane, const double* ring_w,
@@ -741,8 +744,8 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
     }
   }
   // ---- ybar_e = sum_k P_k y_ke (writeP), gamma partials sum_k y_ke r_k, alpha partials z_kc r_k ----
-  // in halves of 8 components: gamma partials, then (writeP) the cross-lane ybar sums through an
-  // [8][33] scratch (the row's own ring slot once its reads are done, when large enough; else red_w)
+  // in halves of 8 components: gamma partials, then (writeP) the cross-lane ybar sums by a
+  // reduce-scatter over shuffles (warp_sum8)
 #pragma unroll
   for (int e8 = 0; e8 < YZS_F; e8 += 8) {
     if (e8 < f) {
@@ -816,7 +819,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
 
 // Phase E of one tile for warp w (rows w YZS_R .. + YZS_R - 1): pairs of rows, a single ragged one
 template <int KPL, bool HV>
-__device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, const int* ch_t, double* red_w,
+__device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, const int* ch_t,
                                              const double* alpha, const double* gamma,
                                              double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
                                              int64_t i0, int nt, int KPS, int w, int lane, const double* ring_w,
@@ -827,9 +830,9 @@ __device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, cons
     for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
   int jj = 0;
   if constexpr (YZS_R >= 2)
-    for (; jj + 2 <= n_mine; jj += 2) yzs_rows<KPL, HV, 2>(A, Rs, ch_t, red_w, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+    for (; jj + 2 <= n_mine; jj += 2) yzs_rows<KPL, HV, 2>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
   if (jj < n_mine)
-    yzs_rows<KPL, HV, 1>(A, Rs, ch_t, red_w, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+    yzs_rows<KPL, HV, 1>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
 }
 
 template <int KPL, int CM_MAX, bool HV, bool YZS>
@@ -998,7 +1001,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
       __syncthreads();
       bool done = false;
       if constexpr (YZS) {
-        phase_e_smem<KPL, HV>(A, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, gamz, alp, l_s, l_c, i0, nt, KPS, w,
+        phase_e_smem<KPL, HV>(A, Rs, ch_t, alpha, gamma, gamz, alp, l_s, l_c, i0, nt, KPS, w,
                               lane, Ring + (size_t)w * A.NS * A.SLOT, yst);
         done = true;
       } else if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
