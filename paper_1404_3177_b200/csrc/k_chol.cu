@@ -284,6 +284,11 @@ __device__ __forceinline__ void tile_xyT(const double (*Xs)[LDS], const double (
 }
 
 // rows [j0+jb + 64*tile, +64): L21 = A21 Linv^T; with x: x_r -= L21_r . y_j
+// L1 caching of the operand tiles (cp.async.ca) is safe only across kernel launches: inside the
+// persistent factorisation (k_chol_persist) a line fetched for panel j may hold columns that panel
+// j's trailing update rewrites, so there (PERSIST) the tiles are staged through registers with
+// L2-only loads, all in flight together.
+template <bool PERSIST>
 __device__ __noinline__ void trsm_tile(int n, double* A, int lda, int j0, const double* Linv, double* x, int tile,
                                        double* dsm) {
   __syncthreads();  // smem reuse across consecutive tiles
@@ -293,15 +298,42 @@ __device__ __noinline__ void trsm_tile(int n, double* A, int lda, int j0, const 
   const int jb = min(NB, n - j0);
   const int r0 = j0 + jb + tile * NB;
   const int tid = threadIdx.x;
-  load_tile(Xs, A, lda, r0, j0, n - r0, jb);  // rows beyond n / columns beyond jb: zero
-  {
-    double v[16];
+  if constexpr (PERSIST) {  // one round trip through registers (L2 loads)
+    const int nr = n - r0;
+    double va[16], vl[16];
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = __ldcg(Linv + tid + 256 * m);
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      const bool ok = r < nr && c < jb;
+      va[m] = ok ? __ldcg(A + (int64_t)(r0 + r) * lda + j0 + c) : 0.0;
+      vl[m] = __ldcg(Linv + e);
+    }
 #pragma unroll
-    for (int m = 0; m < 16; ++m) Ys[(tid + 256 * m) >> 6][(tid + 256 * m) & 63] = v[m];
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      Xs[r][c] = va[m];
+      Ys[r][c] = vl[m];
+    }
+  } else {  // one round trip: the A21 tile (zero beyond n / jb) and Linv[j] straight into shared memory
+    const int nr = n - r0;
+#pragma unroll 4
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      const bool ok = r < nr && c < jb;
+      const double* g = A + (int64_t)(r0 + (ok ? r : 0)) * lda + j0 + (ok ? c : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]))),
+                   "l"(g), "r"(ok ? 8 : 0)
+                   : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(&Ys[r][c]))),
+                   "l"(Linv + e)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   if (x && tid < NB) yv[tid] = tid < jb ? __ldcg(x + j0 + tid) : 0.0;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   double acc[2][4][2];
   tile_xyT(Xs, Ys, acc);
@@ -331,11 +363,12 @@ __device__ __noinline__ void trsm_tile(int n, double* A, int lda, int j0, const 
 
 __global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, int j0, const double* Linv, double* x) {
   extern __shared__ __align__(16) double dsm[];
-  trsm_tile(n, A, lda, j0, Linv, x, blockIdx.x, dsm);
+  trsm_tile<false>(n, A, lda, j0, Linv, x, blockIdx.x, dsm);
 }
 
 // trailing update tile (ti, tj), ti >= tj, of A22 -= L21 L21^T (tile coordinates relative to the
 // first row/column after panel j0)
+template <bool PERSIST>
 __device__ __noinline__ void syrk_tile(int n, double* A, int lda, int j0, int ti, int tj, double* dsm) {
   __syncthreads();  // smem reuse across consecutive tiles
   double(*Li)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
@@ -344,13 +377,11 @@ __device__ __noinline__ void syrk_tile(int n, double* A, int lda, int j0, int ti
   const int s0 = j0 + jb;
   const int ri = s0 + ti * NB, rj = s0 + tj * NB;
   const int tid = threadIdx.x;
-  load_tile(Li, A, lda, ri, j0, n - ri, jb);
-  load_tile(Lj, A, lda, rj, j0, n - rj, jb);
-  __syncthreads();
-  double acc[2][4][2];
-  tile_xyT(Li, Lj, acc);
   const int lane = tid & 31, w = tid >> 5;
   const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
+  // one round trip: the two L21 tiles go to shared memory (cp.async, or through registers in the
+  // persistent kernel) while this thread's 16 entries of the C tile are loaded into registers
+  double cv[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -358,7 +389,54 @@ __device__ __noinline__ void syrk_tile(int n, double* A, int lda, int j0, int ti
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = ri + wr + a * 8 + lr, c = rj + wc + b * 8 + 2 * lk + h;
-        if (r < n && c < n && c <= r) A[(int64_t)r * lda + c] = __ldcg(A + (int64_t)r * lda + c) - acc[a][b][h];
+        cv[a][b][h] = (r < n && c < n && c <= r) ? __ldcg(A + (int64_t)r * lda + c) : 0.0;
+      }
+  if constexpr (PERSIST) {
+    const int nri = n - ri, nrj = n - rj;
+    double vi[16], vj[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      vi[m] = (r < nri && c < jb) ? __ldcg(A + (int64_t)(ri + r) * lda + j0 + c) : 0.0;
+      vj[m] = (r < nrj && c < jb) ? __ldcg(A + (int64_t)(rj + r) * lda + j0 + c) : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      Li[r][c] = vi[m];
+      Lj[r][c] = vj[m];
+    }
+  } else {
+    const int nri = n - ri, nrj = n - rj;
+#pragma unroll 4
+    for (int m = 0; m < 16; ++m) {
+      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
+      const bool oki = r < nri && c < jb, okj = r < nrj && c < jb;
+      const double* gi = A + (int64_t)(ri + (oki ? r : 0)) * lda + j0 + (oki ? c : 0);
+      const double* gj = A + (int64_t)(rj + (okj ? r : 0)) * lda + j0 + (okj ? c : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(&Li[r][c]))),
+                   "l"(gi), "r"(oki ? 8 : 0)
+                   : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(&Lj[r][c]))),
+                   "l"(gj), "r"(okj ? 8 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  double acc[2][4][2];
+  tile_xyT(Li, Lj, acc);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = ri + wr + a * 8 + lr, c = rj + wc + b * 8 + 2 * lk + h;
+        if (r < n && c < n && c <= r) A[(int64_t)r * lda + c] = cv[a][b][h] - acc[a][b][h];
       }
 }
 
@@ -383,7 +461,7 @@ __global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, i
     ti += first;
     tj += first;
   }
-  syrk_tile(n, A, lda, j0, ti, tj, dsm);
+  syrk_tile<false>(n, A, lda, j0, ti, tj, dsm);
 }
 
 // ---- triangular solve wavefront ------------------------------------------------------------
@@ -519,9 +597,9 @@ __global__ void __launch_bounds__(256, 1) k_chol_persist(int n, double* A, int l
   for (int j = 0; j + 1 < np; ++j) {
     const int j0 = j * NB, rem = n - j0 - NB, mt = (rem + NB - 1) / NB;
     const double* Lj = Linv + (size_t)j * NB * NB;
-    for (int t = b; t < mt; t += G) trsm_tile(n, A, lda, j0, Lj, x, t, dsm);          // (B)
+    for (int t = b; t < mt; t += G) trsm_tile<true>(n, A, lda, j0, Lj, x, t, dsm);    // (B)
     grid_barrier(bar, bar + 1, my_gen, G);
-    for (int t = b; t < mt; t += G) syrk_tile(n, A, lda, j0, t, 0, dsm);             // (C)
+    for (int t = b; t < mt; t += G) syrk_tile<true>(n, A, lda, j0, t, 0, dsm);       // (C)
     grid_barrier(bar, bar + 1, my_gen, G);
     if (b == 0) {                                                                    // (A)
       potrf_block(n, A, lda, j0 + NB, Linv + (size_t)(j + 1) * NB * NB, info, x, dsm);
@@ -530,7 +608,7 @@ __global__ void __launch_bounds__(256, 1) k_chol_persist(int n, double* A, int l
       for (int t = b - 1; t < nrest; t += G - 1) {
         int ti, tj;
         tri_tile(t, ti, tj);
-        syrk_tile(n, A, lda, j0, ti + 1, tj + 1, dsm);
+        syrk_tile<true>(n, A, lda, j0, ti + 1, tj + 1, dsm);
       }
     }
     grid_barrier(bar, bar + 1, my_gen, G);
