@@ -15,6 +15,7 @@
 // The matrix is row-major with leading dimension lda; only the lower triangle is referenced.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.h"
@@ -722,9 +723,11 @@ int persist_grid() {
 cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
   set_attrs();
   if (!ensure_work(n)) return cudaErrorMemoryAllocation;
-  // persistent single launch while the panel chain dominates; above ~3000 the trailing updates
-  // dominate and the multi-kernel path (3 CTAs per SM for them) is faster (measured crossover)
-  if (n <= 2816 && persist_grid() > 1) return factor_persist(n, A, lda, info, x, st);
+  // persistent single launch: since the tiles fetch their operands in one round trip it is faster
+  // than the two-stream multi-kernel path at every measured n (2816: 1.92 vs 2.36 ms; 5049: 5.35 vs
+  // 5.58 ms); MNL_CHOL_STREAMS=1 forces the multi-kernel path, MNL_CHOL_PERSIST_MAX caps n
+  static const int persist_max = getenv("MNL_CHOL_PERSIST_MAX") ? atoi(getenv("MNL_CHOL_PERSIST_MAX")) : 16384;
+  if (n <= persist_max && persist_grid() > 1) return factor_persist(n, A, lda, info, x, st);
   if (!g_la.side) {
     int lo = 0, hi = 0;  // the panel chain is the critical path: give it the highest priority
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
