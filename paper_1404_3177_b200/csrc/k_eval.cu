@@ -795,15 +795,14 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
   }
 #pragma unroll
   for (int c0 = 0; c0 < YZS_D; c0 += 4) {
-    if (c0 < d) {
+    if (c0 + 4 <= d) {  // a whole chunk of 4 components: all loads first
       double z[4][NI][KPL];
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
         for (int j = 0; j < NI; ++j)
 #pragma unroll
-          for (int kk = 0; kk < KPL; ++kk)
-            z[t][j][kk] = (kok[kk] && c0 + t < d) ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
+          for (int kk = 0; kk < KPL; ++kk) z[t][j][kk] = kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -813,6 +812,19 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
           for (int j = 0; j < NI; ++j) a = fma(z[t][j][kk], r[j][kk], a);
           alp[kk][c0 + t] = a;
         }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (c0 + t < d) {
+#pragma unroll
+          for (int kk = 0; kk < KPL; ++kk) {
+            double a = alp[kk][c0 + t];
+#pragma unroll
+            for (int j = 0; j < NI; ++j) a = fma(kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0, r[j][kk], a);
+            alp[kk][c0 + t] = a;
+          }
+        }
+      }
     }
   }
 }
