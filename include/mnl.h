@@ -37,7 +37,9 @@
  * Calls are serialised internally (one scratch cache per process).
  *
  * SIZE LIMITS OF THIS BUILD (MNL_ERR_ARG beyond them): 2 <= K <= 256, 0 <= p <= 255,
- * 0 <= d <= 16, 0 <= f <= 64, 1 <= N < 2^31, n_p <= 16384.
+ * 0 <= d <= 16, 0 <= f <= 64, 1 <= N < 2^31, n_p <= 16384, and the pass-1 kernel's per-CTA shared
+ * memory (<= 227 KB; it grows with ceil(K/32) * (p + d) and f — e.g. K > 128 allows d <= 4).
+ * mnl_check_shape() tells whether a shape is supported without touching a device.
  */
 #ifndef MNL_H_
 #define MNL_H_
@@ -62,6 +64,10 @@ typedef enum {
 
 /* n_p = (K-1)(p+1) + K*d + f, or -1 for K < 2 or negative sizes. */
 int64_t mnl_num_params(int32_t K, int32_t p, int32_t f, int32_t d);
+
+/* MNL_OK if every entry point supports the shape (N, K, p, f, d) in this build, else MNL_ERR_ARG
+ * (the size limits above, including the pass-1 shared-memory bound). No device is needed. */
+int mnl_check_shape(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d);
 
 /* One evaluation at `coef`: log-likelihood, gradient and, when
  * `hess` != NULL, the full Hessian.

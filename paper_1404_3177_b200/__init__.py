@@ -24,7 +24,7 @@ EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
             "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec",
             "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms", "mnl_eval_async", "mnl_sym_pack",
-            "mnl_sym_unpack")
+            "mnl_sym_unpack", "mnl_check_shape")
 
 MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
 MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
@@ -87,6 +87,8 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_opts.restype = ctypes.c_int
     lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_hessvec.restype = ctypes.c_int
+    lib.mnl_check_shape.argtypes = [I64, I32, I32, I32, I32]
+    lib.mnl_check_shape.restype = ctypes.c_int
     lib.mnl_sym_pack.argtypes = [I32, V, V, V]
     lib.mnl_sym_pack.restype = ctypes.c_int
     lib.mnl_sym_unpack.argtypes = [I32, V, V, V]
@@ -122,6 +124,11 @@ def load(build_if_missing: bool = False):
 
 def status_string(code: int) -> str:
     return load().mnl_status_string(code).decode()
+
+
+def shape_supported(N: int, K: int, p: int, f: int = 0, d: int = 0) -> bool:
+    """True if this build supports the shape (mnl_check_shape; no device needed)."""
+    return load().mnl_check_shape(N, K, p, f, d) == MNL_OK
 
 
 def num_params(K: int, p: int, f: int = 0, d: int = 0) -> int:

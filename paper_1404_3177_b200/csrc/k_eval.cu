@@ -968,6 +968,8 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
   };
 
   int buf = 0;
+  __syncthreads();  // the shared-memory initialisation (Xs ones / zeros, Bs, Cf) is complete before any
+                    // cp.async of the first tile can land in Xs
   if ((int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x, 0);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
     const int64_t i0 = tile * TI;

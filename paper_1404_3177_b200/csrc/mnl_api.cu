@@ -397,6 +397,13 @@ const char* mnl_status_string(int code) {
 
 int64_t mnl_last_launch_count(void) { return g_launches; }
 
+int mnl_check_shape(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d) {
+  Dims D;
+  if (!dims_of(N, K, p, f, d, &D)) return MNL_ERR_ARG;
+  EvalPlan ep;
+  return eval_plan(D, &ep, 148) ? MNL_OK : MNL_ERR_ARG;  // the pass-1 shared-memory bound
+}
+
 int mnl_last_eval_ms(double* ms) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!ms || !g_ws.ev_eval[0]) return MNL_ERR_ARG;

@@ -534,3 +534,45 @@ def test_recovery_of_true_coefficients(cfg):
     rms = float(np.sqrt(np.mean(z ** 2)))
     assert np.abs(z).max() < 5.5, np.abs(z).max()
     assert 0.9 <= rms <= 1.1, rms
+
+
+def _random_shapes(count=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        K = int(rng.choice([2, 3, 5, 8, 17, 31, 32, 33, 50, 64, 65, 100, 129, 256]))
+        p = int(rng.choice([0, 1, 2, 7, 16, 31, 50]))
+        f = int(rng.choice([0, 0, 1, 2, 4, 6, 10, 16]))
+        d = int(rng.choice([0, 0, 1, 2, 3, 5, 8]))
+        if p + f + d == 0:
+            p = 1
+        if (K - 1) * (p + 1) + K * d + f > 2500:  # keep the oracle's full Hessian quick
+            p = min(p, 7)
+        nmax = max(40, 60000 // (K * (1 + f + d) + p + 1))
+        N = int(rng.integers(1, min(nmax, 3000) + 1))
+        out.append((N, K, p, f, d))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes(), ids=lambda s: "x".join(map(str, s)))
+def test_eval_parity_random_shapes(shape):
+    """Seeded random shapes across the size limits (K up to 256, every pass-1 variant, ragged N):
+    loglik, gradient, Hessian and H v against the oracle."""
+    N, K, p, f, d = shape
+    prob = datagen.custom(N, K, p, f, d, seed=N + K, coef_sd=0.3, require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    th = datagen.perturbed_theta(prob, 0.2)
+    if not M.shape_supported(N, K, p, f, d):  # beyond the documented pass-1 shared-memory bound
+        with pytest.raises(M.MnlError) as ei:
+            M.mnl_eval(dp, dev(th), grad=True, hess=False)
+        assert ei.value.code == M.MNL_ERR_ARG
+        return
+    l_o, g_o, H_o = O.mnl_eval(D, th)
+    l, g, H = gpu_eval(dp, th)
+    check_lg(l, g, l_o, g_o)
+    assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+    assert np.array_equal(H, H.T)
+    v = np.random.default_rng(N).standard_normal(D.n_p)
+    hv = M.mnl_hessvec(dp, dev(th), dev(v)).cpu().numpy()
+    assert np.linalg.norm(hv - H_o @ v) <= 1e-10 * np.linalg.norm(H_o @ v)
