@@ -536,7 +536,7 @@ def test_recovery_of_true_coefficients(cfg):
     assert 0.9 <= rms <= 1.1, rms
 
 
-def _random_shapes(count=24, seed=2024):
+def _random_shapes(count=40, seed=2024):
     rng = np.random.default_rng(seed)
     out = []
     for _ in range(count):
@@ -576,3 +576,35 @@ def test_eval_parity_random_shapes(shape):
     v = np.random.default_rng(N).standard_normal(D.n_p)
     hv = M.mnl_hessvec(dp, dev(th), dev(v)).cpu().numpy()
     assert np.linalg.norm(hv - H_o @ v) <= 1e-10 * np.linalg.norm(H_o @ v)
+
+
+def _random_fit_shapes(count=10, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        K = int(rng.choice([2, 3, 4, 6, 9, 13, 33]))
+        p = int(rng.choice([0, 1, 3, 5, 9]))
+        f = int(rng.choice([0, 1, 2, 4]))
+        d = int(rng.choice([0, 1, 2, 3]))
+        n_p = (K - 1) * (p + 1) + K * d + f
+        if n_p > 400:
+            continue
+        N = int(rng.integers(30 * K + 10 * n_p, 30 * K + 10 * n_p + 800))
+        out.append((N, K, p, f, d))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_fit_shapes(), ids=lambda s: "x".join(map(str, s)))
+def test_fit_parity_random_shapes(shape):
+    """Seeded random shapes (ragged Cholesky blocks, every pass-1 variant): the GPU Newton fit takes
+    the oracle's iterations and halvings and reaches its coefficients (1e-8)."""
+    N, K, p, f, d = shape
+    prob = datagen.custom(N, K, p, f, d, seed=N, coef_sd=0.4)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    ref = O.newton_fit(D, tol=1e-6)
+    fit = M.mnl_newton_fit(dp, tol=1e-6)
+    assert fit.status == ref.status == M.MNL_OK
+    assert fit.iters == ref.iters
+    assert fit.stats["halvings_per_iter"][:fit.iters] == [h["halvings"] for h in ref.history]
+    assert np.linalg.norm(fit.coef.cpu().numpy() - ref.coef) <= 1e-8 * np.linalg.norm(ref.coef)
