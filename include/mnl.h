@@ -37,8 +37,9 @@
  * Calls are serialised internally (one scratch cache per process).
  *
  * SIZE LIMITS OF THIS BUILD (MNL_ERR_ARG beyond them): 2 <= K <= 256, 0 <= p <= 255,
- * 0 <= d <= 16, 0 <= f <= 64, 1 <= N < 2^31, n_p <= 16384, and the pass-1 kernel's per-CTA shared
- * memory (<= 227 KB; it grows with ceil(K/32) * (p + d) and f — e.g. K > 128 allows d <= 4).
+ * 0 <= d <= 64, 0 <= f <= 64, 1 <= N < 2^31, n_p <= 16384, and the pass-1 kernel's per-CTA shared
+ * memory (<= 227 KB; it grows with ceil(K/32) * p; the gradient partials of many alternative-
+ * varying variables move to global scratch).
  * mnl_check_shape() tells whether a shape is supported without touching a device.
  */
 #ifndef MNL_H_

@@ -60,7 +60,13 @@ struct GemmParams {
   int nraw;  // raw stages: 2 (prefetch two chunks ahead) or 1 (refill after the generate phase)
   const double* bfrag;  // BPRE: B operand precomputed in fragment-native order [tilesN][nchunks][GB_D]
   unsigned* counter;
+  // >= 0: skip the tiles whose every row r exceeds skip_off + every column c (J2: the lower
+  // triangle of the symmetric Z/Y x Z/Y block, never read by the assembly, which takes (min, max))
+  int skip_off;
 };
+__host__ __device__ __forceinline__ bool skip_tile(int skip_off, int tm, int tn, int bn) {
+  return skip_off >= 0 && (int64_t)tm * 128 > (int64_t)skip_off + (int64_t)tn * bn + bn - 1;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -188,6 +194,10 @@ __global__ void __launch_bounds__(NWARP * 32, (NWARP < 8 ? 8 / NWARP : 1)) k_gen
     if (item >= total) break;
     const int split = item / tiles, t = item - split * tiles;
     const int tm = t / P.tilesN, tn = t - tm * P.tilesN;
+    if (skip_tile(P.skip_off, tm, tn, BN)) {
+      __syncthreads();  // every thread has read s_item before thread 0 fetches the next item
+      continue;
+    }
     const int64_t c_begin = split * P.nchunks / P.splits;
     const int64_t c_end = (split + 1) * P.nchunks / P.splits;
 
@@ -447,6 +457,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P
       }
       const int split = item / tiles, t = item - split * tiles;
       const int tm = t / P.tilesN, tn = t - tm * P.tilesN;
+      if (skip_tile(P.skip_off, tm, tn, BN)) continue;  // never staged: the consumers never see it
       const int64_t cb = split * P.nchunks / P.splits, ce = (split + 1) * P.nchunks / P.splits;
       for (int64_t c = cb; c < ce; ++c) {
         mbar_wait(&empty[s], ph ^ 1u);
@@ -761,6 +772,7 @@ struct GemmJob {
   int dnseg = 0, dseg_id[3] = {0, 0, 0};  // stage layout the descriptors were built against
   bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
+  int skip_off = -1;  // GemmParams::skip_off
   int64_t nchunks;
   ColDesc* dA = nullptr;  // device
   ColDesc* dB = nullptr;
@@ -790,6 +802,15 @@ struct HessPlan {
 };
 
 constexpr size_t kFragSmemMax = 220 * 1024;  // k_frag's staged rows
+// k_frag stages KC / nh rows per CTA (nh | KC / 4): the smallest nh keeping the stage <= 48 KB
+// (occupancy), else the smallest that fits at all; 0 if none does
+static int frag_nh(size_t stage_doubles) {
+  for (int nh = 1; nh <= 8; nh *= 2)
+    if (stage_doubles * sizeof(double) / nh <= 48 * 1024) return nh;
+  for (int nh = 1; nh <= 8; nh *= 2)
+    if (stage_doubles * sizeof(double) / nh <= kFragSmemMax) return nh;
+  return 0;
+}
 
 static int choose_splits(int tiles, int64_t nchunks, int sms, int min_chunks) {
   int best = 1;
@@ -935,7 +956,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       const bool split = nv > 128 && rem > 0 && rem <= 96;
       hp->n1a = split ? nv - rem : nv;
       std::vector<ColDesc> Ba(B.begin(), B.begin() + hp->n1a), Bb(B.begin() + hp->n1a, B.end());
-      const bool frag_fits = (size_t)KC * (pk.ldP + pk.ldX) * sizeof(double) <= kFragSmemMax;
+      const bool frag_fits = frag_nh((size_t)KC * (pk.ldP + pk.ldX)) > 0;
       // Materialise both operands (k_pipe_gemm) when the per-evaluation write of the weights
       // (8 N 128 tilesM bytes) is small next to the GEMM (~23/vech of it at the measured rates):
       // vech >= 256. Otherwise materialise only the design-only B (once per design) if it fits.
@@ -1003,7 +1024,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       // (8 N (MA + MB) bytes) is small next to the GEMM (23 (1/MA + 1/MB) of it): MB >= 192, MA >= 512
       GemmJob& J = hp->j2;
       const int MA = (int)A.size(), MB = (int)B.size();
-      const bool frag_fits = (size_t)KC * (pk.ldP + pk.ldX + (d > 0 ? pk.ldZ : 0)) * sizeof(double) <= kFragSmemMax;
+      const bool frag_fits = frag_nh((size_t)KC * (pk.ldP + pk.ldX + (d > 0 ? pk.ldZ : 0))) > 0;
       int bn2 = choose_bn(MB);
       if (KC == 32 && MB >= 192 && MA >= 512 && frag_fits && !getenv("MNL_NO_PIPE")) {
         const int bnp = choose_bn_pipe(MB);
@@ -1020,6 +1041,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       J.b_design = false;
       J.dnseg = nseg;
       for (int sg = 0; sg < 3; ++sg) J.dseg_id[sg] = segs[sg];
+      J.skip_off = (K - 1) * q;  // n_beta: C2 rows are theta indices, columns start at n_beta
       if (setup_job(J, A, B, bn2, KC, pk, segs, nseg, sms, &bytes, J.mat_a)) break;
       free_job(hp->j2);
       if (KC == 16) ok = false;
@@ -1097,6 +1119,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.nraw = J.nraw;
   P.bfrag = J.bfrag;
   P.counter = counter;
+  P.skip_off = J.skip_off;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP, AGEN, BPRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1126,6 +1149,7 @@ static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaSt
   P.split_stride = J.split_stride;
   P.bfrag = J.bfrag;
   P.counter = counter;
+  P.skip_off = J.skip_off;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_pipe_gemm<BN, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1192,7 +1216,7 @@ static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStr
     cudaFuncSetAttribute(k_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFragSmemMax);
     attr = true;
   }
-  F.nh = (size_t)off * sizeof(double) > 48 * 1024 ? 2 : 1;
+  F.nh = frag_nh((size_t)off);  // > 0: the plan materialises only operands whose stage fits
   k_frag<<<(unsigned)(F.nh * J.nchunks), 256, (size_t)off / F.nh * sizeof(double), st>>>(F);
   count_launch();
 }

@@ -73,7 +73,7 @@ const char* kStatus[] = {"MNL_OK", "MNL_ERR_ARG", "MNL_ERR_CUDA", "MNL_ERR_NOT_S
 
 bool dims_of(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, Dims* D) {
   if (N < 1 || N >= (int64_t(1) << 31) || K < 2 || K > 256 || p < 0 || p > 255 || f < 0 || f > 64 || d < 0 ||
-      d > 16)
+      d > 64)
     return false;
   D->N = N; D->K = K; D->p = p; D->f = f; D->d = d;
   D->q = p + 1;
@@ -134,7 +134,7 @@ HessPlan* get_hess_plan(Workspace& W, const Dims& D, const Packed& pk) {
 int run_eval(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X, const double* Y, const double* Z,
              const int32_t* choice, const double* coef, const Packed* pk, bool writeP, double* grad,
              double* loglik_dev, double* scal_h, cudaStream_t st) {
-  if (!grow(&W.part, &W.cpart, (size_t)ep.grid * ep.n_part)) return MNL_ERR_CUDA;
+  if (!grow(&W.part, &W.cpart, eval_part_doubles(ep))) return MNL_ERR_CUDA;
   cudaMemsetAsync(W.err, 0, sizeof(int), st);
   if (!W.ev_eval[0]) {
     cudaEventCreate(&W.ev_eval[0]);
@@ -156,7 +156,7 @@ int run_eval(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X, c
 // H v at the coefficients of the last evaluation with writeP (P_i in pk->Pr); hv dev [n_p].
 int run_hessvec(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X, const double* Y, const double* Z,
                 const int32_t* choice, const double* v, const Packed* pk, double* hv, cudaStream_t st) {
-  if (!grow(&W.part, &W.cpart, (size_t)ep.grid * ep.n_part)) return MNL_ERR_CUDA;
+  if (!grow(&W.part, &W.cpart, eval_part_doubles(ep))) return MNL_ERR_CUDA;
   cudaError_t e = launch_hessvec(D, ep, X, Y, Z, choice, v, pk, W.part, W.err, st);
   if (e != cudaSuccess) return MNL_ERR_CUDA;
   e = launch_eval_finalize(D, ep, W.part, true, hv, nullptr, W.scal, W.err, W.counter, st);
@@ -494,7 +494,7 @@ int mnl_eval_async(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d, const 
     if (launch_pack(D, pk, X, Z, st) != cudaSuccess) return MNL_ERR_CUDA;
     if (W.hp) hess_plan_design_changed(W.hp);
   }
-  if (!grow(&W.part, &W.cpart, (size_t)ep.grid * ep.n_part)) return MNL_ERR_CUDA;
+  if (!grow(&W.part, &W.cpart, eval_part_doubles(ep))) return MNL_ERR_CUDA;
   HessPlan* hp = want_h ? get_hess_plan(W, D, pk) : nullptr;  // (first use of a shape allocates)
   if (want_h && !hp) return MNL_ERR_CUDA;
   cudaMemsetAsync(W.err, 0, sizeof(int), st);

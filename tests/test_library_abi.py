@@ -83,11 +83,13 @@ def test_argument_errors_are_reported_without_a_device(lib):
     assert lib.mnl_eval_async(10, 4, 2, 0, 0, fake, None, None, fake, fake, fake, None, None, None,
                               None) == M.MNL_ERR_ARG  # status pointer required
     assert lib.mnl_sym_pack(0, fake, fake, None) == M.MNL_ERR_ARG
-    # shape queries: the BASELINE configs are supported; K > 128 with d = 8 exceeds the pass-1 bound
+    # shape queries: the BASELINE configs are supported; p = 255 with K = 256 exceeds the pass-1 bound
     for N, K, p, f, d in [(1000, 4, 3, 2, 1), (20000, 10, 20, 0, 0), (100000, 20, 50, 0, 0),
                           (500000, 100, 50, 0, 0), (200000, 50, 30, 10, 5)]:
         assert lib.mnl_check_shape(N, K, p, f, d) == M.MNL_OK
-    assert lib.mnl_check_shape(15, 129, 7, 4, 8) == M.MNL_ERR_ARG
+    assert lib.mnl_check_shape(15, 129, 7, 4, 8) == M.MNL_OK      # gradient partials in global scratch
+    assert lib.mnl_check_shape(10, 256, 255, 0, 0) == M.MNL_ERR_ARG  # beta block beyond shared memory
+    assert lib.mnl_check_shape(10, 4, 2, 0, 65) == M.MNL_ERR_ARG
     assert lib.mnl_check_shape(10, 1, 2, 0, 0) == M.MNL_ERR_ARG
     assert lib.mnl_sym_unpack(5, None, fake, None) == M.MNL_ERR_ARG
     opts = M.FitOptions(0.0, 0.0, 5, 0, 0, 0.0)  # gtol <= 0
