@@ -36,11 +36,11 @@
  * stream), synchronises that stream before returning, and returns a final status code.
  * Calls are serialised internally (one scratch cache per process).
  *
- * SIZE LIMITS OF THIS BUILD (MNL_ERR_ARG beyond them): 2 <= K <= 256, 0 <= p <= 255,
- * 0 <= d <= 64, 0 <= f <= 64, 1 <= N < 2^31, n_p <= 16384, and the pass-1 kernel's per-CTA shared
- * memory (<= 227 KB; it grows with ceil(K/32) * p; the gradient partials of many alternative-
- * varying variables move to global scratch).
- * mnl_check_shape() tells whether a shape is supported without touching a device.
+ * SIZE LIMITS OF THIS BUILD (MNL_ERR_ARG beyond them): 2 <= K <= 256, 0 <= d <= 64, 0 <= f <= 64,
+ * 1 <= N < 2^31, n_p <= 16384, and p bounded by the pass-1 kernel's register-resident beta-gradient
+ * accumulators: p + 1 <= 128 for K <= 32, <= 64 for K <= 128, <= 32 for K <= 256; plus its per-CTA
+ * shared memory (<= 227 KB; the gradient partials of many alternative-varying variables move to
+ * global scratch). mnl_check_shape() tells whether a shape is supported without touching a device.
  */
 #ifndef MNL_H_
 #define MNL_H_

@@ -48,6 +48,7 @@ void count_launch(int n = 1);
 struct EvalPlan {
   int grid, block, kpl, cm;
   int yzs, ns;  // alternative-varying rows staged per warp (bulk copies into an ns-slot ring)
+  int ti;       // individuals per tile
   int64_t wa;   // > 0: the alpha/gamma gradient partials live in global scratch (wa doubles per CTA,
                 // after the grid x n_part partials) because they do not fit in shared memory
   size_t smem;

@@ -1140,7 +1140,10 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     if (lane < yst.lg_cnt) neu_add(l_s, l_c, yst.lg_a - log(yst.lg_s));  // the deferred logs left over
   __syncthreads();
   double* out = A.part + (size_t)blockIdx.x * A.n_part;
-  double* scratch = YZS ? Ring : Rs;  // reuse (YZS: the drained rings; Rs may be smaller than 2 NWK 32)
+  // finalisation scratch: the dead Bs .. Ps regions when they hold [NWK 32][8] doubles (they do
+  // whenever the tile was shrunk for a large p), else Rs and what follows it; YZS: the drained rings
+  double* fin = (Wa_s - sm >= NWK * 32 * 8) ? sm : Rs;
+  double* scratch = YZS ? Ring : fin;
   // loglik: lanes with r4 == 0 hold rows; combine in (warp, lane) order
   scratch[2 * tid] = l_s;
   scratch[2 * tid + 1] = l_c;
@@ -1202,7 +1205,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     if (e < f) Wa[NWK * KPL * d * 32 + (w * f + e) * 32 + lane] += gam[e];
   __syncthreads();
   // gamma partials: registers (e < 8) -> smem, then fixed-order sums
-  double* gsc = Rs;  // [NWK*32][8]
+  double* gsc = fin;  // [NWK*32][8]
   for (int e = 0; e < 8; ++e) gsc[tid * 8 + e] = gam[e];
   __syncthreads();
   for (int idx = tid; idx < K * d; idx += blockDim.x) {
@@ -1387,8 +1390,8 @@ __global__ void __launch_bounds__(1024) k_cg_dir(int n, double beta, const doubl
 static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
-static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns, bool wa_global = false) {
-  const int KP = 32 * kpl, KPS = KP + 4, TI = yzs ? YZS_TI : tile_rows(kpl, (D.d + D.f) > 0);
+static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns, bool wa_global = false, int ti = 0) {
+  const int KP = 32 * kpl, KPS = KP + 4, TI = yzs ? YZS_TI : (ti ? ti : tile_rows(kpl, (D.d + D.f) > 0));
   const int slot = D.K * (D.f + D.d);
   const int nw = yzs ? NWY : NW;
   size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
@@ -1430,6 +1433,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
       }
     }
   }
+  plan->ti = plan->yzs ? YZS_TI : tile_rows(kpl, (D.d + D.f) > 0);
   if (smem > 227 * 1024 && !plan->yzs && (D.d + D.f) > 0) {
     // many alternative-specific / generic variables: gradient partials to global scratch
     smem = eval_smem(D, kpl, false, 0, true);
@@ -1447,7 +1451,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   plan->kpl = kpl;
   plan->smem = smem;
   plan->block = nwarps * 32;
-  const int ti = plan->yzs ? YZS_TI : tile_rows(kpl, (D.d + D.f) > 0);
+  const int ti = plan->ti;
   const int64_t ntiles = (D.N + ti - 1) / ti;
   int64_t grid = sms;
   if (grid > ntiles) grid = ntiles;
@@ -1463,7 +1467,7 @@ static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const d
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = eval_qp(D); a.XS = eval_xs(D);
-  a.TI = plan.yzs ? YZS_TI : tile_rows(plan.kpl, (D.d + D.f) > 0); a.SCR = 0;
+  a.TI = plan.ti; a.SCR = 0;
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
   a.Pr = (writeP || hv) ? pk->Pr : nullptr;
   a.ldP = (writeP || hv) ? pk->ldP : 0;

@@ -93,6 +93,8 @@ SHAPES = [  # ragged N (not a multiple of the 32/64-row tiles), K at KPL boundar
     (77, 9, 3, 4, 2), (45, 31, 0, 6, 0), (500, 50, 2, 16, 8), (129, 64, 1, 2, 1),
     # many alternative-specific / generic variables (gradient partials in global scratch, d > 16)
     (300, 20, 3, 0, 40), (100, 30, 0, 0, 30), (150, 8, 2, 64, 64), (15, 129, 7, 4, 8),
+    # p at its bound for K <= 32 (p + 1 = 128: 16 accumulator blocks per warp)
+    (60, 32, 127, 0, 0),
 ]
 
 

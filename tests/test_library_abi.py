@@ -88,7 +88,9 @@ def test_argument_errors_are_reported_without_a_device(lib):
                           (500000, 100, 50, 0, 0), (200000, 50, 30, 10, 5)]:
         assert lib.mnl_check_shape(N, K, p, f, d) == M.MNL_OK
     assert lib.mnl_check_shape(15, 129, 7, 4, 8) == M.MNL_OK      # gradient partials in global scratch
-    assert lib.mnl_check_shape(10, 256, 255, 0, 0) == M.MNL_ERR_ARG  # beta block beyond shared memory
+    assert lib.mnl_check_shape(10, 256, 255, 0, 0) == M.MNL_ERR_ARG  # beyond the p bound for K > 128
+    assert lib.mnl_check_shape(10, 256, 31, 0, 0) == M.MNL_OK
+    assert lib.mnl_check_shape(10, 32, 127, 0, 0) == M.MNL_OK and lib.mnl_check_shape(10, 32, 128, 0, 0) == M.MNL_ERR_ARG
     assert lib.mnl_check_shape(10, 4, 2, 0, 65) == M.MNL_ERR_ARG
     assert lib.mnl_check_shape(10, 1, 2, 0, 0) == M.MNL_ERR_ARG
     assert lib.mnl_sym_unpack(5, None, fake, None) == M.MNL_ERR_ARG
