@@ -422,9 +422,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // stage (written before the producer's release-arrive, read after the consumers' acquire-wait).
 template <int BN, int KC, int S>
 __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P, const double* __restrict__ afrag) {
-  // 128 -> 2x4 warps of 64x32; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32; 48 -> 8x1 of 16x48
+  // 128 -> 2x4 warps of 64x32; 112 -> 8x1 of 16x112; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32; 48 -> 8x1 of 16x48
   constexpr int NWARP = 8;
-  constexpr int WARPS_M = (BN == 128) ? 2 : (BN == 48 ? 8 : 4), WARPS_N = NWARP / WARPS_M;
+  constexpr int WARPS_M = (BN == 128) ? 2 : ((BN == 48 || BN == 112) ? 8 : 4), WARPS_N = NWARP / WARPS_M;
   constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   constexpr int MT = WTM / 8, NTL = WTN / 8;
   constexpr int KS = KC / 4, PBA = BM / 16, PBB = BN / 16;
@@ -922,11 +922,11 @@ static double* alloc_frag(int tiles, int width, const Packed& pk, size_t* bytes)
 // smallest padded width.
 static int choose_bn_pipe(int MB) {
   int64_t min_pad = -1;
-  for (int bn : {128, 96, 64, 48}) {
+  for (int bn : {128, 112, 96, 64, 48}) {
     const int64_t pad = (int64_t)(MB + bn - 1) / bn * bn;
     if (min_pad < 0 || pad < min_pad) min_pad = pad;
   }
-  for (int bn : {128, 96, 64, 48})
+  for (int bn : {128, 112, 96, 64, 48})
     if ((double)((MB + bn - 1) / bn * bn) <= 1.05 * (double)min_pad) return bn;
   return 48;
 }
@@ -951,9 +951,9 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
         for (int b = a; b < q; ++b) B.push_back(ColDesc{offX + a, pk.ldX, offX + b, pk.ldX, 0.0, 1.0});
       // padding columns point at Xp[.][0] (finite) with c0 = s = 0
       // Split the vech columns: whole 128-column tiles in j1, a narrow remainder job j1b (its own
-      // width) instead of padding the last tile (c4: 1326 = 10 x 128 + 46).
+      // width) instead of padding the last tile (c4: 1326 = 10 x 128 + 46; c5: 496 = 3 x 128 + 112).
       const int nv = (int)B.size(), rem = nv % 128;
-      const bool split = nv > 128 && rem > 0 && rem <= 96;
+      const bool split = nv > 128 && rem > 0 && rem <= 112;
       hp->n1a = split ? nv - rem : nv;
       std::vector<ColDesc> Ba(B.begin(), B.begin() + hp->n1a), Bb(B.begin() + hp->n1a, B.end());
       const bool frag_fits = frag_nh((size_t)KC * (pk.ldP + pk.ldX)) > 0;
@@ -1169,6 +1169,7 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
   if (J.mat_a) {
     if (J.BN == 128) e = run_pipe<128>(J, counter, sms, st);
     else if (J.BN == 96) e = run_pipe<96>(J, counter, sms, st);
+    else if (J.BN == 112) e = run_pipe<112>(J, counter, sms, st);
     else if (J.BN == 64) e = run_pipe<64>(J, counter, sms, st);
     else e = run_pipe<48>(J, counter, sms, st);
   } else if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)

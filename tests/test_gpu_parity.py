@@ -138,8 +138,9 @@ def test_eval_yz_paths(mode):
 
 
 # Shapes that select each GEMM kernel: J2 materialised (K d + f >= 192) with a generated J1;
-# J1 split into 128-wide tiles + a 48-wide tail (vech 1326 = 10 x 128 + 46); vech 300 = 256 + 44.
-PATH_SHAPES = [(3000, 40, 10, 4, 5), (2500, 12, 50, 0, 0), (1500, 25, 24, 2, 2)]
+# J1 split into 128-wide tiles + a 48-wide tail (vech 1326 = 10 x 128 + 46); vech 300 = 256 + 44;
+# vech 496 = 3 x 128 + a 112-wide tail.
+PATH_SHAPES = [(3000, 40, 10, 4, 5), (2500, 12, 50, 0, 0), (1500, 25, 24, 2, 2), (2000, 10, 30, 0, 0)]
 
 
 @pytest.mark.parametrize("mode", ["default", "MNL_NO_PIPE", "MNL_NO_MATERIALISE"])
