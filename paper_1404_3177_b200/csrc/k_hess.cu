@@ -352,7 +352,11 @@ struct FragArgs {
   const double* seg_ptr[3];
   int seg_ld[3];
   int seg_off[3];
-  int nh;  // CTAs per chunk (1, or 2 when the chunk's rows need > 48 KB of shared memory)
+  int nh;  // CTAs per chunk (frag_nh: KC / nh staged rows)
+  // optional second operand from the same staged rows (J2: A and B in one pass); tiles2 = 0: none
+  const ColDesc* desc2;
+  double* out2;
+  int tiles2, BT2;
 };
 
 // offset into a KC-row stage -> offset into the KC/2-row stage (segment bases halve; the in-row
@@ -384,15 +388,20 @@ __global__ void __launch_bounds__(256) k_frag(const FragArgs F) {
   // one thread per (tile, pair-block, lane): its two columns' descriptors stay in registers over
   // the k-slices; for each k-slice a warp stores 512 contiguous bytes. Descriptor offsets assume
   // KC staged rows per segment (seg_off = KC * preceding lds): rebase to the half-size stage.
-  const int PB = F.BT / 16, KS = F.KC / 4, W = PB * 32;
-  for (int w = threadIdx.x; w < F.tiles * W; w += blockDim.x) {
+  const int KS = F.KC / 4;
+  const int W1 = (F.BT / 16) * 32, W2 = (F.BT2 / 16) * 32, n1 = F.tiles * W1;
+  for (int wi = threadIdx.x; wi < n1 + F.tiles2 * W2; wi += blockDim.x) {
+    const bool second = wi >= n1;  // CTA-uniform ranges; the branch only picks the operand
+    const int w = second ? wi - n1 : wi, W = second ? W2 : W1, BT = second ? F.BT2 : F.BT;
+    const ColDesc* desc = second ? F.desc2 : F.desc;
+    double* outp = second ? F.out2 : F.out;
     const int t = w / W, r = w - t * W, lane = r & 31;
-    const int col = t * F.BT + (r >> 5) * 16 + (lane >> 2);
-    ColDesc d0 = F.desc[col], d1 = F.desc[col + 8];
+    const int col = t * BT + (r >> 5) * 16 + (lane >> 2);
+    ColDesc d0 = desc[col], d1 = desc[col + 8];
     d0.o1 = rebase(F, d0.o1); d0.o2 = rebase(F, d0.o2);
     d1.o1 = rebase(F, d1.o1); d1.o2 = rebase(F, d1.o2);
     const int i0 = lane & 3;
-    double2* dst = reinterpret_cast<double2*>(F.out + ((int64_t)t * F.nchunks + c) * (KS * W * 2)) + r;
+    double2* dst = reinterpret_cast<double2*>(outp + ((int64_t)t * F.nchunks + c) * (KS * W * 2)) + r;
 #pragma unroll 4
     for (int kq = 0; kq < KS / F.nh; ++kq) {
       const int i = 4 * kq + i0, ks = h * (KS / F.nh) + kq;
@@ -1195,8 +1204,19 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
   return cudaGetLastError();
 }
 
-static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStream_t st) {
+static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStream_t st, bool both = false) {
   FragArgs F;
+  F.desc2 = nullptr;
+  F.out2 = nullptr;
+  F.tiles2 = 0;
+  F.BT2 = 16;
+  if (both) {  // A (a_side ignored) and B of the same job from one staging of the rows
+    a_side = true;
+    F.desc2 = J.dB;
+    F.out2 = J.bfrag;
+    F.tiles2 = J.tilesN;
+    F.BT2 = J.BN;
+  }
   F.desc = a_side ? J.dA : J.dB;
   F.out = a_side ? J.afrag : J.bfrag;
   F.tiles = a_side ? J.tilesM : J.tilesN;
@@ -1229,6 +1249,10 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
     const GemmJob* jobs[3] = {&hp->j1, hp->has_j1b ? &hp->j1b : nullptr, hp->has_j2 ? &hp->j2 : nullptr};
     for (const GemmJob* J : jobs) {
       if (!J) continue;
+      if (J->mat_a && J->mat_b && J->own_afrag && !J->b_design) {  // J2: both per evaluation, one pass
+        launch_frag(*J, pk, true, st, true);
+        continue;
+      }
       if (J->mat_b && (!J->b_design || !hp->bvalid)) launch_frag(*J, pk, false, st);
       if (J->mat_a && J->own_afrag) launch_frag(*J, pk, true, st);
     }
