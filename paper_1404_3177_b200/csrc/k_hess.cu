@@ -1068,8 +1068,22 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
     hp->ar_ci = 32;
     while (hp->ar_ci > 4 && (size_t)2 * hp->ar_ci * hp->ar_rs * sizeof(double) > (size_t)200 * 1024) hp->ar_ci /= 2;
     const int64_t nch = pk.Npad / hp->ar_ci;
+    // splits of the individuals: minimise the makespan waves(S) / S (the work per item ~ 1 / S) over
+    // the resident CTAs (registers allow 2 per SM; shared memory may allow fewer), keeping >= 8
+    // chunks per item; the smallest S reaching the minimum (fewest partials to reduce)
+    const size_t ar_smem = (size_t)2 * hp->ar_ci * hp->ar_rs * sizeof(double);
+    const int per_sm = std::max(1, std::min(2, (int)((size_t)(227 * 1024) / std::max<size_t>(ar_smem, 1))));
+    const int64_t slots = (int64_t)sms * per_sm;
     int S = 1;
-    while ((int64_t)base_items * S < 2 * sms && nch / (S * 2) >= 8) S *= 2;
+    double best = 1e30;
+    for (int s2 = 1; s2 <= 256 && nch / s2 >= 8; ++s2) {
+      const int64_t items = (int64_t)base_items * s2;
+      const double span = (double)((items + slots - 1) / slots) / s2;
+      if (span < best * (1.0 - 1e-9)) {
+        best = span;
+        S = s2;
+      }
+    }
     hp->ar_splits = S;
     const size_t tb = ((size_t)K * E * F + 1) / 2 * 2 * sizeof(double);
     if (cudaMalloc(&hp->Tpart, tb * S) != cudaSuccess) ok = false;
