@@ -18,11 +18,13 @@
 //        T_k = sum_i P_ik e_ik f_ik^T,  e = [x~_i, z_ik, y_ik], f = [z_ik, y_ik]
 //  so that  -H = C1 (beta-beta)  and  -H = T - C2 (every other entry).
 //
-// J1/J2 run one persistent, warp-level DMMA kernel (mma.sync.m8n8k4.f64 — tcgen05 has no f64
-// kind on sm_100a): 128 x BN output tiles, 8 warps, inner dimension = individuals in chunks of
-// KC; per chunk the raw rows are fetched by one cp.async.bulk (TMA bulk copy) per segment into
-// a double-buffered stage, every thread generates its fragment-native operand elements
-// (v = R[o1] * (c0 + s R[o2])) into double-buffered smem, and the warps issue DMMAs from it.
+// J1/J2 run warp-level DMMA kernels (mma.sync.m8n8k4.f64 — tcgen05 has no f64 kind on sm_100a)
+// over 128 x BN output tiles, inner dimension = individuals in chunks of KC. Default: both operands
+// are materialised per chunk in fragment-native order by k_frag (W every evaluation, the design
+// products once per design; J2's A and B in one pass) and k_pipe_gemm streams them with one
+// cp.async.bulk each into an mbarrier ring (1 producer warp, 8 consumer warps issuing DMMAs only).
+// Fallback (k_gen_gemm): the raw rows are fetched by cp.async.bulk into a stage and every thread
+// generates its fragment-native operand elements (v = R[o1] * (c0 + s R[o2])) on chip.
 // Split-N partial tiles are reduced in a fixed order (deterministic), then k_assemble gathers
 // H (exactly symmetric) into the caller's row-major n_p x n_p buffer.
 #include <algorithm>
@@ -927,7 +929,7 @@ static double* alloc_frag(int tiles, int width, const Packed& pk, size_t* bytes)
   return p;
 }
 
-// Tile widths k_pipe_gemm is instantiated for: the widest of {128, 96, 64, 48} within 5% of the
+// Tile widths k_pipe_gemm is instantiated for: the widest of {128, 112, 96, 64, 48} within 5% of the
 // smallest padded width.
 static int choose_bn_pipe(int MB) {
   int64_t min_pad = -1;
