@@ -48,6 +48,8 @@ void count_launch(int n = 1);
 struct EvalPlan {
   int grid, block, kpl, cm;
   int yzs, ns;  // alternative-varying rows staged per warp (bulk copies into an ns-slot ring)
+  int stream;   // alpha / gamma gradients by k_yz_grad from residual rows (rg doubles of scratch)
+  int64_t rg;
   int ti;       // individuals per tile
   int64_t wa;   // > 0: the alpha/gamma gradient partials live in global scratch (wa doubles per CTA,
                 // after the grid x n_part partials) because they do not fit in shared memory
@@ -56,7 +58,7 @@ struct EvalPlan {
 };
 bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
 // doubles of the `part` scratch a launch with this plan needs (partials + global gradient partials)
-inline size_t eval_part_doubles(const EvalPlan& ep) { return (size_t)ep.grid * (ep.n_part + ep.wa); }
+inline size_t eval_part_doubles(const EvalPlan& ep) { return (size_t)ep.grid * (ep.n_part + ep.wa) + ep.rg; }
 // Pass 1 (a1-a4): utilities, softmax, loglik partials, gradient partials (if want_grad),
 // and the probability rows Pr (if writeP). part: [grid][n_part].
 cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,

@@ -44,6 +44,8 @@ struct EvalArgs {
   int NS, SLOT;  // YZS path: ring slots per warp, doubles per slot (K (f + d))
   double* wa_g;  // non-null: alpha / gamma gradient partials in global scratch (per CTA)
   int64_t wa;    // doubles per CTA of wa_g
+  double* Rg;    // non-null (stream mode): residual rows r_i [N][K] for k_yz_grad, which then forms
+                 // the alpha / gamma gradients by streaming Z and Y (many alternative-varying vars)
   const double* X;
   const double* Y;  // [N][K][f]
   const double* Z;  // [N][K][d]
@@ -242,6 +244,11 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
         if (A.writeP && kok[kk]) A.Pr[gi * A.ldP + k] = P;
       }
     }
+    if (A.Rg)  // stream mode: the alpha / gamma gradients come from k_yz_grad
+#pragma unroll
+      for (int kk = 0; kk < KPL; ++kk)
+        if (kok[kk]) A.Rg[gi * K + lane + 32 * kk] = r[kk];
+    if (A.Rg && !A.writeP) continue;  // nothing left for this individual
     // ---- pass 2 (L1 hits): ybar_e = sum_k P_k y_ke, gamma and alpha gradients ----
     // 8 components per batch; the cross-lane ybar sums go through red[8][33] (lane 4e'+j adds 8 of
     // the 32 partials, then two shuffles). The first 16 gamma partials stay in registers.
@@ -286,19 +293,20 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
       if (8 * h < f) {
         double yb[8], gg[8];
         ybar_batch(8 * h, yb, gg);
+        if (!A.Rg)
 #pragma unroll
-        for (int t = 0; t < 8; ++t) gam[8 * h + t] += gg[t];  // components >= f add exact zeros
+          for (int t = 0; t < 8; ++t) gam[8 * h + t] += gg[t];  // components >= f add exact zeros
       }
     }
     for (int e0 = gam_regs<KPL>(); e0 < f; e0 += 8) {
       double yb[8], gg[8];
       ybar_batch(e0, yb, gg);
-      if (A.want_grad)
+      if (A.want_grad && !A.Rg)
 #pragma unroll
         for (int t = 0; t < 8; ++t)
           if (e0 + t < f) Wa[NW * KPL * d * 32 + (w * f + e0 + t) * 32 + lane] += gg[t];
     }
-    if (A.want_grad && d) {
+    if (A.want_grad && d && !A.Rg) {
       for (int c = 0; c < d; ++c)
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk)
@@ -869,7 +877,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
   // in global scratch (A.wa_g, L1/L2-resident read-modify-writes) when it does not fit here
   double* Wa_s = Rs + ((d + f) && !YZS ? 2 * TI * KPS : TI * KPS);
   double* Wa = A.wa_g ? A.wa_g + (size_t)blockIdx.x * A.wa : Wa_s;
-  double* Cf = Wa_s + (YZS || A.wa_g ? 0 : NWK * KPL * d * 32 + NWK * f * 32);  // [K*d + f]  alpha, gamma
+  double* Cf = Wa_s + (YZS || A.wa_g || A.Rg ? 0 : NWK * KPL * d * 32 + NWK * f * 32);  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
   double* Red = Cf + K * d + f + 1 + TI;                  // [NWK][8][33] ybar reductions
   // YZS: per-warp mbarriers [NWK][NS] and rings [NWK][NS][SLOT] (16-byte aligned); the ybar scratch
@@ -884,7 +892,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
   }
   for (int idx = tid; idx < 2 * TI * XS; idx += blockDim.x) Xs[idx] = ((idx % XS) == 0) ? 1.0 : 0.0;
   if (!YZS)
-    for (int idx = tid; idx < NWK * KPL * d * 32 + NWK * f * 32; idx += blockDim.x) Wa[idx] = 0.0;
+    for (int idx = tid; idx < (A.Rg ? 0 : NWK * KPL * d * 32 + NWK * f * 32); idx += blockDim.x) Wa[idx] = 0.0;
   for (int idx = tid; idx < K * d + f; idx += blockDim.x) Cf[idx] = A.coef[A.off_alpha + idx];
   const double* alpha = Cf;
   const double* gamma = Cf + K * d;
@@ -1023,7 +1031,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
                               lane, Ring + (size_t)w * A.NS * A.SLOT, yst);
         done = true;
       } else if constexpr (KPL <= 2) {  // register path (the larger KPL would spill)
-        if ((f + d) * KPL <= 32) {
+        if ((f + d) * KPL <= 32 && !A.Rg) {
           phase_e_reg<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
           done = true;
         }
@@ -1199,6 +1207,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     }
     return;
   }
+  if (A.Rg) return;  // stream mode: k_yz_grad writes this CTA's alpha / gamma slots
   // register partials of gamma components 8..15 into Wa (each (warp, lane) slot is private)
 #pragma unroll
   for (int e = 8; e < gam_regs<KPL>(); ++e)
@@ -1223,6 +1232,71 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
         for (int ln = 0; ln < 32; ++ln) v += Wa[NWK * KPL * d * 32 + (ww * f + e) * 32 + ln];
     }
     out[2 + A.off_gamma + e] = v;
+  }
+}
+
+// Stream mode (many alternative-varying variables): the alpha / gamma gradient partials of CTA b
+// over the same contiguous share of the individuals, from the residual rows r_i (Rg) written by
+// pass 1:  g[alpha_k,c] = sum_i z_ikc r_ik,  g[gamma_e] = sum_i sum_k y_ike r_ik.
+// Threads own elements t of the K d (K f) row, 256 x YG_CH per chunk, in registers; Z and Y rows
+// are read once, coalesced; the gamma sums over k go through shared memory in a fixed order.
+constexpr int YG_CH = 8;
+__global__ void __launch_bounds__(256) k_yz_grad(int64_t N, int K, int d, int f, const double* __restrict__ Y,
+                                                const double* __restrict__ Z, const double* __restrict__ Rg,
+                                                double* part, int n_part, int off_alpha, int off_gamma) {
+  __shared__ double sred[256 * YG_CH];
+  __shared__ double gsum[64];
+  const int tid = threadIdx.x;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t i_lo = b * N / G, i_hi = (b + 1) * N / G;
+  double* out = part + b * (int64_t)n_part;
+  // blockIdx.y: alpha chunk y (of 256 YG_CH elements); the y == 0 CTAs also do the gamma pass
+  for (int pass = 0; pass < 2; ++pass) {
+    const int W = pass == 0 ? d : f;  // values per alternative
+    if (W == 0 || (pass == 1 && blockIdx.y != 0)) continue;
+    const double* D = pass == 0 ? Z : Y;
+    const int L = K * W;
+    if (pass == 1) {
+      if (tid < f) gsum[tid] = 0.0;
+      __syncthreads();
+    }
+    const int t_begin = pass == 0 ? (int)blockIdx.y * 256 * YG_CH : 0;
+    const int t_end = pass == 0 ? min(L, t_begin + 256 * YG_CH) : L;
+    for (int t0 = t_begin; t0 < t_end; t0 += 256 * YG_CH) {
+      double acc[YG_CH];
+      int kt[YG_CH];
+#pragma unroll
+      for (int j = 0; j < YG_CH; ++j) {
+        const int t = t0 + tid + 256 * j;
+        kt[j] = t < L ? t / W : -1;
+        acc[j] = 0.0;
+      }
+#pragma unroll 4
+      for (int64_t i = i_lo; i < i_hi; ++i) {
+        const double* row = D + i * L + t0 + tid;
+        const double* rr = Rg + i * K;
+#pragma unroll
+        for (int j = 0; j < YG_CH; ++j)
+          if (kt[j] >= 0) acc[j] = fma(__ldg(row + 256 * j), __ldg(rr + kt[j]), acc[j]);
+      }
+      if (pass == 0) {
+#pragma unroll
+        for (int j = 0; j < YG_CH; ++j)
+          if (kt[j] >= 0) out[2 + off_alpha + t0 + tid + 256 * j] = acc[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < YG_CH; ++j) sred[tid + 256 * j] = kt[j] >= 0 ? acc[j] : 0.0;
+        __syncthreads();
+        if (tid < f) {  // elements t = t0 + idx with t mod f == tid, in increasing idx order
+          const int n = min(256 * YG_CH, L - t0);
+          double v = gsum[tid];
+          for (int idx = ((tid - t0) % f + f) % f; idx < n; idx += f) v += sred[idx];
+          gsum[tid] = v;
+        }
+        __syncthreads();
+      }
+    }
+    if (pass == 1 && tid < f) out[2 + off_gamma + tid] = gsum[tid];
   }
 }
 
@@ -1434,11 +1508,14 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
     }
   }
   plan->ti = plan->yzs ? YZS_TI : tile_rows(kpl, (D.d + D.f) > 0);
+  plan->stream = 0;
   if (smem > 227 * 1024 && !plan->yzs && (D.d + D.f) > 0) {
-    // many alternative-specific / generic variables: gradient partials to global scratch
+    // many alternative-specific / generic variables: no gradient partials in shared memory; pass 1
+    // writes the residual rows and k_yz_grad streams Z and Y for the alpha / gamma gradients
     smem = eval_smem(D, kpl, false, 0, true);
-    plan->wa = (int64_t)NW * kpl * D.d * 32 + (int64_t)NW * D.f * 32;
+    plan->stream = 1;
   }
+  plan->rg = plan->stream ? D.N * (int64_t)D.K : 0;
   if (smem > 227 * 1024) return false;  // sm_100a opt-in maximum (232448 bytes)
   // register budget: phase-C accumulators (cm x cn blocks) + the phase-B row (nbn blocks)
   const int nwarps = plan->yzs ? NWY : NW;
@@ -1460,7 +1537,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   return true;
 }
 
-static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
+static cudaError_t launch_eval_core(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
                                     const double* Z, const int32_t* choice, const double* coef, const Packed* pk,
                                     bool want_grad, bool writeP, bool hv, double* part, int* err, cudaStream_t st) {
   EvalArgs a;
@@ -1475,6 +1552,7 @@ static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const d
   a.part = part; a.n_part = plan.n_part; a.err = err;
   a.wa = plan.wa;
   a.wa_g = plan.wa ? part + (size_t)plan.grid * plan.n_part : nullptr;
+  a.Rg = plan.stream ? part + (size_t)plan.grid * (plan.n_part + plan.wa) : nullptr;
   a.NS = plan.ns;
   a.SLOT = D.K * (D.f + D.d);
 #define MNL_EVAL_CM(KPL_, HV_, YZS_)                                                         \
@@ -1505,6 +1583,19 @@ static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const d
 #undef MNL_EVAL_CM
 #undef MNL_EVAL_CASE
   return cudaErrorInvalidValue;
+}
+
+static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
+                                    const double* Z, const int32_t* choice, const double* coef, const Packed* pk,
+                                    bool want_grad, bool writeP, bool hv, double* part, int* err, cudaStream_t st) {
+  cudaError_t e = launch_eval_core(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, hv, part, err, st);
+  if (e != cudaSuccess || !plan.stream || !want_grad) return e;
+  double* Rg = part + (size_t)plan.grid * (plan.n_part + plan.wa);
+  const int ny = std::max(1, (D.K * D.d + 256 * YG_CH - 1) / (256 * YG_CH));  // alpha chunks
+  k_yz_grad<<<dim3(plan.grid, ny), 256, 0, st>>>(D.N, D.K, D.d, D.f, Y, Z, Rg, part, plan.n_part, D.off_alpha,
+                                                 D.off_gamma);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,
