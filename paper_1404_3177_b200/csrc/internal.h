@@ -51,14 +51,12 @@ struct EvalPlan {
   int stream;   // alpha / gamma gradients by k_yz_grad from residual rows (rg doubles of scratch)
   int64_t rg;
   int ti;       // individuals per tile
-  int64_t wa;   // > 0: the alpha/gamma gradient partials live in global scratch (wa doubles per CTA,
-                // after the grid x n_part partials) because they do not fit in shared memory
   size_t smem;
   int n_part;  // 2 + n_p
 };
 bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
-// doubles of the `part` scratch a launch with this plan needs (partials + global gradient partials)
-inline size_t eval_part_doubles(const EvalPlan& ep) { return (size_t)ep.grid * (ep.n_part + ep.wa) + ep.rg; }
+// doubles of the `part` scratch a launch with this plan needs (CTA partials + stream-mode residual rows)
+inline size_t eval_part_doubles(const EvalPlan& ep) { return (size_t)ep.grid * ep.n_part + ep.rg; }
 // Pass 1 (a1-a4): utilities, softmax, loglik partials, gradient partials (if want_grad),
 // and the probability rows Pr (if writeP). part: [grid][n_part].
 cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, const double* Y,

@@ -42,8 +42,6 @@ struct EvalArgs {
   int64_t N;
   int K, p, f, d, q, n_p, off_alpha, off_gamma, QP, XS, TI, SCR;
   int NS, SLOT;  // YZS path: ring slots per warp, doubles per slot (K (f + d))
-  double* wa_g;  // non-null: alpha / gamma gradient partials in global scratch (per CTA)
-  int64_t wa;    // doubles per CTA of wa_g
   double* Rg;    // non-null (stream mode): residual rows r_i [N][K] for k_yz_grad, which then forms
                  // the alpha / gamma gradients by streaming Z and Y (many alternative-varying vars)
   const double* X;
@@ -874,10 +872,10 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
   // [TI][KPS] utilities from phase B (YZS: in place in Rs, each lane overwrites its own u by r)
   double* Ps = YZS ? Rs : Rs + TI * KPS;
   // [NWK][KPL][d][32] alpha-gradient, lane-private, then [NWK][f][32] gamma-gradient (e >= 8);
-  // in global scratch (A.wa_g, L1/L2-resident read-modify-writes) when it does not fit here
+  // absent in stream mode (A.Rg: k_yz_grad forms those gradients) and in the YZS path (registers)
   double* Wa_s = Rs + ((d + f) && !YZS ? 2 * TI * KPS : TI * KPS);
-  double* Wa = A.wa_g ? A.wa_g + (size_t)blockIdx.x * A.wa : Wa_s;
-  double* Cf = Wa_s + (YZS || A.wa_g || A.Rg ? 0 : NWK * KPL * d * 32 + NWK * f * 32);  // [K*d + f]  alpha, gamma
+  double* Wa = Wa_s;
+  double* Cf = Wa_s + (YZS || A.Rg ? 0 : NWK * KPL * d * 32 + NWK * f * 32);  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
   double* Red = Cf + K * d + f + 1 + TI;                  // [NWK][8][33] ybar reductions
   // YZS: per-warp mbarriers [NWK][NS] and rings [NWK][NS][SLOT] (16-byte aligned); the ybar scratch
@@ -1464,13 +1462,13 @@ __global__ void __launch_bounds__(1024) k_cg_dir(int n, double beta, const doubl
 static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }
 
-static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns, bool wa_global = false, int ti = 0) {
+static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns, bool stream = false, int ti = 0) {
   const int KP = 32 * kpl, KPS = KP + 4, TI = yzs ? YZS_TI : (ti ? ti : tile_rows(kpl, (D.d + D.f) > 0));
   const int slot = D.K * (D.f + D.d);
   const int nw = yzs ? NWY : NW;
   size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
              ((D.d + D.f) && !yzs ? (size_t)TI * KPS : 0) +
-             (yzs || wa_global ? 0 : (size_t)nw * kpl * D.d * 32 + (size_t)nw * D.f * 32) +
+             (yzs || stream ? 0 : (size_t)nw * kpl * D.d * 32 + (size_t)nw * D.f * 32) +
              (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
              ((D.d + D.f) && !yzs ? (size_t)nw * 8 * 33 : 0);
   if (yzs) {
@@ -1495,7 +1493,6 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   const bool yzs_ok = (D.d + D.f) > 0 && kpl <= 2 && D.f % 2 == 0 && D.f <= YZS_F && D.d <= YZS_D &&
                       (D.K * D.f) % 2 == 0 && (D.K * D.d) % 2 == 0 && !getenv("MNL_NO_YZS");
   size_t smem = eval_smem(D, kpl, false, 0);
-  plan->wa = 0;
   if (yzs_ok) {
     for (int ns = 4; ns >= 2; --ns) {  // 4: two rows computed while the next two land
       const size_t sz = eval_smem(D, kpl, true, ns);
@@ -1550,9 +1547,7 @@ static cudaError_t launch_eval_core(const Dims& D, const EvalPlan& plan, const d
   a.ldP = (writeP || hv) ? pk->ldP : 0;
   a.want_grad = want_grad; a.writeP = writeP && !hv;
   a.part = part; a.n_part = plan.n_part; a.err = err;
-  a.wa = plan.wa;
-  a.wa_g = plan.wa ? part + (size_t)plan.grid * plan.n_part : nullptr;
-  a.Rg = plan.stream ? part + (size_t)plan.grid * (plan.n_part + plan.wa) : nullptr;
+  a.Rg = plan.stream ? part + (size_t)plan.grid * plan.n_part : nullptr;
   a.NS = plan.ns;
   a.SLOT = D.K * (D.f + D.d);
 #define MNL_EVAL_CM(KPL_, HV_, YZS_)                                                         \
@@ -1590,7 +1585,7 @@ static cudaError_t launch_eval_impl(const Dims& D, const EvalPlan& plan, const d
                                     bool want_grad, bool writeP, bool hv, double* part, int* err, cudaStream_t st) {
   cudaError_t e = launch_eval_core(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, hv, part, err, st);
   if (e != cudaSuccess || !plan.stream || !want_grad) return e;
-  double* Rg = part + (size_t)plan.grid * (plan.n_part + plan.wa);
+  double* Rg = part + (size_t)plan.grid * plan.n_part;
   const int ny = std::max(1, (D.K * D.d + 256 * YG_CH - 1) / (256 * YG_CH));  // alpha chunks
   k_yz_grad<<<dim3(plan.grid, ny), 256, 0, st>>>(D.N, D.K, D.d, D.f, Y, Z, Rg, part, plan.n_part, D.off_alpha,
                                                  D.off_gamma);
