@@ -355,10 +355,14 @@ struct FragArgs {
   int seg_ld[3];
   int seg_off[3];
   int nh;  // CTAs per chunk (frag_nh: KC / nh staged rows)
-  // optional second operand from the same staged rows (J2: A and B in one pass); tiles2 = 0: none
+  // optional second / third operands from the same staged rows (J2: A, B and the tail's B in one
+  // pass); tiles2 / tiles3 = 0: none
   const ColDesc* desc2;
   double* out2;
   int tiles2, BT2;
+  const ColDesc* desc3;
+  double* out3;
+  int tiles3, BT3;
 };
 
 // offset into a KC-row stage -> offset into the KC/2-row stage (segment bases halve; the in-row
@@ -391,12 +395,14 @@ __global__ void __launch_bounds__(256) k_frag(const FragArgs F) {
   // the k-slices; for each k-slice a warp stores 512 contiguous bytes. Descriptor offsets assume
   // KC staged rows per segment (seg_off = KC * preceding lds): rebase to the half-size stage.
   const int KS = F.KC / 4;
-  const int W1 = (F.BT / 16) * 32, W2 = (F.BT2 / 16) * 32, n1 = F.tiles * W1;
-  for (int wi = threadIdx.x; wi < n1 + F.tiles2 * W2; wi += blockDim.x) {
-    const bool second = wi >= n1;  // CTA-uniform ranges; the branch only picks the operand
-    const int w = second ? wi - n1 : wi, W = second ? W2 : W1, BT = second ? F.BT2 : F.BT;
-    const ColDesc* desc = second ? F.desc2 : F.desc;
-    double* outp = second ? F.out2 : F.out;
+  const int W1 = (F.BT / 16) * 32, W2 = (F.BT2 / 16) * 32, W3 = (F.BT3 / 16) * 32;
+  const int n1 = F.tiles * W1, n2 = n1 + F.tiles2 * W2;
+  for (int wi = threadIdx.x; wi < n2 + F.tiles3 * W3; wi += blockDim.x) {
+    const int which = wi < n1 ? 0 : (wi < n2 ? 1 : 2);  // picks the operand only
+    const int w = which == 0 ? wi : (which == 1 ? wi - n1 : wi - n2);
+    const int W = which == 0 ? W1 : (which == 1 ? W2 : W3), BT = which == 0 ? F.BT : (which == 1 ? F.BT2 : F.BT3);
+    const ColDesc* desc = which == 0 ? F.desc : (which == 1 ? F.desc2 : F.desc3);
+    double* outp = which == 0 ? F.out : (which == 1 ? F.out2 : F.out3);
     const int t = w / W, r = w - t * W, lane = r & 31;
     const int col = t * BT + (r >> 5) * 16 + (lane >> 2);
     ColDesc d0 = desc[col], d1 = desc[col + 8];
@@ -706,8 +712,10 @@ struct AsmArgs {
   int ld1;
   const double* C1b; // [pairs_pad][ld1b] vech columns [n1a, ...)
   int ld1b, n1a;
-  const double* C2;  // [n_p_pad][ld2]    (reduced)
+  const double* C2;  // [n_p_pad][ld2]    (reduced) Z/Y columns [0, n2a)
   int ld2;
+  const double* C2b; // [n_p_pad][ld2b]   Z/Y columns [n2a, ...)
+  int ld2b, n2a;
   const double* T;   // [K][E][F]         (reduced)
   double* out;
   int ld_out;
@@ -734,7 +742,8 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
       negH = v < A.n1a ? A.C1[pr * A.ld1 + v] : A.C1b[pr * A.ld1b + (v - A.n1a)];
     } else {
       const int lo = min(r, c), hi = max(r, c);
-      double u = A.C2[(int64_t)lo * A.ld2 + (hi - A.n_beta)];
+      const int c2 = hi - A.n_beta;
+      double u = c2 < A.n2a ? A.C2[(int64_t)lo * A.ld2 + c2] : A.C2b[(int64_t)lo * A.ld2b + (c2 - A.n2a)];
       // same-alternative / generic terms T (J3)
       double tv = 0.0;
       auto cls = [&](int x, int& kind, int& k, int& idx) {
@@ -799,8 +808,10 @@ struct GemmJob {
 
 struct HessPlan {
   bool has_j2;
+  bool has_j2b = false;  // J2's Z/Y columns as whole main tiles + a narrow tail job (shares j2's A)
+  int n2a = 0;           // Z/Y columns computed by j2
   bool bvalid = false;  // J1's precomputed B fragments match the packed design rows
-  GemmJob j1, j1b, j2;  // j1b: the vech columns beyond the last whole 128-column tile of j1
+  GemmJob j1, j1b, j2, j2b;  // j1b / j2b: the columns beyond the last whole main tile of j1 / j2
   bool has_j1b = false;
   int n1a = 0;          // vech columns computed by j1
   int ar_splits, ar_mt, ar_nt, ar_ep, ar_fp, ar_ci, ar_rs;
@@ -1037,24 +1048,62 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       const int MA = (int)A.size(), MB = (int)B.size();
       const bool frag_fits = frag_nh((size_t)KC * (pk.ldP + pk.ldX + (d > 0 ? pk.ldZ : 0))) > 0;
       int bn2 = choose_bn(MB);
+      hp->has_j2b = false;
+      hp->n2a = MB;
+      int bnt = 0;  // tail width when split
       if (KC == 32 && MB >= 192 && MA >= 512 && frag_fits && !getenv("MNL_NO_PIPE")) {
-        const int bnp = choose_bn_pipe(MB);
+        int bnp = choose_bn_pipe(MB);
+        // whole main tiles + a narrow tail when that executes fewer columns (c5: 260 = 2 x 112 + 36
+        // -> 272 instead of 3 x 96 = 288)
+        int best = (MB + bnp - 1) / bnp * bnp;
+        for (int bm : {128, 112, 96}) {
+          const int main_cols = MB / bm * bm, rem = MB - main_cols;
+          if (main_cols == 0 || rem == 0) continue;
+          int tail = 0;
+          for (int bt : {48, 64, 96, 112, 128})
+            if (bt >= rem) { tail = bt; break; }
+          if (tail && main_cols + tail < best * 0.98) {
+            best = main_cols + tail;
+            bnp = bm;
+            bnt = tail;
+            hp->n2a = main_cols;
+          }
+        }
         J.afrag = alloc_frag((MA + BM - 1) / BM, BM, pk, &bytes);
-        J.bfrag = J.afrag ? alloc_frag((MB + bnp - 1) / bnp, bnp, pk, &bytes) : nullptr;
+        J.bfrag = J.afrag ? alloc_frag((hp->n2a + bnp - 1) / bnp, bnp, pk, &bytes) : nullptr;
         if (J.afrag && !J.bfrag) {
           cudaFree(J.afrag);
           J.afrag = nullptr;
         }
         if (J.bfrag) bn2 = bnp;
+        hp->has_j2b = J.bfrag != nullptr && bnt > 0;
+        if (!hp->has_j2b) hp->n2a = MB;
       }
+      std::vector<ColDesc> Ba(B.begin(), B.begin() + hp->n2a), Bb(B.begin() + hp->n2a, B.end());
       J.own_afrag = true;
       J.mat_a = J.mat_b = J.bfrag != nullptr;
       J.b_design = false;
       J.dnseg = nseg;
       for (int sg = 0; sg < 3; ++sg) J.dseg_id[sg] = segs[sg];
       J.skip_off = (K - 1) * q;  // n_beta: C2 rows are theta indices, columns start at n_beta
-      if (setup_job(J, A, B, bn2, KC, pk, segs, nseg, sms, &bytes, J.mat_a)) break;
+      bool good = setup_job(J, A, Ba, bn2, KC, pk, segs, nseg, sms, &bytes, J.mat_a);
+      if (good && hp->has_j2b) {
+        GemmJob& T = hp->j2b;
+        T.agen = false;
+        T.bfrag = alloc_frag(1, bnt, pk, &bytes);
+        T.afrag = J.afrag;  // the tail shares j2's A operand (materialised by j2's k_frag launch)
+        T.own_afrag = false;
+        T.mat_a = T.mat_b = T.bfrag != nullptr;
+        T.b_design = false;
+        T.dnseg = nseg;
+        for (int sg = 0; sg < 3; ++sg) T.dseg_id[sg] = segs[sg];
+        T.skip_off = (K - 1) * q + hp->n2a;  // its columns start at n_beta + n2a
+        good = T.bfrag != nullptr && setup_job(T, A, Bb, bnt, KC, pk, segs, nseg, sms, &bytes, true);
+        if (!good) free_job(hp->j2b);
+      }
+      if (good) break;
       free_job(hp->j2);
+      hp->has_j2b = false;
       if (KC == 16) ok = false;
     }
     const int E = q + d + f, F = d + f;
@@ -1108,6 +1157,7 @@ void hess_plan_destroy(HessPlan* hp) {
   free_job(hp->j1);
   free_job(hp->j1b);
   free_job(hp->j2);
+  free_job(hp->j2b);
   cudaFree(hp->Tpart);
   cudaFree(hp->T);
   cudaFree(hp->counters);
@@ -1220,12 +1270,17 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
   return cudaGetLastError();
 }
 
-static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStream_t st, bool both = false) {
+static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStream_t st, bool both = false,
+                        const GemmJob* tailB = nullptr) {
   FragArgs F;
   F.desc2 = nullptr;
   F.out2 = nullptr;
   F.tiles2 = 0;
   F.BT2 = 16;
+  F.desc3 = tailB ? tailB->dB : nullptr;  // a tail job's B from the same staged rows
+  F.out3 = tailB ? tailB->bfrag : nullptr;
+  F.tiles3 = tailB ? tailB->tilesN : 0;
+  F.BT3 = tailB ? tailB->BN : 16;
   if (both) {  // A (a_side ignored) and B of the same job from one staging of the rows
     a_side = true;
     F.desc2 = J.dB;
@@ -1262,13 +1317,15 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
                            int ld_out, double sign, cudaStream_t st) {
   cudaEventRecord(hp->ev[7], st);
   {  // operand materialisation: weights every evaluation, design-only products after a re-pack
-    const GemmJob* jobs[3] = {&hp->j1, hp->has_j1b ? &hp->j1b : nullptr, hp->has_j2 ? &hp->j2 : nullptr};
+    const GemmJob* jobs[4] = {&hp->j1, hp->has_j1b ? &hp->j1b : nullptr, hp->has_j2 ? &hp->j2 : nullptr,
+                              hp->has_j2b ? &hp->j2b : nullptr};
     for (const GemmJob* J : jobs) {
       if (!J) continue;
-      if (J->mat_a && J->mat_b && J->own_afrag && !J->b_design) {  // J2: both per evaluation, one pass
-        launch_frag(*J, pk, true, st, true);
+      if (J->mat_a && J->mat_b && J->own_afrag && !J->b_design) {  // J2: A, B (+ the tail's B), one pass
+        launch_frag(*J, pk, true, st, true, (J == &hp->j2 && hp->has_j2b) ? &hp->j2b : nullptr);
         continue;
       }
+      if (J == &hp->j2b) continue;  // materialised with j2
       if (J->mat_b && (!J->b_design || !hp->bvalid)) launch_frag(*J, pk, false, st);
       if (J->mat_a && J->own_afrag) launch_frag(*J, pk, true, st);
     }
@@ -1290,6 +1347,10 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
   if (hp->has_j2) {
     e = run_job(hp->j2, pk, hp->counters + 1, hp->sms, st);
     if (e != cudaSuccess) return e;
+    if (hp->has_j2b) {
+      e = run_job(hp->j2b, pk, hp->counters + 1, hp->sms, st);
+      if (e != cudaSuccess) return e;
+    }
     const int E = D.q + D.d + D.f, F = D.d + D.f;
     {
       const int items = (D.K + 7) / 8 * hp->ar_ep * hp->ar_fp * hp->ar_splits;
@@ -1329,6 +1390,8 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
   A.C1 = hp->j1.Cred; A.ld1 = hp->j1.ldc;
   A.C1b = hp->has_j1b ? hp->j1b.Cred : nullptr; A.ld1b = hp->has_j1b ? hp->j1b.ldc : 0; A.n1a = hp->n1a;
   A.C2 = hp->has_j2 ? hp->j2.Cred : nullptr; A.ld2 = hp->has_j2 ? hp->j2.ldc : 0;
+  A.C2b = hp->has_j2b ? hp->j2b.Cred : nullptr; A.ld2b = hp->has_j2b ? hp->j2b.ldc : 0;
+  A.n2a = hp->has_j2b ? hp->n2a : (1 << 30);
   A.T = hp->T;
   A.out = out; A.ld_out = ld_out; A.sign = sign;
   const int64_t total = (int64_t)D.n_p * D.n_p;
