@@ -121,7 +121,8 @@ def test_eval_yz_paths(mode):
         os.environ[mode] = "1"
     try:
         for N, K, p, f, d in [(1000, 4, 3, 2, 1), (333, 50, 5, 10, 5), (2049, 6, 17, 2, 3), (65, 20, 0, 4, 0),
-                              (1, 4, 2, 2, 1), (3, 6, 0, 2, 2), (17, 64, 1, 16, 8), (40, 33, 2, 6, 7)]:
+                              (1, 4, 2, 2, 1), (3, 6, 0, 2, 2), (17, 64, 1, 16, 8), (40, 33, 2, 6, 7),
+                              (150, 8, 2, 64, 64), (60, 100, 0, 5, 20)]:  # stream mode (k_yz_grad)
             prob = datagen.custom(N, K, p, f, d, seed=7, coef_sd=0.3, require_all_classes=False)
             D = oracle_data(prob)
             dp = device_problem(prob)
