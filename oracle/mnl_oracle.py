@@ -53,6 +53,7 @@ from dataclasses import dataclass, field
 import numpy as np
 from scipy.linalg import solve_triangular
 
+KIND = "numpy"
 MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_NONFINITE, MNL_MAXITER = range(7)
 MAX_HALVINGS = 30          # R8
 TAU_REL = 1e-12            # R7: accept l_j >= l - TAU_REL * max(1, |l|)
