@@ -11,11 +11,12 @@ Workload: BASELINE.json configs[3] ("c4", N=500000, K=100, p=50, n_p=5049), the 
 config the metric is quoted on; inputs are synthetic (datagen, seed 0), resident in HBM and larger
 than L2 (X 200 MB, probability rows 416 MB), so no L2 flush is needed between steps.
 
---gpus N > 1: data-parallel over individuals (paper_1404_3177_b200/distributed.py): rank r owns a
-contiguous slice of the c4 individuals, one NCCL all-reduce of (l, g, H) per evaluation, every rank
-factors the same -H (strong scaling: the total work is fixed).
---impl reference: the CPU oracle (oracle/) as it stands, timed on this host's cores on a bounded
-sample of the same workload (the only other place bench.py executes oracle/).
+--gpus N > 1: data-parallel over individuals (mnl_newton_fit_dp; paper_1404_3177_b200/distributed.py):
+rank r owns a contiguous slice of the c4 individuals; NCCL all-reduces [l, flag, g] after every
+evaluation and the packed upper triangle of -H after the Hessian; every rank factors the same -H
+(strong scaling: the total work is fixed).
+--impl reference: the plain C oracle (oracle/oracle.c) as it stands, timed on this host's cores, one
+full-size Newton iteration per step (the only other place bench.py executes oracle/).
 """
 from __future__ import annotations
 
@@ -165,43 +166,15 @@ def run_dp(args):
     ch = torch.from_numpy(prob.choice[lo:hi].astype(np.int32)).to(dev)
     dp = M.problem(X, Y, Z, ch, K=spec.K)
     launches = [0]
-    ev_inner = DP.cuda_evaluator(dp)
-
-    def evaluate(theta, g, h):
-        r = ev_inner(theta, g, h)
-        launches[0] += M.last_launch_count()
-        return r
-
-    def solve(A, g):
-        A = A.contiguous()
-        rc = M.mnl_cholesky(A)
-        launches[0] += M.last_launch_count()
-        if rc != M.MNL_OK:
-            return rc, None
-        x = M.mnl_cholesky_solve(A, g.contiguous())
-        launches[0] += M.last_launch_count()
-        return M.MNL_OK, x
-
-    def all_reduce(t):
-        dist.all_reduce(t)
-
     theta0 = torch.zeros(spec.n_params, dtype=torch.float64, device=dev)
-    pk_inner = DP.cuda_packer()
-
-    def pack(H):
-        v = pk_inner[0](H)
-        launches[0] += M.last_launch_count()
-        return v
-
-    def unpack(v, n):
-        H = pk_inner[1](v, n)
-        launches[0] += M.last_launch_count()
-        return H
-
-    packer = (pack, unpack)
+    allreduce = DP.torch_allreduce()   # NCCL, ordered on the library's stream
 
     def step():
-        return DP.newton_fit_dp(evaluate, all_reduce, solve, theta0, tol=1e-300, max_iter=1, packer=packer)
+        # one Newton iteration of the library's data-parallel driver (mnl_newton_fit_dp): exchanges
+        # [l, flag, g] per evaluation and the packed upper triangle of -H per Hessian
+        f = M.mnl_newton_fit_dp(dp, allreduce, coef0=theta0, tol=1e-300, max_iter=1)
+        launches[0] += M.last_launch_count()
+        return f
 
     for _ in range(args.warmup):
         step()
@@ -262,8 +235,8 @@ def run_dp(args):
             "config": {"workload": f"{args.config}: N={spec.N} K={spec.K} p={spec.p} f={spec.f} d={spec.d} "
                                    f"n_p={spec.n_params}, one Newton iteration from theta=0 per step",
                        "l2": "inputs larger than L2 (no flush)",
-                       "parallelism": f"data-parallel over individuals, {ws} ranks, one NCCL all-reduce of "
-                                      f"(l, g, packed upper triangle of H)"},
+                       "parallelism": f"data-parallel over individuals, {ws} ranks (mnl_newton_fit_dp): NCCL "
+                                      f"all-reduce of [l, flag, g] per evaluation and of the packed -H per Hessian"},
             "s_per_newton_iter": ms / args.steps / 1e3,
             "roofline": roof,
             "gpu_launches": int(launches[0]),
@@ -387,55 +360,99 @@ def run_ours(args):
     return result, prob
 
 
-def oracle_iteration_seconds(prob, n_sample: int):
-    """One oracle Newton iteration (oracle/, as it stands) on the first n_sample individuals."""
-    import oracle as O
-    s = prob.spec
-    D = O.Data(prob.X[:n_sample], prob.Y[:n_sample], prob.Z[:n_sample], prob.choice[:n_sample], s.K)
-    t0 = time.perf_counter()
-    O.newton_fit(D, coef0=None, tol=1e-300, max_iter=1)
-    return time.perf_counter() - t0
-
-
-def cpu_threads():
+def cpu_model() -> str:
     try:
-        from threadpoolctl import threadpool_info
-        info = threadpool_info()
-        return max([i.get("num_threads", 1) for i in info] + [1])
-    except Exception:
-        return os.cpu_count()
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_data(prob, n=None):
+    import oracle as O
+    n = prob.spec.N if n is None else n
+    return O.Data(prob.X[:n], prob.Y[:n], prob.Z[:n], prob.choice[:n], prob.spec.K)
+
+
+def oracle_iteration_seconds(prob, n=None, threads=0):
+    """One Newton iteration of the plain C oracle (oracle/oracle.c, as it stands) from theta = 0 on the
+    first n individuals (all by default): l and g, H, Cholesky of -H, the step-halving line search and
+    l, g at the new iterate -- the same work as one bench step."""
+    from oracle import coracle as OC
+    n0 = OC.set_threads(0)
+    try:
+        OC.set_threads(threads)
+        D = _oracle_data(prob, n)
+        t0 = time.perf_counter()
+        OC.newton_fit(D, coef0=None, tol=1e-300, max_iter=1)
+        return time.perf_counter() - t0
+    finally:
+        OC.set_threads(n0)
 
 
 def cpu_baseline(prob, n_sample):
-    t = oracle_iteration_seconds(prob, n_sample)
-    scale = prob.spec.N / n_sample
-    return {"value": 1.0 / (t * scale), "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"one oracle Newton iteration on the first {n_sample} of {prob.spec.N} individuals "
-                      f"of {prob.spec.name} ({t:.2f} s), time scaled x{scale:.0f} (Hessian work is linear in N)"}
+    """The C oracle on a bounded sample: its N-proportional phases (pass 1, gradient,
+    Hessian, line-search passes) timed on the first n_sample individuals and scaled by N / n_sample,
+    plus its N-independent phase (the Cholesky factor + solves of the full n_p x n_p -H, timed at full
+    size); then the single-thread context of c1-c3 (the paper timed one core)."""
+    from oracle import coracle as OC
+    s = prob.spec
+    D = _oracle_data(prob, n_sample)
+    th = np.zeros(s.n_params)
+    t0 = time.perf_counter()
+    _, g, H = OC.mnl_eval(D, th)              # l, g, H at theta = 0
+    t_eval = time.perf_counter() - t0
+    A = -H
+    t0 = time.perf_counter()
+    L = OC.cholesky(A)                        # n_p^3 / 3: independent of N
+    t_chol = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for _ in range(4):                        # the c4 step's line-search passes + the new iterate's l, g
+        OC.loglik(D, th)
+    t_ls = time.perf_counter() - t0
+    del L
+    scale = s.N / n_sample
+    per_iter = (t_eval + t_ls) * scale + t_chol
+    ctx = {}
+    for c in ("c1", "c2", "c3"):
+        pc = datagen.make(c)
+        ctx[c] = {"s_per_newton_iter_1_thread": oracle_iteration_seconds(pc, threads=1)}
+    return {"value": 1.0 / per_iter, "unit": UNIT, "cores": OC.set_threads(0), "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"C oracle (oracle/oracle.c): l, g, H and 4 loglik passes on the first {n_sample} of {s.N} "
+                      f"individuals of {s.name} ({t_eval + t_ls:.2f} s, scaled x{scale:.0f}: linear in N) + the "
+                      f"Cholesky of the full {s.n_params}x{s.n_params} -H ({t_chol:.2f} s, not scaled)",
+            "single_thread_context": ctx}
 
 
 def run_reference(args):
+    """The reference arm: the plain C oracle as it stands, one FULL-size Newton iteration per step (no
+    sampling, no scaling), on every host core. A step takes about a minute on c4, so the run stops
+    after --ref-budget seconds of timed steps (at least one) and reports the steps it actually ran."""
     ws, rank, local = dist_env()
     if rank != 0:
         return None
+    from oracle import coracle as OC
     prob = datagen.make(args.config, seed=args.seed)
-    n = args.oracle_sample
-    for _ in range(args.warmup):
-        oracle_iteration_seconds(prob, n)
-    times = [oracle_iteration_seconds(prob, n) for _ in range(args.steps)]
-    scale = prob.spec.N / n
-    per_step = float(np.mean(times)) * scale
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < args.steps and (not times or time.perf_counter() - t_start < args.ref_budget):
+        times.append(oracle_iteration_seconds(prob))
+    per_step = float(np.mean(times))
     value = 1.0 / per_step
-    cb = {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
-          "sample": f"each step: one oracle Newton iteration on the first {n} of {prob.spec.N} individuals "
-                    f"of {prob.spec.name}, time scaled x{scale:.0f}"}
     spec = prob.spec
-    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen seed %d)" % args.seed,
+    cb = {"value": value, "unit": UNIT, "cores": OC.set_threads(0), "kind": "oracle", "cpu_model": cpu_model(),
+          "sample": f"none: each step is one full-size C-oracle Newton iteration ({spec.N} individuals); "
+                    f"{len(times)} timed steps, no warm-up (a CPU program without caches to warm)"}
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": len(times), "warmup": 0, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen seed %d)" % args.seed,
             "config": {"workload": f"{args.config}: N={spec.N} K={spec.K} p={spec.p} f={spec.f} d={spec.d} "
                                    f"n_p={spec.n_params}, one Newton iteration from theta=0 per step",
-                       "l2": "n/a (CPU)", "parallelism": "host cores"},
+                       "l2": "n/a (CPU)", "parallelism": "host cores (OpenMP)"},
+            "step_s": times, "requested_steps": args.steps, "requested_warmup": args.warmup,
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -512,7 +529,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=list(datagen.CONFIGS))
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--oracle-sample", type=int, default=2000)
+    ap.add_argument("--oracle-sample", type=int, default=50000)
+    ap.add_argument("--ref-budget", type=float, default=240.0, help="reference arm: seconds of timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true")

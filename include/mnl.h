@@ -30,11 +30,17 @@
  *
  * OWNERSHIP. The caller owns every buffer passed in. Device pointers must be 16-byte aligned
  * (torch allocations are). The library owns its scratch (probabilities, packed design rows,
- * split-N partial tiles, Cholesky workspace), cached per device and freed by mnl_release().
+ * split-N partial tiles, Cholesky workspace), cached per (device, stream) and freed by
+ * mnl_release().
  *
  * SYNCHRONISATION. Every call enqueues on `stream` (a cudaStream_t; NULL = legacy default
- * stream), synchronises that stream before returning, and returns a final status code.
- * Calls are serialised internally (one scratch cache per process).
+ * stream) of the CURRENT device, synchronises that stream before returning (mnl_eval_async
+ * excepted), and returns a final status code.
+ *
+ * THREADING. Reentrant across distinct streams: each (device, stream) pair has its own scratch
+ * and lock, so calls on different streams (from any threads, on any devices) run concurrently;
+ * calls on the same stream are serialised. The host-buffer entry points share one internal
+ * stream per device. mnl_release() must not overlap any other call.
  *
  * SIZE LIMITS OF THIS BUILD (MNL_ERR_ARG beyond them): 2 <= K <= 256, 0 <= d <= 64, 0 <= f <= 64,
  * 1 <= N < 2^31, n_p <= 16384, and p bounded by the pass-1 kernel's register-resident beta-gradient
@@ -90,8 +96,9 @@ int mnl_eval(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
  *           outside [0, K)) or MNL_ERR_NONFINITE (non-finite loglik)
  * Host-side argument errors (sizes, NULL pointers, misalignment) are returned immediately; the
  * return value MNL_OK means "enqueued". The first call for a problem shape allocates library
- * scratch (which synchronises); later calls of the same shape launch only. The scratch is shared:
- * calls on different streams must not overlap in time. */
+ * scratch (which synchronises); later calls of the same shape launch only. The scratch belongs to
+ * `stream`'s workspace, so asynchronous calls on different streams may overlap; consecutive calls
+ * on one stream are ordered by the stream. */
 int mnl_eval_async(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
                    const double* X, const double* Y, const double* Z, const int32_t* choice,
                    const double* coef, double* loglik, double* grad, double* hess, int32_t* status,
@@ -130,6 +137,9 @@ typedef struct {
   double delta_loglik;      /* |l_t - l_(t-1)| of the last accepted update (0 without one) */
   int32_t stop_reason;      /* mnl_stop_reason */
   int32_t cg_iters;         /* total conjugate-gradient iterations (method MNL_METHOD_CG) */
+  double min_margin;        /* R7 audit: min over every line-search decision (accepted or rejected) of
+                               |l_j - (l - tau)| / max(1,|l|); a decision closer than ~1e-13 to its
+                               threshold could flip under a different summation order (+inf if none) */
 } mnl_fit_stats;
 
 /* Why a fit stopped: the first of the paper's three conditions met. */
@@ -173,6 +183,30 @@ int mnl_newton_fit_opts(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
                         const double* X, const double* Y, const double* Z, const int32_t* choice,
                         const double* coef0, const mnl_fit_options* opts,
                         double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats, void* stream);
+
+/* Element-wise sum of `count` doubles of the DEVICE buffer `buf` across all ranks of the caller's
+ * process group, in place, ordered on `stream` (a cudaStream_t) -- e.g. ncclAllReduce(ncclSum) or
+ * torch.distributed.all_reduce. Every rank must receive bitwise-identical sums (true of NCCL and of
+ * any reduction that computes once and broadcasts). Return 0 on success. */
+typedef int (*mnl_allreduce_fn)(double* buf, int64_t count, void* stream, void* ctx);
+
+/* Data-parallel Newton-Raphson fit over individuals: l, g and H are
+ * sums over individuals, so each rank passes ITS OWN individuals
+ * (N, X, Y, Z, choice: a shard, N >= 1) and the same coef0 / options; the library runs the same
+ * driver as mnl_newton_fit_opts and calls `allreduce` at each exchange step:
+ *   after every pass-1 evaluation  [l, bad-choice flag, g]          (n_p + 2 doubles)
+ *   after every Hessian            packed upper triangle of -H      (n_p (n_p + 1) / 2 doubles)
+ *   (MNL_METHOD_CG: after every H v product, n_p doubles, instead of the Hessian)
+ * Every rank therefore takes the same decisions (stop tests, Cholesky of the same -H, line-search
+ * accept / reject on the same summed l) and returns the same coef, iters and loglik. A bad choice
+ * on any rank is MNL_ERR_ARG on every rank; a non-finite l on any rank makes the summed l non-finite
+ * (the trial is rejected everywhere). A CUDA error or a failed `allreduce` (non-zero return) ends
+ * the call on that rank only: the caller must then abort the group. */
+int mnl_newton_fit_dp(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
+                      const double* X, const double* Y, const double* Z, const int32_t* choice,
+                      const double* coef0, const mnl_fit_options* opts,
+                      mnl_allreduce_fn allreduce, void* allreduce_ctx,
+                      double* coef, int32_t* iters, double* loglik, mnl_fit_stats* stats, void* stream);
 
 /* Hessian-vector product at `coef`: hv = H v (P:462-476 applied to v without forming H):
  *   hv = -sum_i J_i^T (diag(P_i) - P_i P_i^T) J_i v,  J_i = d u_i / d theta
@@ -220,8 +254,8 @@ int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, v
 
 /* Packed upper triangle of a symmetric dev [n][n] row-major matrix: packed[off(i) + j - i] =
  * H[i][j] for j >= i, off(i) = i n - i (i - 1) / 2 (n (n + 1) / 2 doubles), and back (both
- * triangles written, exactly symmetric). The data-parallel fit all-reduces [l, g, packed H] in one
- * collective (half the bytes of the full matrix). */
+ * triangles written, exactly symmetric). The data-parallel fit all-reduces the packed -H (written
+ * straight by the Hessian assembly) -- half the bytes of the full matrix. */
 int mnl_sym_pack(int32_t n, const double* H, double* packed, void* stream);
 int mnl_sym_unpack(int32_t n, const double* packed, double* H, void* stream);
 
@@ -237,7 +271,8 @@ int mnl_last_hessian_times(double out[7]);
  * utility / softmax / loglik / gradient pass) launched by any call. */
 int mnl_last_eval_ms(double* ms);
 
-/* Kernel launches made by the last call on this thread (for the bench's gpu_launches). */
+/* Kernel launches made by the last call on this thread (for the bench's gpu_launches).
+ * mnl_last_eval_ms / mnl_last_hessian_times refer to the workspace of this thread's last call. */
 int64_t mnl_last_launch_count(void);
 
 const char* mnl_status_string(int code);

@@ -24,7 +24,7 @@ EXPORTED = ("mnl_num_params", "mnl_eval", "mnl_newton_fit", "mnl_newton_fit_ex",
             "mnl_newton_fit_host", "mnl_cholesky", "mnl_cholesky_solve", "mnl_last_launch_count",
             "mnl_status_string", "mnl_release", "mnl_last_hessian_times", "mnl_newton_fit_opts", "mnl_hessvec",
             "mnl_std_errors", "mnl_predict", "mnl_last_eval_ms", "mnl_eval_async", "mnl_sym_pack",
-            "mnl_sym_unpack", "mnl_check_shape")
+            "mnl_sym_unpack", "mnl_check_shape", "mnl_newton_fit_dp")
 
 MNL_STOP_NONE, MNL_STOP_GTOL, MNL_STOP_FTOL, MNL_STOP_MAXITER = range(4)
 MNL_METHOD_NEWTON, MNL_METHOD_CG = 0, 1
@@ -48,13 +48,16 @@ class FitStats(ctypes.Structure):
                 ("hess_ms", ctypes.c_double), ("chol_ms", ctypes.c_double), ("eval_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("gemm_ms", ctypes.c_double),
                 ("halvings_per_iter", ctypes.c_int32 * 64), ("delta_loglik", ctypes.c_double),
-                ("stop_reason", ctypes.c_int32), ("cg_iters", ctypes.c_int32)]
+                ("stop_reason", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("min_margin", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "halvings_per_iter"}
         d["halvings_per_iter"] = list(self.halvings_per_iter[: min(self.iters, 64)])
         return d
 
+
+# int (*)(double* buf, int64_t count, void* stream, void* ctx): in-place sum across ranks (mnl.h)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
 
 _lib = None
 
@@ -85,6 +88,10 @@ def load(build_if_missing: bool = False):
     lib.mnl_newton_fit_opts.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, ctypes.POINTER(FitOptions), V,
                                         ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(FitStats), V]
     lib.mnl_newton_fit_opts.restype = ctypes.c_int
+    lib.mnl_newton_fit_dp.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, ctypes.POINTER(FitOptions),
+                                      ALLREDUCE_FN, V, V, ctypes.POINTER(I32), ctypes.POINTER(D),
+                                      ctypes.POINTER(FitStats), V]
+    lib.mnl_newton_fit_dp.restype = ctypes.c_int
     lib.mnl_hessvec.argtypes = [I64, I32, I32, I32, I32, V, V, V, V, V, V, V, V]
     lib.mnl_hessvec.restype = ctypes.c_int
     lib.mnl_check_shape.argtypes = [I64, I32, I32, I32, I32]
@@ -279,6 +286,28 @@ def mnl_newton_fit(prob: Problem, coef0=None, tol: float = 1e-6, max_iter: int =
                                     _stream(stream))
     if raise_on_error and rc not in (MNL_OK, MNL_MAXITER):
         raise MnlError(rc, "mnl_newton_fit")
+    return FitResult(coef, it.value, ll.value, rc, st.as_dict())
+
+
+def mnl_newton_fit_dp(prob: Problem, allreduce, coef0=None, tol: float = 1e-6, max_iter: int = 50, stream=None,
+                      raise_on_error: bool = True, ftol: float = 0.0, method: str = "newton",
+                      cg_max_iter: int = 0, cg_rtol: float = 0.0) -> FitResult:
+    """Data-parallel fit (mnl_newton_fit_dp): `prob` holds THIS rank's individuals; `allreduce` is an
+    ALLREDUCE_FN (e.g. distributed.torch_allreduce()) that sums a device buffer across ranks."""
+    torch = _torch()
+    coef = torch.empty(prob.n_p, dtype=torch.float64, device=prob.choice.device)
+    it = ctypes.c_int32(0)
+    ll = ctypes.c_double(0.0)
+    st = FitStats()
+    opts = FitOptions(tol, ftol, max_iter, {"newton": MNL_METHOD_NEWTON, "cg": MNL_METHOD_CG}[method],
+                      cg_max_iter, cg_rtol)
+    X, Y, Z, ch = prob.ptrs()
+    rc = load().mnl_newton_fit_dp(prob.N, prob.K, prob.p, prob.f, prob.d, X, Y, Z, ch,
+                                  coef0.data_ptr() if coef0 is not None else None, ctypes.byref(opts), allreduce,
+                                  None, coef.data_ptr(), ctypes.byref(it), ctypes.byref(ll), ctypes.byref(st),
+                                  _stream(stream))
+    if raise_on_error and rc not in (MNL_OK, MNL_MAXITER):
+        raise MnlError(rc, "mnl_newton_fit_dp")
     return FitResult(coef, it.value, ll.value, rc, st.as_dict())
 
 

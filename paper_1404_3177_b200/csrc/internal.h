@@ -2,9 +2,25 @@
 // (Not part of the ABI; see include/mnl.h.)
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace mnl {
+
+// ---- one-time per-device setup (thread-safe) ----------------------------------------------
+// Kernel attributes set with cudaFuncSetAttribute are per device; f runs once per device for each
+// `mask` (one per call site), under a process-wide lock so no launch can overtake the setter.
+std::mutex& attr_mutex();
+template <class F>
+cudaError_t set_once_per_device(uint64_t& mask, F&& f) {
+  std::lock_guard<std::mutex> lk(attr_mutex());
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if ((mask >> dev) & 1u) return cudaSuccess;
+  const cudaError_t e = f();
+  if (e == cudaSuccess) mask |= uint64_t(1) << dev;
+  return e;
+}
 
 // Problem dimensions and the layout constants derived from them.
 struct Dims {
@@ -81,6 +97,11 @@ cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const doub
                                  bool want_grad, double* grad, double* loglik_out, double* scal,
                                  const int* err, unsigned* counter, cudaStream_t st,
                                  int* status_out = nullptr);
+// Data-parallel exchange of one evaluation: xbuf [2 + n] = [l, bad-choice flag, g] from the
+// finalised scalars [l, ||g||^2, flag] (+ g, or zeros if grad is null); after the all-reduce,
+// grad (if not null) <- the summed g and scal <- [l, ||g||^2, flag] of the sums.
+cudaError_t launch_dp_gather(int n, const double* scal, const double* grad, double* xbuf, cudaStream_t st);
+cudaError_t launch_dp_scatter(int n, const double* xbuf, double* grad, double* scal, cudaStream_t st);
 cudaError_t launch_pack(const Dims& D, const Packed& pk, const double* X, const double* Z,
                         cudaStream_t st);
 cudaError_t launch_axpy_pow2(int n, const double* theta, const double* delta, int j,
@@ -92,7 +113,8 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int device_sms);
 void hess_plan_destroy(HessPlan*);
 size_t hess_plan_bytes(const HessPlan*);
 // Assemble the Hessian from Pr/Xp/Zp (+ Y for the arrow part). sign = +1 writes H,
-// sign = -1 writes -H (the Newton system matrix). out: [n_p][ld_out].
+// sign = -1 writes -H (the Newton system matrix). out: [n_p][ld_out], or with ld_out < 0 the packed
+// upper triangle (row r: columns r..n_p-1 at r n_p - r (r - 1) / 2), the data-parallel exchange.
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y,
                            double* out, int ld_out, double sign, cudaStream_t st);
 // Call after re-packing the design rows (Xp / Zp): invalidates data the plan derived from them.
@@ -105,17 +127,24 @@ cudaError_t launch_sym_pack(int n, const double* H, double* out, cudaStream_t st
 cudaError_t launch_sym_unpack(int n, const double* in, double* H, cudaStream_t st);
 
 // ---- k_chol.cu -------------------------------------------------------------------------
+// Factorisation state (inverse diagonal blocks, grid-barrier words, side stream): one per workspace.
+struct CholCtx;
+CholCtx* chol_ctx_create();
+void chol_ctx_destroy(CholCtx*);
 // In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.
-cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t st);
+cudaError_t launch_cholesky(CholCtx* cc, int n, double* A, int lda, int* info, cudaStream_t st);
 // Factor A in place and solve (L L^T) x = b in the same pass (forward solve fused into the
 // panels, backward solve as one wavefront kernel). x may alias b.
-cudaError_t launch_cholesky_solve_fused(int n, double* A, int lda, int* info, const double* b, double* x,
-                                        cudaStream_t st);
+cudaError_t launch_cholesky_solve_fused(CholCtx* cc, int n, double* A, int lda, int* info, const double* b,
+                                        double* x, cudaStream_t st);
 // se_j = sqrt([(L L^T)^{-1}]_jj) for the factor L in the lower triangle of L (lda); the strict upper
 // triangle of L is overwritten (workspace for the blocks of L^{-1}).
-cudaError_t launch_inv_diag_sqrt(int n, double* L, int lda, double* se, cudaStream_t st);
+cudaError_t launch_inv_diag_sqrt(CholCtx* cc, int n, double* L, int lda, double* se, cudaStream_t st);
+// The Linv blocks of the last factor are reused by launch_chol_solve / launch_inv_diag_sqrt when the
+// same pointer and n come back; chol_forget_factor() drops that association (a caller-supplied L).
+void chol_forget_factor(CholCtx* cc);
 // x = (L L^T)^{-1} b ; x may alias b.
-cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, double* x,
+cudaError_t launch_chol_solve(CholCtx* cc, int n, const double* L, int lda, const double* b, double* x,
                               cudaStream_t st);
 
 }  // namespace mnl

@@ -616,7 +616,10 @@ __global__ void __launch_bounds__(256, 1) k_chol_persist(int n, double* A, int l
   }
 }
 
-struct CholWork {
+}  // namespace
+
+// Per-workspace factorisation state (one per library workspace, i.e. per device and stream).
+struct CholCtx {
   unsigned* bar = nullptr;  // k_chol_persist's grid barrier {count, generation}
   int persist_grid = -1;    // CTAs of the cooperative launch (0: not available)
   double* Linv = nullptr;
@@ -626,10 +629,15 @@ struct CholWork {
   int* flags = nullptr;
   int nflags = 0;
   int epoch = 0;
+  // two-stream lookahead path
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t start = nullptr, done = nullptr;
 };
-CholWork g_cw;
 
-bool ensure_work(int n) {
+namespace {
+
+bool ensure_work(CholCtx& g_cw, int n) {
   const int nblk = (n + NB - 1) / NB;
   const size_t need = (size_t)nblk * NB * NB;
   if (need > g_cw.cap) {
@@ -650,17 +658,17 @@ bool ensure_work(int n) {
 constexpr size_t kDyn = 2 * NB * LDS * sizeof(double);
 constexpr size_t kDynR = 2 * NB * LDR * sizeof(double);
 void set_attrs() {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_mask = 0;
+  set_once_per_device(attr_mask, [] {
     cudaFuncSetAttribute(k_trsm_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
     cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
     cudaFuncSetAttribute(k_trtri_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
-    cudaFuncSetAttribute(k_potrf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
-    attr = true;
-  }
+    cudaFuncSetAttribute(k_chol_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
+    return cudaFuncSetAttribute(k_potrf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
+  });
 }
 
-cudaError_t launch_wave(int n, const double* L, int lda, double* x, int upper, cudaStream_t st) {
+cudaError_t launch_wave(CholCtx& g_cw, int n, const double* L, int lda, double* x, int upper, cudaStream_t st) {
   const int nblk = (n + NB - 1) / NB;
   int epoch = ++g_cw.epoch;
   const double* Linv = g_cw.Linv;
@@ -672,14 +680,7 @@ cudaError_t launch_wave(int n, const double* L, int lda, double* x, int upper, c
   return e;
 }
 
-struct Lookahead {
-  cudaStream_t side = nullptr;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t start = nullptr, done = nullptr;
-};
-Lookahead g_la;
-
-cudaEvent_t la_event(size_t i) {
+cudaEvent_t la_event(CholCtx& g_la, size_t i) {
   while (g_la.ev.size() <= i) {
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -691,7 +692,7 @@ cudaEvent_t la_event(size_t i) {
 // Factorisation with a one-panel lookahead; with x != null also the forward solve x <- L^{-1} x.
 // side stream: [A22 update of the next panel's block column] -> potrf(j+1) -> trsm(j+1)
 // main stream: the rest of panel j's trailing update, concurrently.
-cudaError_t factor_persist(int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
+cudaError_t factor_persist(CholCtx& g_cw, int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
   cudaMemsetAsync(info, 0, sizeof(int), st);
   void* args[] = {(void*)&n, (void*)&A, (void*)&lda, (void*)&g_cw.Linv, (void*)&info, (void*)&x, (void*)&g_cw.bar};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_chol_persist, dim3(g_cw.persist_grid), dim3(256), args,
@@ -703,7 +704,7 @@ cudaError_t factor_persist(int n, double* A, int lda, int* info, double* x, cuda
 }
 
 // CTAs for k_chol_persist: one per SM when the kernel fits there (0 disables the persistent path)
-int persist_grid() {
+int persist_grid(CholCtx& g_cw) {
   if (g_cw.persist_grid >= 0) return g_cw.persist_grid;
   g_cw.persist_grid = 0;
   if (getenv("MNL_CHOL_STREAMS")) return 0;
@@ -711,8 +712,7 @@ int persist_grid() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  if (!coop || cudaFuncSetAttribute(k_chol_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn) != cudaSuccess)
-    return 0;
+  if (!coop) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chol_persist, 256, kDyn) != cudaSuccess || occ < 1) return 0;
   if (cudaMalloc(&g_cw.bar, 2 * sizeof(unsigned)) != cudaSuccess) return 0;
   cudaMemset(g_cw.bar, 0, 2 * sizeof(unsigned));
@@ -720,14 +720,15 @@ int persist_grid() {
   return g_cw.persist_grid;
 }
 
-cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
+cudaError_t factor(CholCtx& g_cw, int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
+  CholCtx& g_la = g_cw;
   set_attrs();
-  if (!ensure_work(n)) return cudaErrorMemoryAllocation;
+  if (!ensure_work(g_cw, n)) return cudaErrorMemoryAllocation;
   // persistent single launch: since the tiles fetch their operands in one round trip it is faster
   // than the two-stream multi-kernel path at every measured n (2816: 1.92 vs 2.36 ms; 5049: 5.35 vs
   // 5.58 ms); MNL_CHOL_STREAMS=1 forces the multi-kernel path, MNL_CHOL_PERSIST_MAX caps n
   static const int persist_max = getenv("MNL_CHOL_PERSIST_MAX") ? atoi(getenv("MNL_CHOL_PERSIST_MAX")) : 16384;
-  if (n <= persist_max && persist_grid() > 1) return factor_persist(n, A, lda, info, x, st);
+  if (n <= persist_max && persist_grid(g_cw) > 1) return factor_persist(g_cw, n, A, lda, info, x, st);
   if (!g_la.side) {
     int lo = 0, hi = 0;  // the panel chain is the critical path: give it the highest priority
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -752,25 +753,25 @@ cudaError_t factor(int n, double* A, int lda, int* info, double* x, cudaStream_t
     }
   };
   panel(0);
-  cudaEventRecord(la_event(2 * 0), sp);  // ev_p(0)
+  cudaEventRecord(la_event(g_la, 2 * 0), sp);  // ev_p(0)
   for (int j = 0; j + 1 < np; ++j) {
     const int j0 = j * NB;
     const int rem = n - j0 - NB;
     const int mt = (rem + NB - 1) / NB;
     // main: rest of panel j's trailing update (tiles with tj >= 1)
-    cudaStreamWaitEvent(st, la_event(2 * j), 0);
+    cudaStreamWaitEvent(st, la_event(g_la, 2 * j), 0);
     if (mt > 1) {
       k_syrk_tiles<<<(mt - 1) * mt / 2, 256, kDyn, st>>>(n, A, lda, j0, 0, 1);
       count_launch();
     }
-    cudaEventRecord(la_event(2 * j + 1), st);  // ev_r(j)
+    cudaEventRecord(la_event(g_la, 2 * j + 1), st);  // ev_r(j)
     // side: next panel's block column, then its factorisation
     k_syrk_tiles<<<mt, 256, kDyn, sp>>>(n, A, lda, j0, 1, 0);
     count_launch();
     panel(j + 1);
-    cudaEventRecord(la_event(2 * (j + 1)), sp);  // ev_p(j+1)
+    cudaEventRecord(la_event(g_la, 2 * (j + 1)), sp);  // ev_p(j+1)
     // the next column update (side, iteration j+1) must follow this rest update (main)
-    cudaStreamWaitEvent(sp, la_event(2 * j + 1), 0);
+    cudaStreamWaitEvent(sp, la_event(g_la, 2 * j + 1), 0);
   }
   cudaEventRecord(g_la.done, sp);
   cudaStreamWaitEvent(st, g_la.done, 0);
@@ -905,40 +906,79 @@ __global__ void __launch_bounds__(256) k_inv_diag(int n, double* A, int lda, con
 
 }  // namespace
 
-cudaError_t launch_cholesky(int n, double* A, int lda, int* info, cudaStream_t st) {
-  return factor(n, A, lda, info, nullptr, st);
+// Kernels that wait on other CTAs of their grid (k_chol_persist's grid barriers, k_trsv_wave's
+// flags) are launched cooperatively; two such grids running at once from different workspaces
+// could each hold part of the SMs and wait forever. Every factor / solve section therefore runs
+// under one process-wide lock and drains its stream before releasing it.
+struct CoopSection {
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  std::lock_guard<std::mutex> lk;
+  cudaStream_t st;
+  explicit CoopSection(cudaStream_t s) : lk(mu()), st(s) {}
+  ~CoopSection() { cudaStreamSynchronize(st); }
+};
+
+CholCtx* chol_ctx_create() { return new CholCtx(); }
+
+void chol_ctx_destroy(CholCtx* c) {
+  if (!c) return;
+  cudaFree(c->bar);
+  cudaFree(c->Linv);
+  cudaFree(c->flags);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->start) cudaEventDestroy(c->start);
+  if (c->done) cudaEventDestroy(c->done);
+  if (c->side) cudaStreamDestroy(c->side);
+  delete c;
 }
 
-cudaError_t launch_cholesky_solve_fused(int n, double* A, int lda, int* info, const double* b, double* x,
-                                        cudaStream_t st) {
+cudaError_t launch_cholesky(CholCtx* cc, int n, double* A, int lda, int* info, cudaStream_t st) {
+  CoopSection cs(st);
+  return factor(*cc, n, A, lda, info, nullptr, st);
+}
+
+cudaError_t launch_cholesky_solve_fused(CholCtx* cc, int n, double* A, int lda, int* info, const double* b,
+                                        double* x, cudaStream_t st) {
+  CoopSection cs(st);
   if (x != b) cudaMemcpyAsync(x, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-  cudaError_t e = factor(n, A, lda, info, x, st);
+  cudaError_t e = factor(*cc, n, A, lda, info, x, st);
   if (e != cudaSuccess) return e;
-  return launch_wave(n, A, lda, x, 1, st);
+  return launch_wave(*cc, n, A, lda, x, 1, st);
 }
 
-cudaError_t launch_inv_diag_sqrt(int n, double* L, int lda, double* se, cudaStream_t st) {
+cudaError_t launch_inv_diag_sqrt(CholCtx* cc, int n, double* L, int lda, double* se, cudaStream_t st) {
+  CholCtx& g_cw = *cc;
   set_attrs();
-  if (!ensure_work(n)) return cudaErrorMemoryAllocation;
+  if (!ensure_work(g_cw, n)) return cudaErrorMemoryAllocation;
   if (g_cw.factor != L || g_cw.factor_n != n) {  // factor from elsewhere: build its Linv blocks
     k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, g_cw.Linv);
     count_launch();
     g_cw.factor = L;
     g_cw.factor_n = n;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
-    attr = true;
-  }
+  static uint64_t attr_mask = 0;
+  set_once_per_device(attr_mask, [] {
+    return cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
+  });
   k_inv_diag<<<(n + NB - 1) / NB, 256, kDyn, st>>>(n, L, lda, g_cw.Linv, se);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, double* x, cudaStream_t st) {
+void chol_forget_factor(CholCtx* cc) {
+  cc->factor = nullptr;
+  cc->factor_n = 0;
+}
+
+cudaError_t launch_chol_solve(CholCtx* cc, int n, const double* L, int lda, const double* b, double* x,
+                              cudaStream_t st) {
+  CoopSection cs(st);
+  CholCtx& g_cw = *cc;
   set_attrs();
-  if (!ensure_work(n)) return cudaErrorMemoryAllocation;
+  if (!ensure_work(g_cw, n)) return cudaErrorMemoryAllocation;
   if (g_cw.factor != L || g_cw.factor_n != n) {  // factor from elsewhere: build its Linv blocks
     k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, g_cw.Linv);
     count_launch();
@@ -946,9 +986,9 @@ cudaError_t launch_chol_solve(int n, const double* L, int lda, const double* b, 
     g_cw.factor_n = n;
   }
   if (x != b) cudaMemcpyAsync(x, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-  cudaError_t e = launch_wave(n, L, lda, x, 0, st);
+  cudaError_t e = launch_wave(g_cw, n, L, lda, x, 0, st);
   if (e != cudaSuccess) return e;
-  return launch_wave(n, L, lda, x, 1, st);
+  return launch_wave(g_cw, n, L, lda, x, 1, st);
 }
 
 }  // namespace mnl

@@ -1398,13 +1398,12 @@ __global__ void k_axpy_pow2(int n, const double* theta, const double* delta, int
 
 template <int KPL, int CM, bool HV, bool YZS>
 cudaError_t launch_k(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_kernel<KPL, CM, HV, YZS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static uint64_t attr_mask = 0;
+  cudaError_t e = set_once_per_device(attr_mask, [] {
+    return cudaFuncSetAttribute(k_eval_kernel<KPL, CM, HV, YZS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024);
+  });
+  if (e != cudaSuccess) return e;
   k_eval_kernel<KPL, CM, HV, YZS><<<plan.grid, plan.block, plan.smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
@@ -1457,7 +1456,46 @@ __global__ void __launch_bounds__(1024) k_cg_dir(int n, double beta, const doubl
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = fma(beta, p[i], r[i]);
 }
 
+// ---- the data-parallel exchange of one evaluation ----------------------------
+// xbuf = [l, bad-choice flag, g (n)] from this rank's finalised scalars [l, ||g||^2, flag] and g
+__global__ void __launch_bounds__(1024) k_dp_gather(int n, const double* scal, const double* grad, double* xbuf) {
+  if (threadIdx.x == 0) {
+    xbuf[0] = scal[0];
+    xbuf[1] = scal[2];
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xbuf[2 + i] = grad ? grad[i] : 0.0;
+}
+
+// after the all-reduce (sums over ranks): g <- xbuf[2..], scal <- [l, ||g||^2 (fixed order), flag]
+__global__ void __launch_bounds__(1024) k_dp_scatter(int n, const double* xbuf, double* grad, double* scal) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double g = xbuf[2 + i];
+    if (grad) grad[i] = g;
+    s = fma(g, g, s);
+  }
+  s = cta_sum(s, red);
+  if (threadIdx.x == 0) {
+    scal[0] = xbuf[0];
+    scal[1] = s;
+    scal[2] = xbuf[1];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_dp_gather(int n, const double* scal, const double* grad, double* xbuf, cudaStream_t st) {
+  k_dp_gather<<<1, 1024, 0, st>>>(n, scal, grad, xbuf);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dp_scatter(int n, const double* xbuf, double* grad, double* scal, cudaStream_t st) {
+  k_dp_scatter<<<1, 1024, 0, st>>>(n, xbuf, grad, scal);
+  count_launch();
+  return cudaGetLastError();
+}
 
 static int eval_qp(const Dims& D) { return (D.q + 3) / 4 * 4; }
 static int eval_xs(const Dims& D) { return pad4mod16(eval_qp(D)); }

@@ -718,7 +718,7 @@ struct AsmArgs {
   int ld2b, n2a;
   const double* T;   // [K][E][F]         (reduced)
   double* out;
-  int ld_out;
+  int ld_out;        // < 0: out is the packed upper triangle (row r: columns r..n_p-1)
   double sign;
 };
 
@@ -733,6 +733,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n_p * n_p;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e / n_p), c = (int)(e - (int64_t)r * n_p);
+    if (A.ld_out < 0 && c < r) continue;
     double negH;
     if (r < A.n_beta && c < A.n_beta) {
       int k1 = r / q, a1 = r - k1 * q, k2 = c / q, a2 = c - k2 * q;  // 0-based k-1
@@ -770,7 +771,8 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
       }
       negH = tv - u;
     }
-    A.out[(int64_t)r * A.ld_out + c] = -A.sign * negH;
+    const int64_t o = A.ld_out < 0 ? (int64_t)r * n_p - (int64_t)r * (r - 1) / 2 + (c - r) : (int64_t)r * A.ld_out + c;
+    A.out[o] = -A.sign * negH;
   }
 }
 
@@ -852,7 +854,6 @@ static int choose_splits(int tiles, int64_t nchunks, int sms, int min_chunks) {
 // padded width (wider tiles reuse each generated operand more; measured equal time on c4 for
 // 128 vs 96).
 static int choose_bn(int MB) {
-  if (const char* e = getenv("MNL_FORCE_BN")) return atoi(e);  // experiments only
   int64_t min_pad = -1;
   for (int bn : {128, 96, 64}) {
     const int64_t pad = (int64_t)(MB + bn - 1) / bn * bn;
@@ -868,14 +869,13 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
                       bool pipe = false) {
   J.BN = BN;
   J.KC = KC;
-  J.nwarp = (BN == 64 && getenv("MNL_J1_NWARP4")) ? 4 : 8;  // experiments: two 4-warp CTAs per SM
-  if (BN == 128 && J.agen && getenv("MNL_J1_NWARP16")) J.nwarp = 16;  // experiments: 16 warps, 32x32 tiles
+  J.nwarp = 8;
   J.MA = (int)A.size();
   J.MB = (int)B.size();
   J.tilesM = (J.MA + BM - 1) / BM;
   J.tilesN = (J.MB + BN - 1) / BN;
   J.nchunks = pk.Npad / KC;
-  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms * (J.nwarp < 8 ? 8 / J.nwarp : 1), 4);
+  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms, 4);
   J.ldc = J.tilesN * BN;
   J.split_stride = (int64_t)J.tilesM * BM * J.ldc;
   J.nseg = nseg;
@@ -900,7 +900,7 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
   *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
   if (pipe) return true;  // k_pipe_gemm: no generator staging
-  const size_t lim = J.nwarp == 4 ? 112 * 1024 : 220 * 1024;
+  const size_t lim = 220 * 1024;
   for (J.nraw = 2; J.nraw >= 1; --J.nraw) {  // prefer two raw stages; one if the stage is large
     J.smem = (size_t)(2 * (KC / 4) * 8 * 64 + 2 * (KC / 4) * (BN / 16) * 64 + J.nraw * J.stage_doubles) *
              sizeof(double);
@@ -1195,13 +1195,12 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.bfrag = J.bfrag;
   P.counter = counter;
   P.skip_off = J.skip_off;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP, AGEN, BPRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr_mask = 0;
+  cudaError_t e = set_once_per_device(attr_mask, [] {
+    return cudaFuncSetAttribute(k_gen_gemm<BN, KC, NWARP, AGEN, BPRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                220 * 1024);
+  });
+  if (e != cudaSuccess) return e;
   const int items = J.tilesM * J.tilesN * J.splits;
   const int grid = std::min(items, sms * (NWARP < 8 ? 8 / NWARP : 1));
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
@@ -1225,12 +1224,11 @@ static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaSt
   P.bfrag = J.bfrag;
   P.counter = counter;
   P.skip_off = J.skip_off;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pipe_gemm<BN, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static uint64_t attr_mask = 0;
+  cudaError_t e = set_once_per_device(attr_mask, [smem] {
+    return cudaFuncSetAttribute(k_pipe_gemm<BN, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   const int items = J.tilesM * J.tilesN * J.splits;
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
   k_pipe_gemm<BN, KC, S><<<std::min(items, sms), 8 * 32 + 32, smem, st>>>(P, J.afrag);
@@ -1248,9 +1246,7 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
     else if (J.BN == 64) e = run_pipe<64>(J, counter, sms, st);
     else e = run_pipe<48>(J, counter, sms, st);
   } else if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
-    if (J.nwarp == 4) e = J.KC == 32 ? run_gemm<64, 32, 4, true>(J, pk, counter, sms, st) : run_gemm<64, 16, 4, true>(J, pk, counter, sms, st);
-    else if (J.nwarp == 16) e = J.KC == 32 ? run_gemm<128, 32, 16, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 16, true>(J, pk, counter, sms, st);
-    else if (J.BN == 128 && J.mat_b) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
+    if (J.BN == 128 && J.mat_b) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true>(J, pk, counter, sms, st);
     else if (J.BN == 96 && J.mat_b) e = J.KC == 32 ? run_gemm<96, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, true>(J, pk, counter, sms, st);
@@ -1303,11 +1299,10 @@ static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStr
     F.seg_off[sg] = off;
     off += J.KC * F.seg_ld[sg];
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFragSmemMax);
-    attr = true;
-  }
+  static uint64_t attr_mask = 0;
+  set_once_per_device(attr_mask, [] {
+    return cudaFuncSetAttribute(k_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFragSmemMax);
+  });
   F.nh = frag_nh((size_t)off);  // > 0: the plan materialises only operands whose stage fits
   k_frag<<<(unsigned)(F.nh * J.nchunks), 256, (size_t)off / F.nh * sizeof(double), st>>>(F);
   count_launch();
@@ -1357,11 +1352,10 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
       const int64_t tstride = ((int64_t)D.K * E * F + 1) / 2 * 2;
 #define MNL_ARROW(MT_, NT_)                                                                                  \
   do {                                                                                                       \
-    static bool attr_ = false;                                                                               \
-    if (!attr_) {                                                                                            \
-      cudaFuncSetAttribute(k_arrow<MT_, NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);      \
-      attr_ = true;                                                                                          \
-    }                                                                                                        \
+    static uint64_t attr_mask_ = 0;                                                                          \
+    set_once_per_device(attr_mask_, [] {                                                                     \
+      return cudaFuncSetAttribute(k_arrow<MT_, NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+    });                                                                                                      \
     k_arrow<MT_, NT_><<<items, 256, (size_t)2 * hp->ar_ci * hp->ar_rs * sizeof(double), st>>>(               \
         D.N, D.K, D.q, D.d, D.f, hp->ar_splits, pk.Npad, hp->ar_ep, hp->ar_fp, hp->ar_ci, hp->ar_rs, pk.Pr,   \
         pk.ldP, pk.Xp, pk.ldX, pk.Zp, pk.ldZ, Y, hp->Tpart, tstride);                                        \

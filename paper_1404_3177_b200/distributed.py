@@ -1,27 +1,27 @@
-"""Data-parallel Newton-Raphson over individuals (NEXT item f3).
+"""Data-parallel Newton-Raphson over individuals (§8(f) f3).
 
-The log-likelihood, gradient and Hessian are sums over individuals, so
-each rank owns a contiguous slice of the individuals, evaluates its partial (l_r, g_r, H_r) with the
-single-GPU kernels, and ONE all-reduce (sum) of [l, g, packed upper triangle of H] per iteration
-forms (l, g, H) on every rank.  Every
-rank then factors the same -H and takes the same step (all-reduce results are identical on all
-ranks), so the iterates stay bitwise identical without broadcasting the coefficients.  Each
-line-search trial needs one scalar all-reduce.
+The log-likelihood, gradient and Hessian are sums over individuals (P:348-351, P:435-443,
+P:462-476), so each rank owns a contiguous slice of the individuals and calls the library's
+data-parallel fit (`mnl_newton_fit_dp`, include/mnl.h) on it. The Newton-Raphson driver itself is
+the library's (csrc/nr_driver.h, the same code as the single-GPU fit); at each exchange step it calls
+back into an all-reduce that sums a DEVICE buffer across ranks:
+  after every pass-1 evaluation   [l, bad-choice flag, g]        n_p + 2 doubles
+  after every Hessian             packed upper triangle of -H    n_p (n_p + 1) / 2 doubles
+All-reduce results are identical on every rank, so every rank factors the same -H and takes the
+same step; the iterates stay bitwise identical without broadcasting the coefficients.
 
-The driver is written against three callables so the host logic is testable on CPU with gloo:
-  evaluate(theta, want_grad, want_hess) -> (l, g, H)   local sums (tensors; g, H may be None)
-  all_reduce(tensor)                                    in-place sum over ranks
-  solve(A, g) -> (status, delta)                        delta = A^{-1} g for the SPD A = -H
-The step control is the same as mnl_newton_fit (include/mnl.h, readings R7-R11).
+This module is argument marshalling only: the shard range, a torch.distributed (NCCL) all-reduce
+callback over a raw device pointer, and the binding of the host-callback build of the same driver
+(libnrhost.so) that tests/test_distributed.py runs on CPU with gloo.
 """
 from __future__ import annotations
 
-import math
-from dataclasses import dataclass, field
+import ctypes
+import os
 
-MNL_OK, MNL_ERR_ARG, MNL_ERR_CUDA, MNL_ERR_NOT_SPD, MNL_ERR_LINESEARCH, MNL_ERR_NONFINITE, MNL_MAXITER = range(7)
-MAX_HALVINGS = 30
-TAU_REL = 1e-12
+from . import ALLREDUCE_FN, LIB_PATH, load, mnl_newton_fit_dp  # noqa: F401
+
+HOST_LIB = os.path.join(os.path.dirname(LIB_PATH), "libnrhost.so")
 
 
 def shard_range(N: int, world: int, rank: int) -> tuple[int, int]:
@@ -31,130 +31,117 @@ def shard_range(N: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < rem else 0)
 
 
-@dataclass
-class DPFit:
-    status: int = MNL_OK
-    iters: int = 0
-    loglik: float = float("nan")
-    grad_norm: float = float("nan")
-    coef: object = None
-    halvings: list = field(default_factory=list)
+class _CudaArray:
+    """A raw device pointer as a __cuda_array_interface__ object (torch.as_tensor wraps it, no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
 
 
-def torch_packer():
-    """(pack, unpack) of the upper triangle with torch indexing (host-logic tests on CPU)."""
+def device_view(ptr: int, count: int):
+    """The library's device buffer [count] float64 as a torch tensor (shares memory)."""
     import torch
-
-    cache = {}
-
-    def idx(n, dev):
-        if (n, dev) not in cache:
-            cache[(n, dev)] = torch.triu_indices(n, n, device=dev)
-        return cache[(n, dev)]
-
-    def pack(H):
-        iu = idx(H.shape[0], H.device)
-        return H[iu[0], iu[1]]
-
-    def unpack(v, n):
-        iu = idx(n, v.device)
-        H = torch.empty(n, n, dtype=v.dtype, device=v.device)
-        H[iu[0], iu[1]] = v
-        H[iu[1], iu[0]] = v
-        return H
-
-    return pack, unpack
+    return torch.as_tensor(_CudaArray(ptr, count), device="cuda")
 
 
-def newton_fit_dp(evaluate, all_reduce, solve, theta0, tol: float = 1e-6, max_iter: int = 50,
-                  packer=None) -> DPFit:
-    """Newton-Raphson with step halving on data sharded over ranks (identical on every rank).
-    With `packer` = (pack, unpack) the Hessian evaluation exchanges ONE buffer [l, g, upper
-    triangle of H] (n_p + 1 + n_p (n_p + 1) / 2 doubles, half the bytes of the full matrix);
-    without it, [l, g] and the full H in two all-reduces."""
+def torch_stream(stream_ptr):
     import torch
-
-    theta = theta0.clone()
-    fit = DPFit()
-
-    def reduced(th, want_hess):
-        l, g, H = evaluate(th, True, want_hess)
-        n = g.shape[0]
-        if H is not None and packer is not None:
-            buf = torch.cat([l.reshape(1).to(g.dtype), g, packer[0](H)])
-            all_reduce(buf)
-            return float(buf[0].item()), buf[1:n + 1], packer[1](buf[n + 1:], n)
-        lg = torch.cat([l.reshape(1).to(g.dtype), g])
-        all_reduce(lg)
-        if H is not None:
-            all_reduce(H)
-        return float(lg[0].item()), lg[1:], H
-
-    l, g, _ = reduced(theta, False)
-    while True:
-        if not math.isfinite(l):
-            fit.status = MNL_ERR_NONFINITE
-            break
-        gnorm = float(torch.sqrt(torch.sum(g * g)).item())
-        fit.loglik, fit.grad_norm = l, gnorm
-        if gnorm < tol:
-            fit.status = MNL_OK
-            break
-        if fit.iters == max_iter:
-            fit.status = MNL_MAXITER
-            break
-        _, _, H = reduced(theta, True)   # the Hessian of the summed problem at theta
-        status, delta = solve(-H, g)
-        if status != MNL_OK:
-            fit.status = status
-            break
-        tau = TAU_REL * max(1.0, abs(l))
-        accepted = False
-        for j in range(MAX_HALVINGS + 1):
-            trial = theta + torch.ldexp(delta, torch.tensor(-j, dtype=torch.int32, device=delta.device))
-            lj, gj, _ = reduced(trial, False)
-            if math.isfinite(lj) and lj >= l - tau:
-                accepted = True
-                break
-        if not accepted:
-            fit.status = MNL_ERR_LINESEARCH
-            break
-        fit.halvings.append(j)
-        theta, l, g = trial, lj, gj
-        fit.iters += 1
-    fit.coef = theta
-    return fit
+    return torch.cuda.ExternalStream(stream_ptr) if stream_ptr else torch.cuda.default_stream()
 
 
-def cuda_evaluator(prob):
-    """evaluate() over this rank's device-resident slice, through the C ABI (mnl_eval)."""
-    from . import mnl_eval
+def torch_allreduce(group=None):
+    """ALLREDUCE_FN summing the buffer over `group` with torch.distributed (NCCL), ordered on the
+    library's stream. Keep the returned object alive for the duration of the fit."""
+    import torch
+    import torch.distributed as dist
 
-    def evaluate(theta, want_grad, want_hess):
-        return mnl_eval(prob, theta, grad=True, hess=want_hess)
+    def cb(buf, count, stream, ctx):
+        try:
+            t = device_view(buf, count)
+            with torch.cuda.stream(torch_stream(stream)):
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed exchange
+            return 1
 
-    return evaluate
-
-
-def cuda_packer():
-    """(pack, unpack) with the library's kernels (mnl_sym_pack / mnl_sym_unpack)."""
-    from . import mnl_sym_pack, mnl_sym_unpack
-
-    def unpack(v, n):
-        return mnl_sym_unpack(v.contiguous(), n)
-
-    return (lambda H: mnl_sym_pack(H.contiguous())), unpack
+    return ALLREDUCE_FN(cb)
 
 
-def cuda_solver():
-    """solve() with the library's Cholesky factor and triangular solves (mnl_cholesky[_solve])."""
-    from . import MNL_OK as OK, mnl_cholesky, mnl_cholesky_solve
+def newton_fit_dp(prob_local, group=None, **kw):
+    """mnl_newton_fit_dp on this rank's shard with the torch.distributed all-reduce."""
+    fn = torch_allreduce(group)
+    return mnl_newton_fit_dp(prob_local, fn, **kw)
 
-    def solve(A, g):
-        A = A.contiguous()
-        rc = mnl_cholesky(A)
-        if rc != OK:
-            return rc, None
-        return OK, mnl_cholesky_solve(A, g.contiguous())
 
-    return solve
+# ---- the same driver over host callbacks (libnrhost.so; CPU tests) ------------------------------
+
+EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                           ctypes.POINTER(ctypes.c_double))
+DIR_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int))
+TRIAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                            ctypes.POINTER(ctypes.c_double))
+ACCEPT_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
+
+
+class HostOps(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("eval_theta", EVAL_FN), ("direction", DIR_FN),
+                ("eval_trial", TRIAL_FN), ("accept", ACCEPT_FN)]
+
+
+class HostReport(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("halvings", ctypes.c_int32), ("evals", ctypes.c_int32),
+                ("status", ctypes.c_int32), ("stop_reason", ctypes.c_int32),
+                ("halvings_per_iter", ctypes.c_int32 * 64), ("loglik", ctypes.c_double),
+                ("grad_norm", ctypes.c_double), ("delta_loglik", ctypes.c_double), ("min_margin", ctypes.c_double)]
+
+
+_host = None
+
+
+def _host_lib():
+    global _host
+    if _host is None:
+        if not os.path.exists(HOST_LIB):
+            from . import build as _b
+            _b.build_host()
+        _host = ctypes.CDLL(HOST_LIB)
+        _host.nr_fit_host.argtypes = [ctypes.POINTER(HostOps), ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                      ctypes.POINTER(HostReport)]
+        _host.nr_fit_host.restype = ctypes.c_int
+    return _host
+
+
+def run_host_driver(eval_theta, direction, eval_trial, accept, gtol=1e-6, ftol=0.0, max_iter=50) -> dict:
+    """The library's Newton-Raphson driver (nr_driver.h) over Python callables:
+      eval_theta() -> (status, l, ||g||^2)        at the current iterate
+      direction() -> (status, not_spd)            the Newton direction there
+      eval_trial(j) -> (status, l, ||g||^2)       at theta + delta / 2^j
+      accept()                                    theta <- the last trial
+    Returns the driver's report as a dict."""
+
+    def _e(ctx, l, g2):
+        rc, lv, gv = eval_theta()
+        l[0], g2[0] = lv, gv
+        return rc
+
+    def _d(ctx, ns):
+        rc, bad = direction()
+        ns[0] = int(bool(bad))
+        return rc
+
+    def _t(ctx, j, l, g2):
+        rc, lv, gv = eval_trial(j)
+        l[0], g2[0] = lv, gv
+        return rc
+
+    def _a(ctx):
+        accept()
+
+    ops = HostOps(None, EVAL_FN(_e), DIR_FN(_d), TRIAL_FN(_t), ACCEPT_FN(_a))
+    rep = HostReport()
+    rc = _host_lib().nr_fit_host(ctypes.byref(ops), gtol, ftol, max_iter, ctypes.byref(rep))
+    out = {k: getattr(rep, k) for k, _ in HostReport._fields_ if k != "halvings_per_iter"}
+    out["halvings_per_iter"] = list(rep.halvings_per_iter[:min(rep.iters, 64)])
+    out["rc"] = rc
+    return out

@@ -97,6 +97,16 @@ def test_argument_errors_are_reported_without_a_device(lib):
     opts = M.FitOptions(0.0, 0.0, 5, 0, 0, 0.0)  # gtol <= 0
     assert lib.mnl_newton_fit_opts(10, 4, 2, 0, 0, fake, None, None, fake, None, ctypes.byref(opts), fake,
                                    ctypes.byref(it), ctypes.byref(ll), None, None) == M.MNL_ERR_ARG
+    # the data-parallel fit: an all-reduce callback is required; options are validated the same way
+    good = M.FitOptions(1e-6, 0.0, 5, 0, 0, 0.0)
+    noop = M.ALLREDUCE_FN(lambda buf, n, st, ctx: 0)
+    assert lib.mnl_newton_fit_dp(10, 4, 2, 0, 0, fake, None, None, fake, None, ctypes.byref(good),
+                                 M.ALLREDUCE_FN(), None, fake, ctypes.byref(it), ctypes.byref(ll), None,
+                                 None) == M.MNL_ERR_ARG
+    assert lib.mnl_newton_fit_dp(10, 4, 2, 0, 0, fake, None, None, fake, None, ctypes.byref(opts), noop, None,
+                                 fake, ctypes.byref(it), ctypes.byref(ll), None, None) == M.MNL_ERR_ARG
+    assert lib.mnl_newton_fit_dp(10, 1, 2, 0, 0, fake, None, None, fake, None, ctypes.byref(good), noop, None,
+                                 fake, ctypes.byref(it), ctypes.byref(ll), None, None) == M.MNL_ERR_ARG
 
 
 def test_library_is_sm100a_only():
