@@ -251,6 +251,11 @@ int mnl_newton_fit_host(int64_t N, int32_t K, int32_t p, int32_t f, int32_t d,
 int mnl_cholesky(int32_t n, double* A, void* stream);
 /* Solve (L L^T) x = b given the factor from mnl_cholesky; b and x dev [n], may alias. */
 int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, void* stream);
+/* Solve A x = b for the SPD dev [n][n] row-major A (lower triangle read; A is NOT modified) by the
+ * Newton step's own path (row a6): the tile-DAG factorisation with the forward solve
+ * fused into its diagonal tiles, then the backward wavefront (one kernel for n <= 64). b and x dev
+ * [n], may alias. MNL_ERR_NOT_SPD if a pivot is <= 0 or NaN (x is then undefined). */
+int mnl_spd_solve(int32_t n, const double* A, const double* b, double* x, void* stream);
 
 /* Packed upper triangle of a symmetric dev [n][n] row-major matrix: packed[off(i) + j - i] =
  * H[i][j] for j >= i, off(i) = i n - i (i - 1) / 2 (n (n + 1) / 2 doubles), and back (both

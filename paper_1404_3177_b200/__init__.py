@@ -117,6 +117,8 @@ def load(build_if_missing: bool = False):
     lib.mnl_cholesky.restype = ctypes.c_int
     lib.mnl_cholesky_solve.argtypes = [I32, V, V, V, V]
     lib.mnl_cholesky_solve.restype = ctypes.c_int
+    lib.mnl_spd_solve.argtypes = [I32, V, V, V, V]
+    lib.mnl_spd_solve.restype = ctypes.c_int
     lib.mnl_last_launch_count.argtypes = []
     lib.mnl_last_launch_count.restype = I64
     lib.mnl_status_string.argtypes = [ctypes.c_int]
@@ -381,6 +383,17 @@ def mnl_cholesky_solve(L, b, stream=None):
     rc = load().mnl_cholesky_solve(L.shape[0], L.data_ptr(), b.data_ptr(), x.data_ptr(), _stream(stream))
     if rc != MNL_OK:
         raise MnlError(rc, "mnl_cholesky_solve")
+    return x
+
+
+def mnl_spd_solve(A, b, stream=None):
+    """x = A^{-1} b for the SPD CUDA float64 [n, n] tensor A (not modified): the Newton step's fused
+    factor + solve path. Raises MnlError (MNL_ERR_NOT_SPD) if A is not positive definite."""
+    torch = _torch()
+    x = torch.empty_like(b)
+    rc = load().mnl_spd_solve(A.shape[0], A.data_ptr(), b.data_ptr(), x.data_ptr(), _stream(stream))
+    if rc != MNL_OK:
+        raise MnlError(rc, "mnl_spd_solve")
     return x
 
 

@@ -41,16 +41,45 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", OUT, *[os.path.join(CSRC, s) for s in SOURCES]]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel, then one link (no cross-unit device code)
+    objdir = os.path.join(HERE, "lib", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    jobs, text = [], ""
+    hdrs = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "nr_driver.h"),
+            os.path.join(HERE, "..", "include", "mnl.h")]
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *cflags, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if not force and os.path.exists(obj) and all(
+                os.path.getmtime(obj) > os.path.getmtime(p) for p in [os.path.join(CSRC, src), *hdrs]):
+            jobs.append((cmd, obj, None))  # up to date
+            continue
+        jobs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    failed = False
+    for cmd, _, pr in jobs:
+        if pr is None:
+            continue
+        out, err = pr.communicate()
+        text += " ".join(cmd) + "\n" + out + err
+        failed |= pr.returncode != 0
     log = os.path.join(HERE, "lib", "build.log")
+    if not failed:
+        tmp = OUT + f".tmp{os.getpid()}"
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp,
+               *[obj for _, obj, _ in jobs]]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        text += " ".join(cmd) + "\n" + r.stdout + r.stderr
+        failed = r.returncode != 0
+        if not failed:
+            os.replace(tmp, OUT)
     with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed ({r.returncode}); see {log}")
+        fh.write(text)
+    if failed:
+        sys.stderr.write(text[-20000:])
+        raise RuntimeError(f"nvcc failed; see {log}")
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(text)
     return OUT
 
 

@@ -1,18 +1,24 @@
-// Newton step: -H = L L^T by a blocked right-looking Cholesky
-// factorisation, then L y = g and L^T delta = y (Eq. "NR update": delta = -H^{-1} g;
-// -H is positive definite by global concavity).
+// Newton step: -H = L L^T by a tiled Cholesky factorisation, then
+// L y = g and L^T delta = y (Eq. "NR update": delta = -H^{-1} g; -H is positive definite
+// by global concavity).
 //
-// Per panel j of NB = 64 columns:
-//   k_potrf_inv   one CTA: Cholesky of the diagonal block in shared memory, fused with the
-//                 inverse of its triangular factor (kept in a workspace, Linv[j]) and, in the
-//                 fused factor+solve, the forward-solve piece y_j = Linv[j] b_j;
-//   k_trsm_gemm   L21 = A21 Linv[j]^T as a DMMA product (one CTA per 64 rows), fused with the
-//                 forward-solve update b_r -= L21_r y_j of its rows;
-//   k_syrk_tiles  A22 -= L21 L21^T, one CTA per 64x64 lower tile (DMMA, mma.sync m8n8k4 f64).
-// The backward solve L^T x = y is one cooperative wavefront kernel: CTA b owns block b, folds in
-// the already-solved blocks as their flags are published, and applies Linv[b]^T (no per-block
-// launches).  The standalone solve (mnl_cholesky_solve) runs the same wavefront forward too.
-// The matrix is row-major with leading dimension lda; only the lower triangle is referenced.
+// k_chol_dag: ONE persistent cooperative kernel, no grid barriers. The lower triangle is cut into
+// 64 x 64 tiles and every tile (i, j), i >= j, is one task, left-looking:
+//     C = A_ij - sum_{k<j} L_ik L_jk^T                       (DMMA, accumulators in registers)
+//     i == j:  L_jj = chol(C) and Linv_j = L_jj^{-1} in shared memory; y_j = Linv_j (b_j - sum_k L_jk y_k)
+//     i >  j:  L_ij = C Linv_j^T                             (DMMA)
+// Tasks are dealt to the CTAs round-robin in column-major order (a topological order of the
+// tile DAG), each CTA runs its tasks in order, and a task waits only for the tiles it reads: one
+// flag per tile (release / acquire, tagged with a per-call epoch). The operands (L_ik, L_jk, and
+// y_k for the diagonal tasks) come from a tile-major copy of L written by the tasks themselves
+// (padded rows of 68 doubles: conflict-free fragment loads), by cp.async.bulk into a two-stage
+// mbarrier ring, so the tile of step k + 1 is in flight while step k multiplies. Every A_ij is read
+// once (row-major, by its own task) and every L_ij written once: the HBM traffic is that of the
+// matrix, not one rewrite of the trailing matrix per panel. The critical path is one chain per
+// tile column (last update, potrf, trsm), not three grid-wide barriers per panel.
+// With a single tile (n <= 64) the backward solve runs in the same task; otherwise it is one
+// cooperative wavefront kernel (k_trsv_wave: CTA b owns block b and folds in the solved blocks as
+// their flags are published).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -26,6 +32,10 @@ namespace {
 constexpr int NB = 64;
 constexpr int LDS = NB + 4;  // 68 = 4 (mod 16) doubles: conflict-free 8x4 fragment gathers
 constexpr int LDR = NB + 1;  // row-per-thread access patterns
+constexpr int TS = NB * LDS; // doubles per stored tile (tile-major L, padded Linv)
+
+// offset of tile (i, j), i >= j, in the tile-major packed lower triangle
+__host__ __device__ __forceinline__ int64_t tile_off(int i, int j) { return ((int64_t)i * (i + 1) / 2 + j) * TS; }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -49,119 +59,101 @@ __device__ __forceinline__ void smem_gemm(double* out, int lo, const double* Am,
   }
 }
 
-// k_potrf_inv: Cholesky of the jb x jb diagonal block fused with X = L^{-1}, blocked by 16:
-// for each 16-column sub-panel: (1) the 16 x 16 diagonal block and its inverse by the whole CTA
-// (one thread per entry), (2) L21 = A21 X11^T, (3) A22 -= L21 L21^T on DMMA by all warps;
-// finally the off-diagonal blocks of X = L^{-1} on DMMA. With x != null it also applies the
-// forward-solve piece y_j = Linv b_j (b_j already holds every earlier panel's update).
+// potrf_core: Cholesky of the jb x jb block in S (shared, LDR rows: the lower triangle, identity
+// beyond jb) fused with X = L^{-1}, by 16-column sub-panels (only those below jb): (1) warp 0
+// factors and inverts the 16 x 16 diagonal block (lane r owns row r of the block in registers; one
+// shared-memory broadcast per column; unscaled right-looking updates a_rk -= a_rc a_kc / a_cc, the
+// scaling by 1 / sqrt(a_cc) applied once at the end; then lane r solves for column r of L^{-1}),
+// (2) L21 = A21 X11^T and (3) A22 -= L21 L21^T on DMMA by all warps; finally (4) the off-diagonal
+// blocks of X on DMMA. S <- L (strict upper zeroed), X <- L^{-1}; returns (in thread 0) whether a
+// pivot was not positive (it is replaced by 1 to keep the values finite). Rows / columns >= jb of S
+// and X are left undefined when jb < 64 (callers mask them).
 constexpr int SB = 16;
-__device__ __noinline__ void potrf_block(int n, double* A, int lda, int j0, double* Linv, int* info, double* x,
-                                         double* dsm) {
-  __syncthreads();  // the CTA may have used dsm for another step just before
+
+// warp 0: the 16 x 16 diagonal block at (c0, c0): S <- L, X <- L^{-1}. Lanes 16..31 mirror 0..15.
+// colb: shared [SB] (the broadcast column).
+__device__ __forceinline__ bool potrf16_warp(double (*S)[LDR], double (*X)[LDR], int c0, double* colb) {
+  const int lane = threadIdx.x & 31, r = lane & 15;
+  double a[SB], rsv[SB];
+#pragma unroll
+  for (int c = 0; c < SB; ++c) a[c] = (c <= r) ? S[c0 + r][c0 + c] : 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < SB; ++c) {
+    if (lane < SB) colb[lane] = a[c];  // column c (rows >= c are current)
+    __syncwarp();
+    double d = colb[c];
+    const bool b = !(d > 0.0) || !isfinite(d);
+    bad |= b;
+    if (b) d = 1.0;
+    const double rs = rsqrt(d);
+    rsv[c] = rs;
+    const double f = a[c] * (rs * rs);  // a_rc / a_cc
+#pragma unroll
+    for (int k = c + 1; k < SB; ++k)
+      if (r >= k) a[k] = fma(-f, colb[k], a[k]);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int c = 0; c < SB; ++c) a[c] = (c <= r) ? a[c] * rsv[c] : 0.0;  // L_rc = a_rc / sqrt(a_cc)
+  if (lane < SB) {
+#pragma unroll
+    for (int c = 0; c < SB; ++c) S[c0 + r][c0 + c] = a[c];
+  }
+  __syncwarp();
+  double x[SB];  // column r of L^{-1}: x_t = (delta_tr - sum_{s<t} L_ts x_s) / L_tt, right-looking
+#pragma unroll
+  for (int t = 0; t < SB; ++t) x[t] = (t == r) ? 1.0 : 0.0;
+#pragma unroll
+  for (int t = 0; t < SB; ++t) {
+    x[t] *= rsv[t];
+#pragma unroll
+    for (int u = t + 1; u < SB; ++u) x[u] = fma(-S[c0 + u][c0 + t], x[t], x[u]);
+  }
+  if (lane < SB) {
+#pragma unroll
+    for (int t = 0; t < SB; ++t) X[c0 + t][c0 + r] = x[t];
+  }
+  return bad;
+}
+
+__device__ __noinline__ bool potrf_core(int jb, double* dsm) {
   double(*S)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm);
   double(*X)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + NB * LDR);
   __shared__ double T[NB][SB + 1];
-  __shared__ double bv[NB];
-  __shared__ double colb[2][SB], xrow[2][SB], pv16[SB];
-  const int jb = min(NB, n - j0);
+  __shared__ double colb[SB];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  {  // all 16 loads of a thread in flight at once (clamped addresses, masked values)
-    double v[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      const int rr = r < jb ? r : jb - 1, ccl = c < jb ? c : jb - 1;
-      v[m] = __ldcg(A + (int64_t)(j0 + rr) * lda + j0 + ccl);  // L2: other CTAs updated it
-    }
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      // rows / columns beyond jb: identity (keeps the blocked steps well defined; never written back)
-      S[r][c] = (r < jb && c <= r) ? v[m] : (r == c ? 1.0 : 0.0);
-      X[r][c] = 0.0;
-    }
-  }
-  if (x && tid < NB) bv[tid] = tid < jb ? __ldcg(x + j0 + tid) : 0.0;
+  const int lr = lane >> 2, lk = lane & 3;
+  for (int e = tid; e < NB * NB; e += 256) X[e >> 6][e & 63] = 0.0;
   __syncthreads();
-  bool bad_any = false;
-  for (int c0 = 0; c0 < NB; c0 += SB) {
-    // (1) the 16 x 16 diagonal block and its inverse with all 256 threads, thread (r, c) holding
-    // entry (r, c) in a register and one barrier per column: factor with the unscaled update
-    // a_rc -= a_rC a_cC / a_CC (column C published to colb at the end of step C - 1), scale once;
-    // then X = L^{-1} row by row (row C scaled by 1 / L_CC and published, rows r > C updated).
-    {
-      const int r = tid >> 4, c = tid & 15;
-      double a = (c <= r) ? S[c0 + r][c0 + c] : 0.0;
-      if (c == 0) colb[0][r] = a;
-      __syncthreads();
-      for (int C = 0; C < SB; ++C) {
-        const double* cb = colb[C & 1];
-        double piv = cb[C];
-        const bool bad = !(piv > 0.0) || !isfinite(piv);
-        if (bad) piv = 1.0;  // keep the values finite; info reports the failure
-        if (tid == 0) {
-          pv16[C] = piv;
-          bad_any |= bad;
-        }
-        const double inv = 1.0 / piv;
-        if (c > C && r >= c) a = fma(-cb[r] * inv, cb[c], a);
-        if (c == C + 1) colb[(C + 1) & 1][r] = a;
-        __syncthreads();
-      }
-      if (c <= r) {
-        const double rs = rsqrt(pv16[c]);
-        S[c0 + r][c0 + c] = (r == c) ? pv16[c] * rs : a * rs;
-      }
-      __syncthreads();
-      double xv = (r == c) ? 1.0 : 0.0;
-      for (int C = 0; C < SB; ++C) {
-        if (r == C && c <= C) {
-          xv *= 1.0 / S[c0 + C][c0 + C];
-          xrow[C & 1][c] = xv;
-        }
-        __syncthreads();
-        if (r > C && c <= C) xv = fma(-S[c0 + r][c0 + C], xrow[C & 1][c], xv);
-      }
-      X[c0 + r][c0 + c] = (c <= r) ? xv : 0.0;
-    }
+  bool bad = false;
+#pragma unroll 1
+  for (int c0 = 0; c0 < jb; c0 += SB) {
+    if (w == 0) bad |= potrf16_warp(S, X, c0, colb);  // (1)
     __syncthreads();
     const int r0 = c0 + SB, R = NB - r0;
     if (R > 0) {
-      // (2) L21 = A21 X11^T  (rows r0.., 16 columns), via registers then in place
-      double l21[3];
+      // (2) T = A21 X11^T (R x 16; warp w: 8 x 8 output tiles w, w + 8)
+      for (int tt = w; tt < (R / 8) * 2; tt += 8) {
+        const int tm = tt >> 1, tn = tt & 1;
+        double c0v = 0.0, c1v = 0.0;
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int e = tid + 256 * m;
-        l21[m] = 0.0;
-        if (e < R * SB) {
-          const int i = r0 + e / SB, j = e % SB;
-          double acc = 0.0;
-          for (int t = 0; t <= j; ++t) acc = fma(S[i][c0 + t], X[c0 + j][c0 + t], acc);
-          l21[m] = acc;
-        }
+        for (int k0 = 0; k0 < SB; k0 += 4)
+          dmma(c0v, c1v, S[r0 + tm * 8 + lr][c0 + k0 + lk], X[c0 + tn * 8 + lr][c0 + k0 + lk]);
+        T[tm * 8 + lr][tn * 8 + 2 * lk] = c0v;
+        T[tm * 8 + lr][tn * 8 + 2 * lk + 1] = c1v;
       }
       __syncthreads();
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int e = tid + 256 * m;
-        if (e < R * SB) S[r0 + e / SB][c0 + e % SB] = l21[m];
-      }
-      __syncthreads();
-      // (3) A22 -= L21 L21^T on DMMA: 8x8 blocks (mb >= nb) of the R x R trailing matrix
+      for (int e = tid; e < R * SB; e += 256) S[r0 + e / SB][c0 + e % SB] = T[e / SB][e % SB];
+      // (3) A22 -= L21 L21^T: 8 x 8 tiles (mb >= nb) of the R x R trailing block, from T
       const int MBk = R / 8;
-      const int lr = lane >> 2, lk = lane & 3;
       for (int blk = w; blk < MBk * (MBk + 1) / 2; blk += 8) {
-        int mb = (int)((sqrt(8.0 * blk + 1.0) - 1.0) * 0.5);
+        int mb = 0;
         while ((mb + 1) * (mb + 2) / 2 <= blk) ++mb;
-        while (mb * (mb + 1) / 2 > blk) --mb;
         const int nb = blk - mb * (mb + 1) / 2;
         double c0v = 0.0, c1v = 0.0;
 #pragma unroll
-        for (int k0 = 0; k0 < SB; k0 += 4) {
-          const double a = S[r0 + mb * 8 + lr][c0 + k0 + lk];
-          const double b = S[r0 + nb * 8 + lr][c0 + k0 + lk];
-          dmma(c0v, c1v, a, b);
-        }
+        for (int k0 = 0; k0 < SB; k0 += 4) dmma(c0v, c1v, T[mb * 8 + lr][k0 + lk], T[nb * 8 + lr][k0 + lk]);
         const int rr = r0 + mb * 8 + lr, cc = r0 + nb * 8 + 2 * lk;
         if (cc <= rr) S[rr][cc] -= c0v;
         if (cc + 1 <= rr) S[rr][cc + 1] -= c1v;
@@ -169,10 +161,8 @@ __device__ __noinline__ void potrf_block(int n, double* A, int lda, int j0, doub
       __syncthreads();
     }
   }
-  if (tid == 0 && bad_any) atomicCAS(info, 0, j0 + 1);
-  // (4) off-diagonal blocks of X = L^{-1} (the 16 x 16 diagonal blocks came from step 1) on DMMA:
-  // X_ba = -X_bb (L_ba X_aa) for the 16-blocks of each 32-block, then for the two 32-blocks.
-  // The strict upper triangle of S is zeroed first (the blocks are read whole).
+  // (4) off-diagonal blocks of X = L^{-1} on DMMA: X_ba = -X_bb (L_ba X_aa) for the 16-blocks of
+  // each 32-block, then for the two 32-blocks. The strict upper triangle of S is zeroed first.
   for (int e = tid; e < NB * NB; e += 256) {
     const int r = e >> 6, c = e & 63;
     if (c > r) S[r][c] = 0.0;
@@ -185,30 +175,14 @@ __device__ __noinline__ void potrf_block(int n, double* A, int lda, int j0, doub
     __syncthreads();
     smem_gemm(&X[o + 16][o], LDR, &X[o + 16][o + 16], LDR, &T2[16 * h][0], 33, 16, 16, 16, -1.0, w & 3, 4);
     __syncthreads();
-    smem_gemm(&T2[0][0], 33, &S[32][0], LDR, &X[0][0], LDR, 32, 32, 32, 1.0, w, 8);
-    __syncthreads();
-    smem_gemm(&X[32][0], LDR, &X[32][32], LDR, &T2[0][0], 33, 32, 32, 32, -1.0, w, 8);
-    __syncthreads();
+    if (jb > 32) {
+      smem_gemm(&T2[0][0], 33, &S[32][0], LDR, &X[0][0], LDR, 32, 32, 32, 1.0, w, 8);
+      __syncthreads();
+      smem_gemm(&X[32][0], LDR, &X[32][32], LDR, &T2[0][0], 33, 32, 32, 32, -1.0, w, 8);
+      __syncthreads();
+    }
   }
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (r < jb && c <= r) A[(int64_t)(j0 + r) * lda + j0 + c] = S[r][c];
-    Linv[e] = (r < jb && c <= r) ? X[r][c] : 0.0;  // [NB][NB], zero outside the triangle
-  }
-  if (x) {
-    const int r = tid >> 2, q = tid & 3;
-    double sacc = 0.0;
-    for (int t = q; t <= r; t += 4) sacc = fma(X[r][t], bv[t], sacc);
-    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-    if (q == 0 && r < jb) x[j0 + r] = sacc;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_potrf_inv(int n, double* A, int lda, int j0, double* Linv, int* info,
-                                                   double* x) {
-  extern __shared__ __align__(16) double dsm[];
-  potrf_block(n, A, lda, j0, Linv, info, x, dsm);
+  return bad;
 }
 
 __global__ void __launch_bounds__(256) k_trtri_blocks(int n, const double* A, int lda, double* Linv) {
@@ -261,15 +235,47 @@ __device__ __forceinline__ void load_tile(double (*T)[LDS], const double* A, int
   }
 }
 
-// out[64x64] = X[64x64] * Y[64x64]^T from two smem tiles (row-major, LDS); 8 warps of 16x32
-__device__ __forceinline__ void tile_xyT(const double (*Xs)[LDS], const double (*Ys)[LDS], double acc[2][4][2]) {
+
+// ---- flags, mbarriers, bulk copies -----------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// acc[64x64] += X[64x64] * Y[64x64]^T from two smem tiles (row-major, LDS); 8 warps of 16x32: thread
+// (warp w, lane) holds entries (wr + 8a + lane/4, wc + 8b + 2 (lane%4) + h), wr = 16 (w/2), wc = 32 (w%2)
+__device__ __forceinline__ void tile_acc_xyT(const double (*Xs)[LDS], const double (*Ys)[LDS], double acc[2][4][2]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wr = (w >> 1) * 16, wc = (w & 1) * 32;
   const int lr = lane >> 2, lk = lane & 3;
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll 4
   for (int k0 = 0; k0 < NB; k0 += 4) {
     double af[2], bf[4];
@@ -284,203 +290,373 @@ __device__ __forceinline__ void tile_xyT(const double (*Xs)[LDS], const double (
   }
 }
 
-// rows [j0+jb + 64*tile, +64): L21 = A21 Linv^T; with x: x_r -= L21_r . y_j
-// L1 caching of the operand tiles (cp.async.ca) is safe only across kernel launches: inside the
-// persistent factorisation (k_chol_persist) a line fetched for panel j may hold columns that panel
-// j's trailing update rewrites, so there (PERSIST) the tiles are staged through registers with
-// L2-only loads, all in flight together.
-template <bool PERSIST>
-__device__ __noinline__ void trsm_tile(int n, double* A, int lda, int j0, const double* Linv, double* x, int tile,
-                                       double* dsm) {
-  __syncthreads();  // smem reuse across consecutive tiles
-  double(*Xs)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
-  double(*Ys)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + NB * LDS);
-  __shared__ double yv[NB];
-  const int jb = min(NB, n - j0);
-  const int r0 = j0 + jb + tile * NB;
-  const int tid = threadIdx.x;
-  if constexpr (PERSIST) {  // one round trip through registers (L2 loads)
-    const int nr = n - r0;
-    double va[16], vl[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      const bool ok = r < nr && c < jb;
-      va[m] = ok ? __ldcg(A + (int64_t)(r0 + r) * lda + j0 + c) : 0.0;
-      vl[m] = __ldcg(Linv + e);
-    }
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      Xs[r][c] = va[m];
-      Ys[r][c] = vl[m];
-    }
-  } else {  // one round trip: the A21 tile (zero beyond n / jb) and Linv[j] straight into shared memory
-    const int nr = n - r0;
-#pragma unroll 4
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      const bool ok = r < nr && c < jb;
-      const double* g = A + (int64_t)(r0 + (ok ? r : 0)) * lda + j0 + (ok ? c : 0);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                       static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]))),
-                   "l"(g), "r"(ok ? 8 : 0)
-                   : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                       static_cast<unsigned>(__cvta_generic_to_shared(&Ys[r][c]))),
-                   "l"(Linv + e)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  if (x && tid < NB) yv[tid] = tid < jb ? __ldcg(x + j0 + tid) : 0.0;
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  double acc[2][4][2];
-  tile_xyT(Xs, Ys, acc);
-  __syncthreads();  // done reading Xs: reuse it for the result
-  const int lane = tid & 31, w = tid >> 5;
+__device__ __forceinline__ int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// ---- the tile-DAG factorisation -------------------------------------------------------------
+// A: the SPD matrix, row-major (lda), lower triangle read (once; never written by this kernel).
+// Lt: tile-major packed L (tile_off), LinvP: Linv_j padded [nt][NB][LDS], Linv: the same unpadded
+// [nt][NB][NB] (k_trsv_wave, k_inv_diag). b (optional): right-hand side; ybuf [nt NB] <- L^{-1} b
+// (zero padded); with nt == 1 and x != null, x <- (L L^T)^{-1} b directly. flags [nt (nt+1)/2].
+//
+// Tasks, column-major: column j holds D_j, then (i, j) for i >= j + 2. D_j computes the
+// sub-diagonal tile (j, j-1) AND the diagonal tile (j, j): it accumulates both over k < j - 1
+// while column j - 1 is still being factored, then, as soon as Linv_{j-1} is published, forms
+// L_{j,j-1}, publishes it, applies its last update L_{j,j-1} L_{j,j-1}^T from shared memory and
+// factors. The column-to-column critical path is thus potrf, one bulk load of Linv, two 64^3 DMMA
+// products, potrf, ... with no flag round trip for the sub-diagonal tile.
+constexpr int kDagSmemDoubles = 5 * TS + 3 * NB;  // 2 stages x 2 tiles, Linv_{j-1}, 2 stages x y_k, y_{j-1}
+
+// Task order (topological, with a lookahead of one column for the diagonal tasks): group 0 =
+// [D_0, D_1]; group g >= 1 = [(i, g-1) for i = g+1 .. nt-1, then D_{g+1}]. D_j is taken as soon as
+// column j-2 is, so its long accumulation runs alongside column j-1 instead of after it.
+__device__ __forceinline__ int dag_off_tasks(int nt, int g) { return g == 0 ? 0 : max(0, nt - g - 1); }
+__device__ __forceinline__ int dag_group_tasks(int nt, int g) {
+  return g == 0 ? min(nt, 2) : dag_off_tasks(nt, g) + (g + 1 < nt ? 1 : 0);
+}
+
+// fragment loads of A (row-major) for tile rows i0.., columns j0..: identity beyond n on the
+// diagonal, zero in the strict upper triangle
+__device__ __forceinline__ void load_a_frag(const double* __restrict__ A, int lda, int n, int i0, int j0,
+                                            double (&cv)[2][4][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int rl = wr + a * 8 + lr, c = wc + b * 8 + 2 * lk + h;
-        Xs[rl][c] = (c < jb) ? acc[a][b][h] : 0.0;
-        if (r0 + rl < n && c < jb) A[(int64_t)(r0 + rl) * lda + j0 + c] = acc[a][b][h];
+        const int r = i0 + wr + a * 8 + lr, c = j0 + wc + bb * 8 + 2 * lk + h;
+        cv[a][bb][h] = (r < n && c <= r) ? __ldg(A + (int64_t)r * lda + c) : (r == c ? 1.0 : 0.0);
       }
-  if (x) {
+}
+
+// fragments -> smem tile (LDS rows)
+__device__ __forceinline__ void frag_to_smem(double* T, const double (&v)[2][4][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb)
+      *reinterpret_cast<double2*>(T + (wr + a * 8 + lr) * LDS + wc + bb * 8 + 2 * lk) = make_double2(v[a][bb][0], v[a][bb][1]);
+}
+
+__device__ __forceinline__ void frag_zero(double (&v)[2][4][2]) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) v[a][bb][0] = v[a][bb][1] = 0.0;
+}
+
+__global__ void __launch_bounds__(256, 1) k_chol_dag(int n, int nt, const double* __restrict__ A, int lda, double* Lt,
+                                                     double* LinvP, double* Linv, const double* __restrict__ b,
+                                                     double* ybuf, double* x, int* info, int* flags, int epoch,
+                                                     int* next_task) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ __align__(8) uint64_t bars[3];
+  __shared__ double bv[NB], yv[NB], part[4][NB];
+  __shared__ int task_s;
+  double* const TA[2] = {dsm, dsm + 2 * TS};
+  double* const TB[2] = {dsm + TS, dsm + 3 * TS};
+  double* const LI = dsm + 4 * TS;
+  double* const YB[2] = {dsm + 5 * TS, dsm + 5 * TS + NB};
+  double* const YL = dsm + 5 * TS + 2 * NB;
+  const int tid = threadIdx.x;
+  const int rq = tid >> 2, q4 = tid & 3;  // row-per-4-threads mapping (forward solve pieces)
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph[2] = {0u, 0u}, phl = 0u;  // mbarrier parities (identical in every thread)
+  int ntask = 0;
+  for (int g = 0; g < nt; ++g) ntask += dag_group_tasks(nt, g);
+  auto publish = [&](int fi) {  // every thread's global writes of the task (ordered by the CTA
+    __syncthreads();             // barrier, then made gpu-visible by thread 0's fence), then its flag
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("fence.proxy.async;" ::: "memory");
+      st_release(flags + fi, epoch);
+    }
+  };
+  auto wait_flag = [&](int fi) {
+    while (ld_acquire(flags + fi) != epoch) __nanosleep(64);
+  };
+  int g = 0, grp0 = 0;
+  for (;;) {
+    // dynamic dealing in the topological order: a CTA takes the next task when it is free (the
+    // tasks it waits on were all taken before it, by running CTAs, so this cannot deadlock)
+    if (tid == 0) task_s = atomicAdd(next_task, 1);
+    __syncthreads();
+    const int t = task_s;
+    __syncthreads();
+    if (t >= ntask) break;
+    while (t >= grp0 + dag_group_tasks(nt, g)) {
+      grp0 += dag_group_tasks(nt, g);
+      ++g;
+    }
+    const int u = t - grp0;
+    const bool diag = g == 0 || u >= dag_off_tasks(nt, g);
+    // diagonal task D_j: rows i = j, partner tile row m = j - 1 (the sub-diagonal tile (j, m));
+    // off-diagonal task: tile (i, j), partner tile row m = j
+    const int j = diag ? (g == 0 ? u : g + 1) : g - 1;
+    const int i = diag ? j : g + 1 + u;
+    const int m = diag ? j - 1 : j;
+    const int kend = diag ? j - 1 : j;  // k-steps of the accumulation (k < kend)
+    const bool want_y = diag && b != nullptr;
+    double acc[2][4][2], acc2[2][4][2];  // (i, m) tile; diagonal task: also the (j, j) tile
+    frag_zero(acc);
+    frag_zero(acc2);
+    double xs = 0.0;  // diagonal task: row rq of sum_k L_jk y_k over columns q4 + 4 s
+    const unsigned bytes = 2u * TS * 8u + (want_y ? NB * 8u : 0u);
+    auto ready = [&](int k) {
+      return ld_acquire(flags + tri(i, k)) == epoch && ld_acquire(flags + tri(m, k)) == epoch &&
+             (!want_y || ld_acquire(flags + tri(k, k)) == epoch);
+    };
+    auto issue = [&](int k) {
+      const int s = k & 1;
+      asm volatile("fence.proxy.async;" ::: "memory");  // generic accesses before the async copy
+      mbar_expect(&bars[s], bytes);
+      bulk_g2s(TA[s], Lt + tile_off(i, k), TS * 8u, &bars[s]);
+      bulk_g2s(TB[s], Lt + tile_off(m, k), TS * 8u, &bars[s]);
+      if (want_y) bulk_g2s(YB[s], ybuf + (int64_t)k * NB, NB * 8u, &bars[s]);
+    };
+    int issued = 0;  // thread 0: steps issued so far
+    for (int k = 0; k < kend; ++k) {
+      const int s = k & 1;
+      if (tid == 0) {
+        if (issued == k) {
+          while (!ready(k)) __nanosleep(64);
+          issue(k);
+          ++issued;
+        }
+        if (issued == k + 1 && k + 1 < kend && ready(k + 1)) {  // lookahead: only if already published
+          issue(k + 1);
+          ++issued;
+        }
+      }
+      mbar_wait(&bars[s], ph[s]);
+      ph[s] ^= 1u;
+      const double(*ta)[LDS] = reinterpret_cast<const double(*)[LDS]>(TA[s]);
+      const double(*tb)[LDS] = reinterpret_cast<const double(*)[LDS]>(TB[s]);
+      tile_acc_xyT(ta, tb, acc);
+      if (diag) {
+        tile_acc_xyT(ta, ta, acc2);
+        if (want_y) {
+#pragma unroll
+          for (int s4 = 0; s4 < 16; ++s4) xs = fma(ta[rq][q4 + 4 * s4], YB[s][q4 + 4 * s4], xs);
+        }
+      }
+      __syncthreads();  // stage s is free for step k + 2
+    }
+    if (m >= 0) {
+      // L_im = (A_im - acc) Linv_m^T once the diagonal task of column m has published Linv_m (and y_m)
+      if (tid == 0) {
+        wait_flag(tri(m, m));
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_expect(&bars[2], TS * 8u + (want_y ? NB * 8u : 0u));
+        bulk_g2s(LI, LinvP + (int64_t)m * TS, TS * 8u, &bars[2]);
+        if (want_y) bulk_g2s(YL, ybuf + (int64_t)m * NB, NB * 8u, &bars[2]);
+      }
+      double cv[2][4][2];
+      load_a_frag(A, lda, n, i * NB, m * NB, cv);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) cv[a][bb][h] -= acc[a][bb][h];
+      frag_to_smem(TA[0], cv);  // the stages are free: the loop ended with a CTA barrier (or did not run)
+      __syncthreads();
+      mbar_wait(&bars[2], phl);
+      phl ^= 1u;
+      frag_zero(acc);
+      tile_acc_xyT(reinterpret_cast<const double(*)[LDS]>(TA[0]), reinterpret_cast<const double(*)[LDS]>(LI), acc);
+      frag_to_smem(Lt + tile_off(i, m), acc);
+      if (diag) frag_to_smem(TB[0], acc);  // L_{j,j-1} for the diagonal tile's last update
+      publish(tri(i, m));
+      if (diag) {  // the last update of the diagonal tile: acc2 += L_jm L_jm^T, xs += L_jm y_m
+        const double(*tl)[LDS] = reinterpret_cast<const double(*)[LDS]>(TB[0]);
+        tile_acc_xyT(tl, tl, acc2);
+        if (want_y) {
+#pragma unroll
+          for (int s4 = 0; s4 < 16; ++s4) xs = fma(tl[rq][q4 + 4 * s4], YL[q4 + 4 * s4], xs);
+        }
+        __syncthreads();  // TB[0] is overwritten by the factorisation's workspace
+      }
+    }
+    if (!diag) continue;
+    // the diagonal tile: C = A_jj - acc2, L_jj = chol(C), Linv_j, y_j
+    double(*S)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm);
+    double(*X)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + NB * LDR);
+    const int j0 = j * NB, jb = min(NB, n - j0);
+    {
+      double cv[2][4][2];
+      load_a_frag(A, lda, n, j0, j0, cv);
+      const int lane = tid & 31, w = tid >> 5;
+      const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = wr + a * 8 + lr, c = wc + bb * 8 + 2 * lk + h;
+            S[r][c] = c <= r ? cv[a][bb][h] - acc2[a][bb][h] : 0.0;
+          }
+    }
+    if (want_y) {
+      xs += __shfl_xor_sync(0xffffffffu, xs, 1);
+      xs += __shfl_xor_sync(0xffffffffu, xs, 2);
+      if (q4 == 0) bv[rq] = rq < jb ? __ldg(b + j0 + rq) - xs : 0.0;
+    }
+    __syncthreads();
+    const bool bad = potrf_core(jb, dsm);  // ends with a CTA barrier
+    if (tid == 0 && bad) atomicCAS(info, 0, j0 + 1);
+    double* out = Lt + tile_off(j, j);
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int r = e >> 6, c = e & 63;
+      const bool in = r < jb && c <= r;
+      out[r * LDS + c] = in ? S[r][c] : 0.0;
+      const double xv = in ? X[r][c] : 0.0;
+      LinvP[(int64_t)j * TS + r * LDS + c] = xv;
+      Linv[(int64_t)j * NB * NB + e] = xv;
+    }
+    if (want_y) {  // y_j = Linv_j (b_j - sum_k L_jk y_k)
+      double sacc = 0.0;
+      for (int tt = q4; tt <= rq && tt < jb; tt += 4) sacc = fma(X[rq][tt], bv[tt], sacc);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+      if (q4 == 0) {
+        const double yj = rq < jb ? sacc : 0.0;
+        ybuf[j0 + rq] = yj;
+        yv[rq] = yj;
+      }
+      if (nt == 1 && x) {  // single tile: the backward solve x = Linv^T y here as well
+        __syncthreads();
+        const int c = tid & 63, g = tid >> 6;
+        double o = 0.0;
+        for (int tt = c + (g - c % 4 + 4) % 4; tt < jb; tt += 4) o = fma(X[tt][c], yv[tt], o);  // rows tt >= c
+        part[g][c] = o;
+        __syncthreads();
+        if (tid < jb) x[tid] = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+      }
+    }
+    publish(tri(j, j));
+  }
+}
+
+// tile-major L -> the lower triangle of the row-major A (lda); row r per CTA
+__global__ void __launch_bounds__(256) k_untile(int n, const double* __restrict__ Lt, double* A, int lda) {
+  const int r = blockIdx.x, ti = r / NB, rr = r % NB;
+  for (int c = threadIdx.x; c <= r; c += 256) A[(int64_t)r * lda + c] = Lt[tile_off(ti, c / NB) + rr * LDS + c % NB];
+}
+
+// Backward solve L^T z = y on the tile-major factor of k_chol_dag (one CTA per 64-block b, blocks
+// solved in descending order): z_b = Linv_b^T (y_b - L_{b+1,b}^T z_{b+1} - sum_{j>=b+2} L_jb^T z_j).
+// Off the critical chain, each CTA first forms W_b = Linv_b^T L_{b+1,b}^T (DMMA) and folds in the
+// blocks j >= b + 2 as their flags are published, giving w_b = Linv_b^T (y_b - sum_{j>=b+2} ...);
+// the chain from block b + 1 to block b is then one 64 x 64 product: z_b = w_b - W_b z_{b+1}.
+// Contraction orders are fixed (deterministic). ybuf [nt NB] (zero padded), x [n] out.
+__global__ void __launch_bounds__(256, 1) k_trsv_bwd_tiles(int n, const double* __restrict__ Lt,
+                                                           const double* __restrict__ LinvP,
+                                                           const double* __restrict__ ybuf, double* x, int* flags,
+                                                           int epoch) {
+  extern __shared__ __align__(16) double dsm[];
+  double(*Xs)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);            // Linv_b^T
+  double(*Ys)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + TS);       // L_{b+1,b}
+  double(*Ws)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + 2 * TS);   // W_b
+  __shared__ double part[4][NB], wv[NB], zn[NB];
+  const int nblk = (n + NB - 1) / NB;
+  const int b = nblk - 1 - blockIdx.x;
+  const int b0 = b * NB, bb = min(NB, n - b0);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const bool has_next = b + 1 < nblk;
+  for (int e = tid; e < NB * NB; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    Xs[c][r] = LinvP[(int64_t)b * TS + r * LDS + c];  // transposed
+    if (has_next) Ys[r][c] = Lt[tile_off(b + 1, b) + r * LDS + c];
+  }
+  __syncthreads();
+  if (has_next) {  // W_b[r][c] = sum_t Linv_b[t][r] L_{b+1,b}[c][t]
+    double acc[2][4][2];
+    frag_zero(acc);
+    tile_acc_xyT(Xs, Ys, acc);
+    const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) Ws[wr + a * 8 + lr][wc + b2 * 8 + 2 * lk + h] = acc[a][b2][h];
+  }
+  // fold the blocks j >= b + 2 (descending, as they are published): thread -> column c of block b,
+  // rows g + 4k of block j
+  const int c = tid & 63, g = tid >> 6;
+  double s = 0.0;
+  for (int j = nblk - 1; j >= b + 2; --j) {
+    const int j0 = j * NB, jbb = min(NB, n - j0);
+    double Lr[16];
+    const double* Lj = Lt + tile_off(j, b);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Lr[k] = Lj[(g + 4 * k) * LDS + c];  // zero beyond n (padded tiles)
+    if (tid == 0)
+      while (ld_acquire(flags + j) != epoch) __nanosleep(32);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int t = g + 4 * k;
+      if (t < jbb) s = fma(Lr[k], __ldcg(x + j0 + t), s);
+    }
+  }
+  part[g][c] = s;
+  __syncthreads();
+  if (tid < NB) wv[tid] = ybuf[b0 + tid] - ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]));
+  __syncthreads();
+  {  // w_b = Linv_b^T v: thread (c, g) sums rows t = g + 4k of Linv_b (Xs[c][t] = Linv_b[t][c])
+    double o = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o = fma(Xs[c][g + 4 * k], wv[g + 4 * k], o);
+    part[g][c] = o;
+  }
+  __syncthreads();
+  if (tid < NB) wv[tid] = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+  // the chain: z_b = w_b - W_b z_{b+1}
+  if (has_next) {
+    const int bn0 = b0 + NB, bnb = min(NB, n - bn0);
+    if (tid == 0)
+      while (ld_acquire(flags + b + 1) != epoch) __nanosleep(32);
+    __syncthreads();
+    if (tid < NB) zn[tid] = tid < bnb ? __ldcg(x + bn0 + tid) : 0.0;
     __syncthreads();
     const int r = tid >> 2, q4 = tid & 3;
-    double s = 0.0;
-    for (int t = q4; t < jb; t += 4) s = fma(Xs[r][t], yv[t], s);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (q4 == 0 && r0 + r < n) x[r0 + r] = __ldcg(x + r0 + r) - s;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_trsm_gemm(int n, double* A, int lda, int j0, const double* Linv, double* x) {
-  extern __shared__ __align__(16) double dsm[];
-  trsm_tile<false>(n, A, lda, j0, Linv, x, blockIdx.x, dsm);
-}
-
-// trailing update tile (ti, tj), ti >= tj, of A22 -= L21 L21^T (tile coordinates relative to the
-// first row/column after panel j0)
-template <bool PERSIST>
-__device__ __noinline__ void syrk_tile(int n, double* A, int lda, int j0, int ti, int tj, double* dsm) {
-  __syncthreads();  // smem reuse across consecutive tiles
-  double(*Li)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
-  double(*Lj)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm + NB * LDS);
-  const int jb = min(NB, n - j0);
-  const int s0 = j0 + jb;
-  const int ri = s0 + ti * NB, rj = s0 + tj * NB;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, w = tid >> 5;
-  const int wr = (w >> 1) * 16, wc = (w & 1) * 32, lr = lane >> 2, lk = lane & 3;
-  // one round trip: the two L21 tiles go to shared memory (cp.async, or through registers in the
-  // persistent kernel) while this thread's 16 entries of the C tile are loaded into registers
-  double cv[2][4][2];
+    double o = 0.0;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = ri + wr + a * 8 + lr, c = rj + wc + b * 8 + 2 * lk + h;
-        cv[a][b][h] = (r < n && c < n && c <= r) ? __ldcg(A + (int64_t)r * lda + c) : 0.0;
-      }
-  if constexpr (PERSIST) {
-    const int nri = n - ri, nrj = n - rj;
-    double vi[16], vj[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      vi[m] = (r < nri && c < jb) ? __ldcg(A + (int64_t)(ri + r) * lda + j0 + c) : 0.0;
-      vj[m] = (r < nrj && c < jb) ? __ldcg(A + (int64_t)(rj + r) * lda + j0 + c) : 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      Li[r][c] = vi[m];
-      Lj[r][c] = vj[m];
-    }
+    for (int k = 0; k < 16; ++k) o = fma(Ws[r][q4 + 4 * k], zn[q4 + 4 * k], o);
+    o += __shfl_xor_sync(0xffffffffu, o, 1);
+    o += __shfl_xor_sync(0xffffffffu, o, 2);
+    if (q4 == 0 && r < bb) x[b0 + r] = wv[r] - o;
   } else {
-    const int nri = n - ri, nrj = n - rj;
-#pragma unroll 4
-    for (int m = 0; m < 16; ++m) {
-      const int e = tid + 256 * m, r = e >> 6, c = e & 63;
-      const bool oki = r < nri && c < jb, okj = r < nrj && c < jb;
-      const double* gi = A + (int64_t)(ri + (oki ? r : 0)) * lda + j0 + (oki ? c : 0);
-      const double* gj = A + (int64_t)(rj + (okj ? r : 0)) * lda + j0 + (okj ? c : 0);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                       static_cast<unsigned>(__cvta_generic_to_shared(&Li[r][c]))),
-                   "l"(gi), "r"(oki ? 8 : 0)
-                   : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                       static_cast<unsigned>(__cvta_generic_to_shared(&Lj[r][c]))),
-                   "l"(gj), "r"(okj ? 8 : 0)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    __syncthreads();
+    if (tid < bb) x[b0 + tid] = wv[tid];
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  double acc[2][4][2];
-  tile_xyT(Li, Lj, acc);
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = ri + wr + a * 8 + lr, c = rj + wc + b * 8 + 2 * lk + h;
-        if (r < n && c < n && c <= r) A[(int64_t)r * lda + c] = cv[a][b][h] - acc[a][b][h];
-      }
-}
-
-// linear index over the lower triangle of tiles (row-major) -> (ti, tj), ti >= tj
-__device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
-  ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-  while (ti * (ti + 1) / 2 > t) --ti;
-  tj = t - ti * (ti + 1) / 2;
-}
-
-// col_only = 1: only block-column 0 of the trailing matrix (the next panel, lookahead path);
-// col_only = 0: the lower triangle starting at tile (first, first).
-__global__ void __launch_bounds__(256) k_syrk_tiles(int n, double* A, int lda, int j0, int col_only, int first) {
-  extern __shared__ __align__(16) double dsm[];
-  int ti, tj;
-  if (col_only) {
-    ti = blockIdx.x;
-    tj = 0;
-  } else {
-    tri_tile(blockIdx.x, ti, tj);
-    ti += first;
-    tj += first;
+  if (tid == 0) {
+    __threadfence();
+    st_release(flags + b, epoch);
   }
-  syrk_tile<false>(n, A, lda, j0, ti, tj, dsm);
 }
-
 // ---- triangular solve wavefront ------------------------------------------------------------
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // forward (upper = 0): y_b = Linv_b (x_b - sum_{j<b} L[b, j] y_j), block b = blockIdx.x.
 // backward (upper = 1): z_b = Linv_b^T (y_b - sum_{j>b} L[j, b]^T z_j), blocks in reverse order.
-// x is overwritten in place. The L block of the next step is loaded into registers before the
-// flag wait; the contraction order over blocks and within a block is fixed (deterministic).
+// The right-hand side is read from xin (which may be x) and the result written to x (row-major L,
+// lda). The L block of the next step is loaded into registers before the flag wait; the
+// contraction order over blocks and within a block is fixed (deterministic).
 __global__ void __launch_bounds__(256) k_trsv_wave(int n, const double* L, int lda, const double* Linv,
-                                                   double* x, int* flags, int epoch, int upper) {
+                                                   const double* xin, double* x, int* flags, int epoch, int upper) {
   __shared__ double Li[NB][LDR];
   __shared__ double part[4][NB];
   __shared__ double v[NB];
@@ -527,13 +703,13 @@ __global__ void __launch_bounds__(256) k_trsv_wave(int n, const double* L, int l
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (q4 == 0) part[0][r] = acc;
     __syncthreads();
-    if (tid < NB) v[tid] = tid < bb ? x[b0 + tid] - part[0][tid] : 0.0;
+    if (tid < NB) v[tid] = tid < bb ? xin[b0 + tid] - part[0][tid] : 0.0;
   } else {
     part[g][c] = acc;
     __syncthreads();
     if (tid < NB) {
       const double s = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
-      v[tid] = tid < bb ? x[b0 + tid] - s : 0.0;
+      v[tid] = tid < bb ? xin[b0 + tid] - s : 0.0;
     }
   }
   __syncthreads();
@@ -555,255 +731,12 @@ __global__ void __launch_bounds__(256) k_trsv_wave(int n, const double* L, int l
   if (tid == 0) st_release(flags + b, epoch);
 }
 
-// ---- persistent factorisation (one cooperative launch) -------------------------------------
-// Grid barrier over all CTAs of a cooperative launch: count + generation (sense) in global memory.
-// Writes before the barrier are published with a gpu-scope fence; the phases read A / Linv / x
-// through L2 (__ldcg), never through a possibly stale L1.
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned& my_gen, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned g = my_gen;
-    if (atomicAdd(count, 1u) == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
-    } else {
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
-        if (v == g) __nanosleep(32);
-      } while (v == g);
-    }
-  }
-  my_gen += 1;
-  __syncthreads();
-}
-
-// The blocked right-looking factorisation of factor() in one kernel (n <= 2816), with the same one-panel
-// lookahead: per panel j, (B) all CTAs compute the trsm tiles of panel j, (C) all CTAs update
-// block column j+1, (A) CTA 0 factors panel j+1 while the other CTAs apply the rest of panel j's
-// trailing update. Every tile runs exactly the arithmetic of the multi-kernel path (same device
-// functions, same order per entry), so the factor is bitwise identical; only launch and
-// cross-stream synchronisation costs go away. bar = {count, generation}.
-__global__ void __launch_bounds__(256, 1) k_chol_persist(int n, double* A, int lda, double* Linv, int* info, double* x,
-                                                         unsigned* bar) {
-  extern __shared__ __align__(16) double dsm[];
-  const unsigned G = gridDim.x, b = blockIdx.x;
-  unsigned my_gen = 0;
-  if (threadIdx.x == 0) my_gen = *reinterpret_cast<volatile unsigned*>(bar + 1);
-  const int np = (n + NB - 1) / NB;
-  if (b == 0) potrf_block(n, A, lda, 0, Linv, info, x, dsm);
-  grid_barrier(bar, bar + 1, my_gen, G);
-  for (int j = 0; j + 1 < np; ++j) {
-    const int j0 = j * NB, rem = n - j0 - NB, mt = (rem + NB - 1) / NB;
-    const double* Lj = Linv + (size_t)j * NB * NB;
-    for (int t = b; t < mt; t += G) trsm_tile<true>(n, A, lda, j0, Lj, x, t, dsm);    // (B)
-    grid_barrier(bar, bar + 1, my_gen, G);
-    for (int t = b; t < mt; t += G) syrk_tile<true>(n, A, lda, j0, t, 0, dsm);       // (C)
-    grid_barrier(bar, bar + 1, my_gen, G);
-    if (b == 0) {                                                                    // (A)
-      potrf_block(n, A, lda, j0 + NB, Linv + (size_t)(j + 1) * NB * NB, info, x, dsm);
-    } else {
-      const int nrest = (mt - 1) * mt / 2;
-      for (int t = b - 1; t < nrest; t += G - 1) {
-        int ti, tj;
-        tri_tile(t, ti, tj);
-        syrk_tile<true>(n, A, lda, j0, ti + 1, tj + 1, dsm);
-      }
-    }
-    grid_barrier(bar, bar + 1, my_gen, G);
-  }
-}
-
-}  // namespace
-
-// Per-workspace factorisation state (one per library workspace, i.e. per device and stream).
-struct CholCtx {
-  unsigned* bar = nullptr;  // k_chol_persist's grid barrier {count, generation}
-  int persist_grid = -1;    // CTAs of the cooperative launch (0: not available)
-  double* Linv = nullptr;
-  size_t cap = 0;
-  const double* factor = nullptr;  // matrix whose Linv blocks are current
-  int factor_n = 0;
-  int* flags = nullptr;
-  int nflags = 0;
-  int epoch = 0;
-  // two-stream lookahead path
-  cudaStream_t side = nullptr;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t start = nullptr, done = nullptr;
-};
-
-namespace {
-
-bool ensure_work(CholCtx& g_cw, int n) {
-  const int nblk = (n + NB - 1) / NB;
-  const size_t need = (size_t)nblk * NB * NB;
-  if (need > g_cw.cap) {
-    cudaFree(g_cw.Linv);
-    if (cudaMalloc(&g_cw.Linv, need * sizeof(double)) != cudaSuccess) { g_cw.cap = 0; return false; }
-    g_cw.cap = need;
-  }
-  if (nblk > g_cw.nflags) {
-    cudaFree(g_cw.flags);
-    if (cudaMalloc(&g_cw.flags, nblk * sizeof(int)) != cudaSuccess) { g_cw.nflags = 0; return false; }
-    cudaMemset(g_cw.flags, 0, nblk * sizeof(int));
-    g_cw.nflags = nblk;
-    g_cw.epoch = 0;
-  }
-  return true;
-}
-
-constexpr size_t kDyn = 2 * NB * LDS * sizeof(double);
-constexpr size_t kDynR = 2 * NB * LDR * sizeof(double);
-void set_attrs() {
-  static uint64_t attr_mask = 0;
-  set_once_per_device(attr_mask, [] {
-    cudaFuncSetAttribute(k_trsm_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
-    cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
-    cudaFuncSetAttribute(k_trtri_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
-    cudaFuncSetAttribute(k_chol_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
-    return cudaFuncSetAttribute(k_potrf_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
-  });
-}
-
-cudaError_t launch_wave(CholCtx& g_cw, int n, const double* L, int lda, double* x, int upper, cudaStream_t st) {
-  const int nblk = (n + NB - 1) / NB;
-  int epoch = ++g_cw.epoch;
-  const double* Linv = g_cw.Linv;
-  int* flags = g_cw.flags;
-  void* args[] = {(void*)&n, (void*)&L, (void*)&lda, (void*)&Linv, (void*)&x, (void*)&flags, (void*)&epoch,
-                  (void*)&upper};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_trsv_wave, dim3(nblk), dim3(256), args, 0, st);
-  count_launch();
-  return e;
-}
-
-cudaEvent_t la_event(CholCtx& g_la, size_t i) {
-  while (g_la.ev.size() <= i) {
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    g_la.ev.push_back(e);
-  }
-  return g_la.ev[i];
-}
-
-// Factorisation with a one-panel lookahead; with x != null also the forward solve x <- L^{-1} x.
-// side stream: [A22 update of the next panel's block column] -> potrf(j+1) -> trsm(j+1)
-// main stream: the rest of panel j's trailing update, concurrently.
-cudaError_t factor_persist(CholCtx& g_cw, int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
-  cudaMemsetAsync(info, 0, sizeof(int), st);
-  void* args[] = {(void*)&n, (void*)&A, (void*)&lda, (void*)&g_cw.Linv, (void*)&info, (void*)&x, (void*)&g_cw.bar};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_chol_persist, dim3(g_cw.persist_grid), dim3(256), args,
-                                              kDyn, st);
-  count_launch();
-  g_cw.factor = A;
-  g_cw.factor_n = n;
-  return e;
-}
-
-// CTAs for k_chol_persist: one per SM when the kernel fits there (0 disables the persistent path)
-int persist_grid(CholCtx& g_cw) {
-  if (g_cw.persist_grid >= 0) return g_cw.persist_grid;
-  g_cw.persist_grid = 0;
-  if (getenv("MNL_CHOL_STREAMS")) return 0;
-  int dev = 0, sms = 0, coop = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  if (!coop) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chol_persist, 256, kDyn) != cudaSuccess || occ < 1) return 0;
-  if (cudaMalloc(&g_cw.bar, 2 * sizeof(unsigned)) != cudaSuccess) return 0;
-  cudaMemset(g_cw.bar, 0, 2 * sizeof(unsigned));
-  g_cw.persist_grid = sms;  // one CTA per SM: the panel CTA has its SM to itself
-  return g_cw.persist_grid;
-}
-
-cudaError_t factor(CholCtx& g_cw, int n, double* A, int lda, int* info, double* x, cudaStream_t st) {
-  CholCtx& g_la = g_cw;
-  set_attrs();
-  if (!ensure_work(g_cw, n)) return cudaErrorMemoryAllocation;
-  // persistent single launch: since the tiles fetch their operands in one round trip it is faster
-  // than the two-stream multi-kernel path at every measured n (2816: 1.92 vs 2.36 ms; 5049: 5.35 vs
-  // 5.58 ms); MNL_CHOL_STREAMS=1 forces the multi-kernel path, MNL_CHOL_PERSIST_MAX caps n
-  static const int persist_max = getenv("MNL_CHOL_PERSIST_MAX") ? atoi(getenv("MNL_CHOL_PERSIST_MAX")) : 16384;
-  if (n <= persist_max && persist_grid(g_cw) > 1) return factor_persist(g_cw, n, A, lda, info, x, st);
-  if (!g_la.side) {
-    int lo = 0, hi = 0;  // the panel chain is the critical path: give it the highest priority
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&g_la.side, cudaStreamNonBlocking, hi);
-    cudaEventCreateWithFlags(&g_la.start, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&g_la.done, cudaEventDisableTiming);
-  }
-  cudaStream_t sp = g_la.side;
-  const int np = (n + NB - 1) / NB;
-  cudaMemsetAsync(info, 0, sizeof(int), st);
-  cudaEventRecord(g_la.start, st);
-  cudaStreamWaitEvent(sp, g_la.start, 0);
-  auto panel = [&](int j) {  // potrf + trsm of panel j on the side stream
-    const int j0 = j * NB, jb = std::min(NB, n - j0);
-    double* Lj = g_cw.Linv + (size_t)j * NB * NB;
-    k_potrf_inv<<<1, 256, kDynR, sp>>>(n, A, lda, j0, Lj, info, x);
-    count_launch();
-    const int rem = n - j0 - jb;
-    if (rem > 0) {
-      k_trsm_gemm<<<(rem + NB - 1) / NB, 256, kDyn, sp>>>(n, A, lda, j0, Lj, x);
-      count_launch();
-    }
-  };
-  panel(0);
-  cudaEventRecord(la_event(g_la, 2 * 0), sp);  // ev_p(0)
-  for (int j = 0; j + 1 < np; ++j) {
-    const int j0 = j * NB;
-    const int rem = n - j0 - NB;
-    const int mt = (rem + NB - 1) / NB;
-    // main: rest of panel j's trailing update (tiles with tj >= 1)
-    cudaStreamWaitEvent(st, la_event(g_la, 2 * j), 0);
-    if (mt > 1) {
-      k_syrk_tiles<<<(mt - 1) * mt / 2, 256, kDyn, st>>>(n, A, lda, j0, 0, 1);
-      count_launch();
-    }
-    cudaEventRecord(la_event(g_la, 2 * j + 1), st);  // ev_r(j)
-    // side: next panel's block column, then its factorisation
-    k_syrk_tiles<<<mt, 256, kDyn, sp>>>(n, A, lda, j0, 1, 0);
-    count_launch();
-    panel(j + 1);
-    cudaEventRecord(la_event(g_la, 2 * (j + 1)), sp);  // ev_p(j+1)
-    // the next column update (side, iteration j+1) must follow this rest update (main)
-    cudaStreamWaitEvent(sp, la_event(g_la, 2 * j + 1), 0);
-  }
-  cudaEventRecord(g_la.done, sp);
-  cudaStreamWaitEvent(st, g_la.done, 0);
-  g_cw.factor = A;
-  g_cw.factor_n = n;
-  return cudaGetLastError();
-}
-
 // ---- diag((L L^T)^{-1}) for standard errors ---------------------
 // CTA J owns block column J of W = L^{-1}: W_JJ = Linv[J]; for I = J+1 .. : W_IJ = -Linv[I]
 // sum_{K=J}^{I-1} L_IK W_KJ (DMMA 64x64 tiles). The finished blocks W_KJ are kept, transposed, in
 // the (unused) strict upper triangle of A at block (J, K); columns of A^{-1} = W^T W have
 // diag_c = sum_r W_rc^2, summed in a fixed order (rows of a tile by shuffles, warps via smem, I
 // ascending). Block columns are independent; the first one carries the longest chain.
-__device__ __forceinline__ void tile_acc_xyT(const double (*Xs)[LDS], const double (*Ys)[LDS], double acc[2][4][2]) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int wr = (w >> 1) * 16, wc = (w & 1) * 32;
-  const int lr = lane >> 2, lk = lane & 3;
-#pragma unroll 4
-  for (int k0 = 0; k0 < NB; k0 += 4) {
-    double af[2], bf[4];
-#pragma unroll
-    for (int a = 0; a < 2; ++a) af[a] = Xs[wr + a * 8 + lr][k0 + lk];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) bf[b] = Ys[wc + b * 8 + lr][k0 + lk];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-  }
-}
-
 __global__ void __launch_bounds__(256) k_inv_diag(int n, double* A, int lda, const double* Linv, double* se) {
   extern __shared__ __align__(16) double dsm[];
   double(*Xs)[LDS] = reinterpret_cast<double(*)[LDS]>(dsm);
@@ -906,7 +839,115 @@ __global__ void __launch_bounds__(256) k_inv_diag(int n, double* A, int lda, con
 
 }  // namespace
 
-// Kernels that wait on other CTAs of their grid (k_chol_persist's grid barriers, k_trsv_wave's
+// Per-workspace factorisation state (one per library workspace, i.e. per device and stream).
+struct CholCtx {
+  int sms = 0, occ = 0;
+  double* Lt = nullptr;  // tile-major L [nt (nt+1)/2][NB][LDS]
+  size_t cap_lt = 0;     // tiles
+  double* LinvP = nullptr;  // [nt][NB][LDS]
+  double* Linv = nullptr;   // [nt][NB][NB]
+  double* ybuf = nullptr;   // [nt][NB]
+  int cap_nt = 0;
+  int* dflags = nullptr;  // k_chol_dag tile flags [nt (nt+1)/2], then its task counter
+  int depoch = 0;
+  int* flags = nullptr;  // k_trsv_wave block flags [nt]
+  int epoch = 0;
+  const double* factor = nullptr;  // row-major matrix holding the factor whose Linv blocks are current
+  int factor_n = 0;
+};
+
+namespace {
+
+constexpr size_t kDyn = 2 * NB * LDS * sizeof(double);
+constexpr size_t kDynR = 2 * NB * LDR * sizeof(double);
+constexpr size_t kDagSmem = kDagSmemDoubles * sizeof(double);
+constexpr size_t kBwdSmem = (2 * TS + NB * LDR) * sizeof(double);
+
+void set_attrs() {
+  static uint64_t attr_mask = 0;
+  set_once_per_device(attr_mask, [] {
+    cudaFuncSetAttribute(k_trtri_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynR);
+    cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
+    cudaFuncSetAttribute(k_trsv_bwd_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+    return cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDagSmem);
+  });
+}
+
+bool ensure_work(CholCtx& c, int n) {
+  set_attrs();
+  const int nt = (n + NB - 1) / NB;
+  const size_t ntri = (size_t)nt * (nt + 1) / 2;
+  if (!c.sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ, k_chol_dag, 256, kDagSmem) != cudaSuccess || c.occ < 1)
+      return false;
+  }
+  if (ntri > c.cap_lt) {
+    cudaFree(c.Lt);
+    cudaFree(c.dflags);
+    c.cap_lt = 0;
+    if (cudaMalloc(&c.Lt, ntri * TS * sizeof(double)) != cudaSuccess) return false;
+    if (cudaMalloc(&c.dflags, (ntri + 1) * sizeof(int)) != cudaSuccess) return false;
+    cudaMemset(c.dflags, 0, (ntri + 1) * sizeof(int));
+    c.depoch = 0;
+    c.cap_lt = ntri;
+  }
+  if (nt > c.cap_nt) {
+    cudaFree(c.LinvP);
+    cudaFree(c.Linv);
+    cudaFree(c.ybuf);
+    cudaFree(c.flags);
+    c.cap_nt = 0;
+    if (cudaMalloc(&c.LinvP, (size_t)nt * TS * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c.Linv, (size_t)nt * NB * NB * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c.ybuf, (size_t)nt * NB * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c.flags, (size_t)nt * sizeof(int)) != cudaSuccess)
+      return false;
+    cudaMemset(c.flags, 0, nt * sizeof(int));
+    c.epoch = 0;
+    c.cap_nt = nt;
+  }
+  return true;
+}
+
+// the wavefront triangular solve on a row-major factor L (lda)
+cudaError_t launch_wave(CholCtx& c, int n, const double* L, int lda, const double* xin, double* x, int upper,
+                        cudaStream_t st) {
+  const int nblk = (n + NB - 1) / NB;
+  int epoch = ++c.epoch;
+  const double* Linv = c.Linv;
+  int* flags = c.flags;
+  void* args[] = {(void*)&n,   (void*)&L, (void*)&lda,   (void*)&Linv,  (void*)&xin,
+                  (void*)&x, (void*)&flags, (void*)&epoch, (void*)&upper};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_trsv_wave, dim3(nblk), dim3(256), args, 0, st);
+  count_launch();
+  return e;
+}
+
+// the tile-DAG factorisation of the row-major A (read only); with b, also ybuf = L^{-1} b (and, for
+// one tile, x = A^{-1} b)
+cudaError_t factor_dag(CholCtx& c, int n, const double* A, int lda, int* info, const double* b, double* x,
+                       cudaStream_t st) {
+  const int nt = (n + NB - 1) / NB;
+  const int ntask = nt * (nt + 1) / 2 - (nt - 1);  // the sub-diagonal tiles ride with the diagonal tasks
+  const int grid = std::min(ntask, c.sms * c.occ);
+  int epoch = ++c.depoch;
+  int* next_task = c.dflags + c.cap_lt;  // past every flag slot (never read as a flag)
+  cudaMemsetAsync(info, 0, sizeof(int), st);
+  cudaMemsetAsync(next_task, 0, sizeof(int), st);
+  void* args[] = {(void*)&n,  (void*)&nt,   (void*)&A,    (void*)&lda,  (void*)&c.Lt,    (void*)&c.LinvP,
+                  (void*)&c.Linv, (void*)&b, (void*)&c.ybuf, (void*)&x, (void*)&info, (void*)&c.dflags,
+                  (void*)&epoch, (void*)&next_task};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_chol_dag, dim3(grid), dim3(256), args, kDagSmem, st);
+  count_launch();
+  return e;
+}
+
+}  // namespace
+
+// Kernels that wait on other CTAs of their grid (k_chol_dag's tile flags, k_trsv_wave's block
 // flags) are launched cooperatively; two such grids running at once from different workspaces
 // could each hold part of the SMs and wait forever. Every factor / solve section therefore runs
 // under one process-wide lock and drains its stream before releasing it.
@@ -925,45 +966,54 @@ CholCtx* chol_ctx_create() { return new CholCtx(); }
 
 void chol_ctx_destroy(CholCtx* c) {
   if (!c) return;
-  cudaFree(c->bar);
+  cudaFree(c->Lt);
+  cudaFree(c->dflags);
+  cudaFree(c->LinvP);
   cudaFree(c->Linv);
+  cudaFree(c->ybuf);
   cudaFree(c->flags);
-  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
-  if (c->start) cudaEventDestroy(c->start);
-  if (c->done) cudaEventDestroy(c->done);
-  if (c->side) cudaStreamDestroy(c->side);
   delete c;
 }
 
 cudaError_t launch_cholesky(CholCtx* cc, int n, double* A, int lda, int* info, cudaStream_t st) {
   CoopSection cs(st);
-  return factor(*cc, n, A, lda, info, nullptr, st);
+  if (!ensure_work(*cc, n)) return cudaErrorMemoryAllocation;
+  cudaError_t e = factor_dag(*cc, n, A, lda, info, nullptr, nullptr, st);
+  if (e != cudaSuccess) return e;
+  k_untile<<<n, 256, 0, st>>>(n, cc->Lt, A, lda);
+  count_launch();
+  cc->factor = A;
+  cc->factor_n = n;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_cholesky_solve_fused(CholCtx* cc, int n, double* A, int lda, int* info, const double* b,
                                         double* x, cudaStream_t st) {
   CoopSection cs(st);
-  if (x != b) cudaMemcpyAsync(x, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-  cudaError_t e = factor(*cc, n, A, lda, info, x, st);
-  if (e != cudaSuccess) return e;
-  return launch_wave(*cc, n, A, lda, x, 1, st);
+  if (!ensure_work(*cc, n)) return cudaErrorMemoryAllocation;
+  cc->factor = nullptr;  // A keeps -H: the factor lives in the tile-major copy only
+  cc->factor_n = 0;
+  cudaError_t e = factor_dag(*cc, n, A, lda, info, b, x, st);
+  if (e != cudaSuccess || n <= NB) return e;
+  const int nblk = (n + NB - 1) / NB;
+  int epoch = ++cc->epoch;
+  void* args[] = {(void*)&n, (void*)&cc->Lt, (void*)&cc->LinvP, (void*)&cc->ybuf, (void*)&x, (void*)&cc->flags,
+                  (void*)&epoch};
+  e = cudaLaunchCooperativeKernel((const void*)k_trsv_bwd_tiles, dim3(nblk), dim3(256), args, kBwdSmem, st);
+  count_launch();
+  return e;
 }
 
 cudaError_t launch_inv_diag_sqrt(CholCtx* cc, int n, double* L, int lda, double* se, cudaStream_t st) {
-  CholCtx& g_cw = *cc;
-  set_attrs();
-  if (!ensure_work(g_cw, n)) return cudaErrorMemoryAllocation;
-  if (g_cw.factor != L || g_cw.factor_n != n) {  // factor from elsewhere: build its Linv blocks
-    k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, g_cw.Linv);
+  CholCtx& c = *cc;
+  if (!ensure_work(c, n)) return cudaErrorMemoryAllocation;
+  if (c.factor != L || c.factor_n != n) {  // factor from elsewhere: build its Linv blocks
+    k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, c.Linv);
     count_launch();
-    g_cw.factor = L;
-    g_cw.factor_n = n;
+    c.factor = L;
+    c.factor_n = n;
   }
-  static uint64_t attr_mask = 0;
-  set_once_per_device(attr_mask, [] {
-    return cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
-  });
-  k_inv_diag<<<(n + NB - 1) / NB, 256, kDyn, st>>>(n, L, lda, g_cw.Linv, se);
+  k_inv_diag<<<(n + NB - 1) / NB, 256, kDyn, st>>>(n, L, lda, c.Linv, se);
   count_launch();
   return cudaGetLastError();
 }
@@ -976,19 +1026,17 @@ void chol_forget_factor(CholCtx* cc) {
 cudaError_t launch_chol_solve(CholCtx* cc, int n, const double* L, int lda, const double* b, double* x,
                               cudaStream_t st) {
   CoopSection cs(st);
-  CholCtx& g_cw = *cc;
-  set_attrs();
-  if (!ensure_work(g_cw, n)) return cudaErrorMemoryAllocation;
-  if (g_cw.factor != L || g_cw.factor_n != n) {  // factor from elsewhere: build its Linv blocks
-    k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, g_cw.Linv);
+  CholCtx& c = *cc;
+  if (!ensure_work(c, n)) return cudaErrorMemoryAllocation;
+  if (c.factor != L || c.factor_n != n) {  // factor from elsewhere: build its Linv blocks
+    k_trtri_blocks<<<(n + NB - 1) / NB, 256, kDynR, st>>>(n, L, lda, c.Linv);
     count_launch();
-    g_cw.factor = L;
-    g_cw.factor_n = n;
+    c.factor = L;
+    c.factor_n = n;
   }
-  if (x != b) cudaMemcpyAsync(x, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-  cudaError_t e = launch_wave(g_cw, n, L, lda, x, 0, st);
+  cudaError_t e = launch_wave(c, n, L, lda, b, x, 0, st);
   if (e != cudaSuccess) return e;
-  return launch_wave(g_cw, n, L, lda, x, 1, st);
+  return launch_wave(c, n, L, lda, x, x, 1, st);
 }
 
 }  // namespace mnl

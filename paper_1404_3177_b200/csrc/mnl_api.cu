@@ -795,6 +795,21 @@ int mnl_cholesky_solve(int32_t n, const double* L, const double* b, double* x, v
   return MNL_OK;
 }
 
+int mnl_spd_solve(int32_t n, const double* A, const double* b, double* x, void* stream) {
+  g_launches = 0;
+  if (n < 1 || !A || !b || !x) return MNL_ERR_ARG;
+  Session s(stream);
+  if (s.rc) return s.rc;
+  Workspace& W = *s.W;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (launch_cholesky_solve_fused(W.chol, n, const_cast<double*>(A), n, W.info, b, x, st) != cudaSuccess)
+    return MNL_ERR_CUDA;
+  int info = 0;
+  cudaMemcpyAsync(&info, W.info, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return MNL_ERR_CUDA;
+  return info ? MNL_ERR_NOT_SPD : MNL_OK;
+}
+
 int mnl_sym_pack(int32_t n, const double* H, double* packed, void* stream) {
   g_launches = 0;
   if (n < 1 || !H || !packed) return MNL_ERR_ARG;

@@ -210,35 +210,40 @@ def test_cholesky_and_solve(n):
     assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref)
 
 
-@pytest.mark.parametrize("n", [3000, 3100])
+@pytest.mark.parametrize("n", [3000, 3100, 5049])
 def test_cholesky_large(n):
-    """Large n on the default (persistent, single cooperative launch) factorisation."""
+    """Large n (c4's n_p = 5049 included) on the tile-DAG factorisation."""
     test_cholesky_and_solve(n)
 
 
-def test_cholesky_streams_path_small_and_fit(tmp_path):
-    """The multi-kernel (two-stream lookahead) factorisation forced by MNL_CHOL_STREAMS (read once per
-    process): a fresh interpreter factors n = 700 and n = 3100, compared with LAPACK."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, json, sys\n"
-        "sys.path.insert(0, %r)\n"
-        "import paper_1404_3177_b200 as M, datagen\n"
-        "errs = []\n"
-        "for n in (700, 3100):\n"
-        "    rng = np.random.default_rng(7)\n"
-        "    B = rng.standard_normal((n, n + 3)); A = B @ B.T / n + np.eye(n) * 0.1\n"
-        "    Ad = torch.from_numpy(A).cuda(); assert M.mnl_cholesky(Ad) == M.MNL_OK\n"
-        "    L = np.tril(Ad.cpu().numpy()); Lr = np.linalg.cholesky(A)\n"
-        "    errs.append(float(np.max(np.abs(L - Lr)) / np.max(np.abs(Lr))))\n"
-        "print(json.dumps({'err': max(errs)}))\n"
-    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MNL_CHOL_STREAMS="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stderr[-2000:]
-    err = json.loads(out.stdout.strip().splitlines()[-1])["err"]
-    assert err <= 1e-11
+@pytest.mark.parametrize("n", [1, 2, 18, 63, 64, 65, 127, 128, 129, 189, 700, 969, 1779, 3100, 5049])
+def test_spd_solve_fused(n):
+    """The Newton step's own path (factor with the forward solve fused into the diagonal tiles, then the
+    backward wavefront; one kernel for n <= 64) against LAPACK, A untouched, x aliasing b allowed;
+    n = 18 / 189 / 969 / 1779 / 5049 are the n_p of c1 / c2 / c3 / c5 / c4."""
+    rng = np.random.default_rng(1000 + n)
+    B = rng.standard_normal((n, n + 5))
+    A = B @ B.T / n + np.eye(n) * 0.05
+    b = rng.standard_normal(n)
+    x_ref = np.linalg.solve(A, b)
+    Ad, bd = dev(A), dev(b)
+    x = M.mnl_spd_solve(Ad, bd).cpu().numpy()
+    assert np.linalg.norm(x - x_ref) <= 1e-9 * np.linalg.norm(x_ref), n
+    assert np.array_equal(Ad.cpu().numpy(), A)
+    x2 = M.mnl_spd_solve(Ad, bd).cpu().numpy()  # deterministic run to run
+    assert np.array_equal(x, x2)
+    # in place (x aliases b) through the raw ABI
+    rc = M.load().mnl_spd_solve(n, Ad.data_ptr(), bd.data_ptr(), bd.data_ptr(), None)
+    assert rc == M.MNL_OK and np.array_equal(bd.cpu().numpy(), x)
+
+
+def test_spd_solve_not_spd():
+    for n, bad in ((40, 17), (300, 250)):
+        A = np.eye(n)
+        A[bad, bad] = -1.0
+        with pytest.raises(M.MnlError) as e:
+            M.mnl_spd_solve(dev(A), dev(np.ones(n)))
+        assert e.value.code == M.MNL_ERR_NOT_SPD
 
 
 def test_cholesky_not_spd():
