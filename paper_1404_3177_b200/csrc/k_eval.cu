@@ -89,6 +89,18 @@ __device__ __forceinline__ double exp_shifted(double x) {
   return x < -708.0 ? 0.0 : e * scale;
 }
 
+// 1 / s for the softmax row sums s >= ~1 (the shifted maximum contributes ~1): the hardware
+// approximate reciprocal refined by two Newton steps (relative error <= ~1 ulp), instead of the
+// ~15-instruction IEEE division.
+__device__ __forceinline__ double recip_ge1(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  double e = fma(-s, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-s, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Sums of 8 per-lane values over the warp (reduce-scatter by butterfly): returns, in every lane, the
 // warp sum of component (lane >> 2) & 7.
 __device__ __forceinline__ double warp_sum8(const double (&v)[8], int lane) {
@@ -231,7 +243,7 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
       ssum = warp_sum(ssum);
       const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
       if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
-      const double inv_s = 1.0 / ssum;
+      const double inv_s = recip_ge1(ssum);
   #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
@@ -411,7 +423,7 @@ __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us,
       ssum = warp_sum(ssum);
       const double uy = __shfl_sync(0xffffffffu, uy_l, y & 31);
       if (lane == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));  // one lane per individual
-      const double inv_s = 1.0 / ssum;
+      const double inv_s = recip_ge1(ssum);
   #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
@@ -547,7 +559,7 @@ constexpr int YZS_F = 16, YZS_D = 8;  // register capacity of the YZS path (gamm
 // NI consecutive rows of this warp (ii0 ..), computed together so that their dependency chains
 // (loads -> utilities -> max / sum shuffles -> exp -> gradient sums) interleave. Lane k holds
 // alternatives k + 32 kk. Reads its rows' staged Y [K][f] and Z [K][d] from the ring.
-template <int KPL, bool HV, int NI>
+template <int KPL, bool HV, int NI, bool WP>
 __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const int* ch_t,
                                          const double* alpha, const double* gamma,
                                          double (&gam)[YZS_F], double (&alp)[KPL][YZS_D], double& l_s, double& l_c,
@@ -739,7 +751,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
         neu_add(l_s, l_c, st.lg_a - log(st.lg_s));
         st.lg_cnt = 0;
       }
-      const double inv_s = 1.0 / ssum[j];
+      const double inv_s = recip_ge1(ssum[j]);
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
         const int k = lane + 32 * kk;
@@ -747,7 +759,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
         u[j][kk] = P;
         r[j][kk] = kok[kk] ? ((k == y[j] ? 1.0 : 0.0) - P) : 0.0;
         if (k < KPS) Rs[(ii0 + j) * KPS + k] = r[j][kk];
-        if (A.writeP && kok[kk]) A.Pr[gi[j] * A.ldP + k] = P;
+        if (WP && kok[kk]) A.Pr[gi[j] * A.ldP + k] = P;
       }
     }
   }
@@ -781,8 +793,10 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
             for (int j = 0; j < NI; ++j)
 #pragma unroll
               for (int kk = 0; kk < KPL; ++kk) {
-                yb[j][e - e8 + 2 * h] = fma(u[j][kk], v[h][j][kk].x, yb[j][e - e8 + 2 * h]);
-                yb[j][e - e8 + 2 * h + 1] = fma(u[j][kk], v[h][j][kk].y, yb[j][e - e8 + 2 * h + 1]);
+                if constexpr (WP) {  // ybar only for the Hessian pass
+                  yb[j][e - e8 + 2 * h] = fma(u[j][kk], v[h][j][kk].x, yb[j][e - e8 + 2 * h]);
+                  yb[j][e - e8 + 2 * h + 1] = fma(u[j][kk], v[h][j][kk].y, yb[j][e - e8 + 2 * h + 1]);
+                }
                 g0 = fma(v[h][j][kk].x, r[j][kk], g0);
                 g1 = fma(v[h][j][kk].y, r[j][kk], g1);
               }
@@ -791,7 +805,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
           }
         }
       }
-      if (!HV && A.writeP) {
+      if constexpr (!HV && WP) {
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
           const int t = (lane >> 2) & 7;  // the component warp_sum8 leaves in this lane
@@ -850,9 +864,14 @@ __device__ __forceinline__ void phase_e_smem(const EvalArgs& A, double* Rs, cons
     for (int k = lane; k < KPS; k += 32) Rs[ii * KPS + k] = 0.0;
   int jj = 0;
   if constexpr (YZS_R >= 2)
-    for (; jj + 2 <= n_mine; jj += 2) yzs_rows<KPL, HV, 2>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
-  if (jj < n_mine)
-    yzs_rows<KPL, HV, 1>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+    for (; jj + 2 <= n_mine; jj += 2) {
+      if (!HV && A.writeP) yzs_rows<KPL, HV, 2, true>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+      else yzs_rows<KPL, HV, 2, false>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+    }
+  if (jj < n_mine) {
+    if (!HV && A.writeP) yzs_rows<KPL, HV, 1, true>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+    else yzs_rows<KPL, HV, 1, false>(A, Rs, ch_t, alpha, gamma, gam, alp, l_s, l_c, i0, ib + jj, KPS, w, lane, ring_w, st);
+  }
 }
 
 template <int KPL, int CM_MAX, bool HV, bool YZS>
@@ -995,10 +1014,11 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     // ---------------- phase B: u = X~ B on DMMA, then softmax / loglik / residuals ----------------
     // YZS (16-row tiles): the warps split 2 row blocks x NG groups of alternative blocks (groups
     // beyond NBN idle)
-    constexpr int NG = NWK / 2;
+    constexpr int RB = YZS_TI / 8;  // YZS: 8-row blocks of the tile
+    constexpr int NG = NWK / RB;
     constexpr int NBW = YZS ? (NBN >= NG ? NBN / NG : 1) : NBN;  // alternative blocks per warp
-    const int il = YZS ? 8 * (w & 1) + c8 : (8 * w + c8) % TI;  // this lane's individual (C-fragment row)
-    const int nb0 = YZS ? (w >> 1) * NBW : 0;
+    const int il = YZS ? 8 * (w % RB) + c8 : (8 * w + c8) % TI;  // this lane's individual (C-fragment row)
+    const int nb0 = YZS ? (w / RB) * NBW : 0;
     const bool in_b = YZS ? nb0 < NBN : 8 * w < TI;  // warps without a block skip phase B
     double u[NBN][2];
 #pragma unroll
@@ -1095,7 +1115,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     uy += __shfl_xor_sync(0xffffffffu, uy, 1);
     uy += __shfl_xor_sync(0xffffffffu, uy, 2);
     if (valid && r4 == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));
-    const double inv_s = 1.0 / ssum;
+    const double inv_s = recip_ge1(ssum);
     double* Rrow = Rs + il * KPS;
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb) {
