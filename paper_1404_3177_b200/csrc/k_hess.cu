@@ -50,6 +50,7 @@ struct GemmParams {
   const ColDesc* descB;
   int tilesM, tilesN, splits;
   int64_t nchunks;
+  int64_t cstride;  // chunk dimension of the fragment buffers (k_pipe_gemm; = nchunks unless N-slabbed)
   double* C;
   int ldc;
   int64_t split_stride;
@@ -349,7 +350,8 @@ struct FragArgs {
   const ColDesc* desc;
   double* out;
   int tiles, BT, KC;
-  int64_t nchunks;
+  int64_t nchunks;  // chunk dimension of the output buffers (the grid covers count <= nchunks chunks)
+  int64_t c_base;   // first individual chunk of this launch (N-slab)
   int nseg;
   const double* seg_ptr[3];
   int seg_ld[3];
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(256) k_frag(const FragArgs F) {
     if (sg >= F.nseg) break;
     const int n2 = RH * F.seg_ld[sg] / 2;  // leading dimensions are even
     const double2* src =
-        reinterpret_cast<const double2*>(F.seg_ptr[sg] + (c * F.KC + h * RH) * (int64_t)F.seg_ld[sg]);
+        reinterpret_cast<const double2*>(F.seg_ptr[sg] + ((F.c_base + c) * F.KC + h * RH) * (int64_t)F.seg_ld[sg]);
     double2* dst = reinterpret_cast<double2*>(rs + F.seg_off[sg] / F.nh);  // seg_off: offsets for KC rows
     for (int e = threadIdx.x; e < n2; e += blockDim.x) dst[e] = src[e];
   }
@@ -484,8 +486,8 @@ __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                      "r"((unsigned)((GA_D + GB_D) * 8))
                      : "memory");
-        bulk_g2s(st, afrag + ((int64_t)tm * P.nchunks + c) * GA_D, GA_D * 8, &full[s]);
-        bulk_g2s(st + GA_D, P.bfrag + ((int64_t)tn * P.nchunks + c) * GB_D, GB_D * 8, &full[s]);
+        bulk_g2s(st, afrag + ((int64_t)tm * P.cstride + c) * GA_D, GA_D * 8, &full[s]);
+        bulk_g2s(st + GA_D, P.bfrag + ((int64_t)tn * P.cstride + c) * GB_D, GB_D * 8, &full[s]);
         if (++s == S) { s = 0; ph ^= 1u; }
       }
     }
@@ -794,6 +796,11 @@ struct GemmJob {
   int dnseg = 0, dseg_id[3] = {0, 0, 0};  // stage layout the descriptors were built against
   bool agen = true;  // A operand uses the general generator form (J1)
   int MA, MB, tilesM, tilesN, splits;
+  // N-slabs (k_pipe_gemm jobs whose whole-N operands do not fit): the fragment buffers hold
+  // slab_chunks chunks; the operands are materialised and consumed one slab at a time, each slab
+  // writing its own split partials (nslab x splits, reduced in a fixed order)
+  int64_t slab_chunks = 0;
+  int nslab = 1;
   int skip_off = -1;  // GemmParams::skip_off
   int64_t nchunks;
   ColDesc* dA = nullptr;  // device
@@ -875,7 +882,9 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   J.tilesM = (J.MA + BM - 1) / BM;
   J.tilesN = (J.MB + BN - 1) / BN;
   J.nchunks = pk.Npad / KC;
-  J.splits = choose_splits(J.tilesM * J.tilesN, J.nchunks, sms, 4);
+  if (J.slab_chunks <= 0 || J.slab_chunks >= J.nchunks) J.slab_chunks = J.nchunks;
+  J.nslab = (int)((J.nchunks + J.slab_chunks - 1) / J.slab_chunks);
+  J.splits = choose_splits(J.tilesM * J.tilesN, J.slab_chunks, sms, 4);
   J.ldc = J.tilesN * BN;
   J.split_stride = (int64_t)J.tilesM * BM * J.ldc;
   J.nseg = nseg;
@@ -896,9 +905,9 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   cudaMemcpy(J.dA, hA.data(), hA.size() * sizeof(ColDesc), cudaMemcpyHostToDevice);
   cudaMemcpy(J.dB, hB.data(), hB.size() * sizeof(ColDesc), cudaMemcpyHostToDevice);
   const size_t cbytes = (size_t)J.split_stride * sizeof(double);
-  if (cudaMalloc(&J.Cpart, cbytes * J.splits) != cudaSuccess) return false;
+  if (cudaMalloc(&J.Cpart, cbytes * J.splits * J.nslab) != cudaSuccess) return false;
   if (cudaMalloc(&J.Cred, cbytes) != cudaSuccess) return false;
-  *bytes += cbytes * (J.splits + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
+  *bytes += cbytes * (J.splits * J.nslab + 1) + (hA.size() + hB.size()) * sizeof(ColDesc);
   if (pipe) return true;  // k_pipe_gemm: no generator staging
   const size_t lim = 220 * 1024;
   for (J.nraw = 2; J.nraw >= 1; --J.nraw) {  // prefer two raw stages; one if the stage is large
@@ -938,6 +947,39 @@ static double* alloc_frag(int tiles, int width, const Packed& pk, size_t* bytes)
   }
   *bytes += fb;
   return p;
+}
+
+// Fragment buffer of `tiles` operand tiles over `chunks` chunks of KC individuals (an N-slab).
+static double* alloc_frag_chunks(int tiles, int width, int64_t chunks, int KC, size_t* bytes) {
+  const size_t fb = (size_t)tiles * width * (size_t)chunks * KC * sizeof(double);
+  double* p = nullptr;
+  if (cudaMalloc(&p, fb) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  *bytes += fb;
+  return p;
+}
+
+// Chunks per N-slab for materialised operands of `per_chunk` bytes per chunk: all of them when they
+// fit in min(48 GB, free - 4 GB), else the balanced slab size under that budget; 0 when even a
+// 64-chunk slab does not fit (the operands are then generated in-kernel). MNL_FRAG_SLAB_CHUNKS
+// forces a slab size (tests of the slabbed path at small N).
+static int64_t frag_slab_chunks(size_t per_chunk, int64_t nch) {
+  if (const char* e = getenv("MNL_FRAG_SLAB_CHUNKS")) {
+    const int64_t f = atoll(e);
+    if (f > 0) return std::min<int64_t>(f, nch);
+  }
+  if (getenv("MNL_NO_MATERIALISE")) return 0;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t reserve = (size_t)4 << 30, cap = (size_t)48 << 30;
+  const size_t budget = std::min(cap, free_b > reserve ? free_b - reserve : (size_t)0);
+  const int64_t fit = (int64_t)(budget / per_chunk);
+  if (fit >= nch) return nch;
+  if (fit < 64) return 0;
+  const int64_t nslab = (nch + fit - 1) / fit;
+  return (nch + nslab - 1) / nslab;
 }
 
 // Tile widths k_pipe_gemm is instantiated for: the widest of {128, 112, 96, 64, 48} within 5% of the
@@ -984,20 +1026,40 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       // vech >= 256. Otherwise materialise only the design-only B (once per design) if it fits.
       GemmJob& J = hp->j1;
       const int tilesM = (int)((A.size() + BM - 1) / BM);
-      double* af = (KC == 32 && nv >= 256 && frag_fits && !getenv("MNL_NO_PIPE")) ? alloc_frag(tilesM, BM, pk, &bytes) : nullptr;
-      int bn1 = split ? 128 : (af ? choose_bn_pipe(nv) : choose_bn(nv));
-      double* bf = frag_fits ? alloc_frag((hp->n1a + bn1 - 1) / bn1, bn1, pk, &bytes) : nullptr;
-      if (af && !bf) {
-        cudaFree(af);
-        af = nullptr;
+      const int64_t nch = pk.Npad / KC;
+      const bool pipe_ok = KC == 32 && nv >= 256 && frag_fits && !getenv("MNL_NO_PIPE");
+      int bn1 = split ? 128 : (pipe_ok ? choose_bn_pipe(nv) : choose_bn(nv));
+      const int bnt_p = split ? choose_bn_pipe(rem) : 0;
+      double *af = nullptr, *bf = nullptr, *tbf = nullptr;
+      int64_t slab = 0;
+      if (pipe_ok) {  // both operands materialised, whole-N or in N-slabs of the same size
+        const size_t per_chunk =
+            ((size_t)tilesM * BM + (size_t)((hp->n1a + bn1 - 1) / bn1) * bn1 + bnt_p) * KC * sizeof(double);
+        slab = frag_slab_chunks(per_chunk, nch);
+        if (slab > 0) {
+          af = alloc_frag_chunks(tilesM, BM, slab, KC, &bytes);
+          bf = af ? alloc_frag_chunks((hp->n1a + bn1 - 1) / bn1, bn1, slab, KC, &bytes) : nullptr;
+          tbf = (bf && split) ? alloc_frag_chunks(1, bnt_p, slab, KC, &bytes) : nullptr;
+          if (!bf || (split && !tbf)) {
+            cudaFree(af);
+            cudaFree(bf);
+            cudaFree(tbf);
+            af = bf = tbf = nullptr;
+          }
+        }
+      }
+      if (!af) {  // weights generated in-kernel; the design-only B materialised whole if it fits
+        slab = 0;
         if (!split) bn1 = choose_bn(nv);
+        bf = frag_fits ? alloc_frag((hp->n1a + bn1 - 1) / bn1, bn1, pk, &bytes) : nullptr;
       }
       J.afrag = af;
       J.bfrag = bf;
       J.own_afrag = true;
       J.mat_a = af != nullptr;
       J.mat_b = bf != nullptr;
-      J.b_design = true;
+      J.slab_chunks = slab;
+      J.b_design = slab == 0 || slab >= nch;  // B cached across evaluations only when whole-N
       J.dnseg = 2;
       J.dseg_id[0] = 0;
       J.dseg_id[1] = 1;
@@ -1007,14 +1069,13 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       hp->has_j1b = split;
       if (good && split) {
         GemmJob& T = hp->j1b;
-        int bnt = J.mat_a ? choose_bn_pipe(rem) : choose_bn(rem);
-        double* tbf = J.mat_a ? alloc_frag(1, bnt, pk, &bytes) : nullptr;  // the tail shares j1's weights
-        if (J.mat_a && !tbf) bnt = choose_bn(rem);
+        const int bnt = J.mat_a ? bnt_p : choose_bn(rem);
         T.bfrag = tbf;
-        T.afrag = tbf ? J.afrag : nullptr;
+        T.afrag = tbf ? J.afrag : nullptr;  // the tail shares j1's weights (slab by slab)
         T.own_afrag = tbf == nullptr;
         T.mat_a = T.mat_b = tbf != nullptr;
-        T.b_design = true;
+        T.slab_chunks = J.slab_chunks;
+        T.b_design = J.b_design;
         T.dnseg = 2;
         T.dseg_id[0] = 0;
         T.dseg_id[1] = 1;
@@ -1177,6 +1238,7 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   P.tilesN = J.tilesN;
   P.splits = J.splits;
   P.nchunks = J.nchunks;
+  P.cstride = J.nchunks;
   P.C = J.Cpart;
   P.ldc = J.ldc;
   P.split_stride = J.split_stride;
@@ -1210,15 +1272,16 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
 }
 
 template <int BN>
-static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaStream_t st) {
+static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaStream_t st, int slab) {
   constexpr int KC = 32, S = (200 * 1024) / ((KC / 4) * (BM / 16 + BN / 16) * 64 * 8);  // stages in ~200 KB
   constexpr size_t smem = (size_t)S * (KC / 4) * (BM / 16 + BN / 16) * 64 * sizeof(double);
   GemmParams P{};
   P.tilesM = J.tilesM;
   P.tilesN = J.tilesN;
   P.splits = J.splits;
-  P.nchunks = J.nchunks;
-  P.C = J.Cpart;
+  P.nchunks = std::min<int64_t>(J.slab_chunks, J.nchunks - (int64_t)slab * J.slab_chunks);  // this slab's
+  P.cstride = J.slab_chunks;
+  P.C = J.Cpart + (size_t)slab * J.splits * J.split_stride;
   P.ldc = J.ldc;
   P.split_stride = J.split_stride;
   P.bfrag = J.bfrag;
@@ -1236,15 +1299,16 @@ static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaSt
   return cudaGetLastError();
 }
 
-static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
-                           cudaEvent_t after_gemm = nullptr) {
+// the GEMM of one job (of its N-slab `slab` when the operands are slabbed), without the reduction
+static cudaError_t run_gemm_only(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
+                                 int slab = 0) {
   cudaError_t e;
   if (J.mat_a) {
-    if (J.BN == 128) e = run_pipe<128>(J, counter, sms, st);
-    else if (J.BN == 96) e = run_pipe<96>(J, counter, sms, st);
-    else if (J.BN == 112) e = run_pipe<112>(J, counter, sms, st);
-    else if (J.BN == 64) e = run_pipe<64>(J, counter, sms, st);
-    else e = run_pipe<48>(J, counter, sms, st);
+    if (J.BN == 128) e = run_pipe<128>(J, counter, sms, st, slab);
+    else if (J.BN == 96) e = run_pipe<96>(J, counter, sms, st, slab);
+    else if (J.BN == 112) e = run_pipe<112>(J, counter, sms, st, slab);
+    else if (J.BN == 64) e = run_pipe<64>(J, counter, sms, st, slab);
+    else e = run_pipe<48>(J, counter, sms, st, slab);
   } else if (J.agen) {  // J1: weights P_k (delta_kl - P_l) x vech(x~ x~^T)
     if (J.BN == 128 && J.mat_b) e = J.KC == 32 ? run_gemm<128, 32, 8, true, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true, true>(J, pk, counter, sms, st);
     else if (J.BN == 128) e = J.KC == 32 ? run_gemm<128, 32, 8, true>(J, pk, counter, sms, st) : run_gemm<128, 16, 8, true>(J, pk, counter, sms, st);
@@ -1257,17 +1321,28 @@ static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter
     else if (J.BN == 96) e = J.KC == 32 ? run_gemm<96, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<96, 16, 8, false>(J, pk, counter, sms, st);
     else e = J.KC == 32 ? run_gemm<64, 32, 8, false>(J, pk, counter, sms, st) : run_gemm<64, 16, 8, false>(J, pk, counter, sms, st);
   }
-  if (e != cudaSuccess) return e;
-  if (after_gemm) cudaEventRecord(after_gemm, st);
+  return e;
+}
+
+// fixed-order sum of the job's split (x slab) partials
+static cudaError_t reduce_job(const GemmJob& J, cudaStream_t st) {
   const int64_t n = J.split_stride;
   const int blocks = (int)std::min<int64_t>((n / 2 + 255) / 256, 148 * 8);
-  k_reduce_splits<<<blocks, 256, 0, st>>>(J.Cred, J.Cpart, n, J.splits, J.split_stride);
+  k_reduce_splits<<<blocks, 256, 0, st>>>(J.Cred, J.Cpart, n, J.splits * J.nslab, J.split_stride);
   count_launch();
   return cudaGetLastError();
 }
 
+static cudaError_t run_job(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
+                           cudaEvent_t after_gemm = nullptr) {
+  cudaError_t e = run_gemm_only(J, pk, counter, sms, st);
+  if (e != cudaSuccess) return e;
+  if (after_gemm) cudaEventRecord(after_gemm, st);
+  return reduce_job(J, st);
+}
+
 static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStream_t st, bool both = false,
-                        const GemmJob* tailB = nullptr) {
+                        const GemmJob* tailB = nullptr, int slab = 0) {
   FragArgs F;
   F.desc2 = nullptr;
   F.out2 = nullptr;
@@ -1289,7 +1364,9 @@ static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStr
   F.tiles = a_side ? J.tilesM : J.tilesN;
   F.BT = a_side ? BM : J.BN;
   F.KC = J.KC;
-  F.nchunks = J.nchunks;
+  F.nchunks = J.slab_chunks;  // buffer stride; this launch covers slab `slab`
+  F.c_base = (int64_t)slab * J.slab_chunks;
+  const int64_t count = std::min<int64_t>(J.slab_chunks, J.nchunks - F.c_base);
   F.nseg = J.dnseg;
   int off = 0;
   for (int sg = 0; sg < J.dnseg; ++sg) {
@@ -1304,7 +1381,7 @@ static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStr
     return cudaFuncSetAttribute(k_frag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFragSmemMax);
   });
   F.nh = frag_nh((size_t)off);  // > 0: the plan materialises only operands whose stage fits
-  k_frag<<<(unsigned)(F.nh * J.nchunks), 256, (size_t)off / F.nh * sizeof(double), st>>>(F);
+  k_frag<<<(unsigned)(F.nh * count), 256, (size_t)off / F.nh * sizeof(double), st>>>(F);
   count_launch();
 }
 
@@ -1316,6 +1393,7 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
                               hp->has_j2b ? &hp->j2b : nullptr};
     for (const GemmJob* J : jobs) {
       if (!J) continue;
+      if (J->nslab > 1) continue;  // N-slabbed J1: materialised slab by slab below
       if (J->mat_a && J->mat_b && J->own_afrag && !J->b_design) {  // J2: A, B (+ the tail's B), one pass
         launch_frag(*J, pk, true, st, true, (J == &hp->j2 && hp->has_j2b) ? &hp->j2b : nullptr);
         continue;
@@ -1329,14 +1407,32 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
     if (e != cudaSuccess) return e;
   }
   cudaEventRecord(hp->ev[0], st);
-  cudaError_t e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
-  if (e != cudaSuccess) return e;
-  cudaEventRecord(hp->ev[2], st);
-  if (hp->has_j1b) {
-    e = run_job(hp->j1b, pk, hp->counters, hp->sms, st, hp->ev[3]);
+  cudaError_t e = cudaSuccess;
+  if (hp->j1.nslab > 1) {
+    // N-slabs: per slab, both operands (and the tail's B) materialised from one staging of the
+    // rows, then the main and tail GEMMs over that slab; the slab partials are reduced at the end
+    // (the operand time is then counted in the GEMM phases)
+    for (int sl = 0; sl < hp->j1.nslab && e == cudaSuccess; ++sl) {
+      launch_frag(hp->j1, pk, true, st, true, hp->has_j1b ? &hp->j1b : nullptr, sl);
+      e = run_gemm_only(hp->j1, pk, hp->counters, hp->sms, st, sl);
+      if (e == cudaSuccess && hp->has_j1b) e = run_gemm_only(hp->j1b, pk, hp->counters, hp->sms, st, sl);
+    }
     if (e != cudaSuccess) return e;
-  } else {
+    cudaEventRecord(hp->ev[1], st);
+    if ((e = reduce_job(hp->j1, st)) != cudaSuccess) return e;
+    cudaEventRecord(hp->ev[2], st);
     cudaEventRecord(hp->ev[3], st);
+    if (hp->has_j1b && (e = reduce_job(hp->j1b, st)) != cudaSuccess) return e;
+  } else {
+    e = run_job(hp->j1, pk, hp->counters, hp->sms, st, hp->ev[1]);
+    if (e != cudaSuccess) return e;
+    cudaEventRecord(hp->ev[2], st);
+    if (hp->has_j1b) {
+      e = run_job(hp->j1b, pk, hp->counters, hp->sms, st, hp->ev[3]);
+      if (e != cudaSuccess) return e;
+    } else {
+      cudaEventRecord(hp->ev[3], st);
+    }
   }
   cudaEventRecord(hp->ev[4], st);
   if (hp->has_j2) {

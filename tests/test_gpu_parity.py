@@ -140,12 +140,15 @@ def test_eval_yz_paths(mode):
 PATH_SHAPES = [(3000, 40, 10, 4, 5), (2500, 12, 50, 0, 0), (1500, 25, 24, 2, 2), (2000, 10, 30, 0, 0)]
 
 
-@pytest.mark.parametrize("mode", ["default", "MNL_NO_PIPE", "MNL_NO_MATERIALISE"])
+@pytest.mark.parametrize("mode", ["default", "MNL_NO_PIPE", "MNL_NO_MATERIALISE", "MNL_FRAG_SLAB_CHUNKS=7"])
 def test_hessian_kernel_paths(mode):
-    """Every GEMM path (materialised operands + k_pipe_gemm; B-only materialised + k_gen_gemm<BPRE>;
-    fully generated k_gen_gemm) against the oracle's full Hessian."""
+    """Every GEMM path (materialised operands + k_pipe_gemm; the same materialised and consumed in
+    N-slabs of 7 chunks, as when the whole-N operands exceed the memory budget; B-only materialised
+    + k_gen_gemm<BPRE>; fully generated k_gen_gemm) against the oracle's full Hessian."""
+    key, _, val = mode.partition("=")
+    mode = key
     if mode != "default":
-        os.environ[mode] = "1"
+        os.environ[mode] = val or "1"
     M.release()  # the plan (and its kernel choice) is rebuilt under the environment
     try:
         for N, K, p, f, d in PATH_SHAPES:
