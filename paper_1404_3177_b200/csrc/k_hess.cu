@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(256) k_frag(const FragArgs F) {
       double2 o;
       o.x = rs[d0.o1 + i * d0.ld1] * fma(d0.s, rs[d0.o2 + i * d0.ld2], d0.c0);
       o.y = rs[d1.o1 + i * d1.ld1] * fma(d1.s, rs[d1.o2 + i * d1.ld2], d1.c0);
-      dst[ks * W] = o;
+      __stcs(dst + ks * W, o);  // streamed: the GEMM reads it back from HBM
     }
   }
 }

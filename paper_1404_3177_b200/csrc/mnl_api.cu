@@ -5,6 +5,7 @@
 // scalars cross to the host (loglik, ||g||^2, the bad-choice flag) for step control. Scratch is
 // per (device, stream) workspace: calls on distinct streams are independent.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cmath>
@@ -16,6 +17,15 @@
 #include "../../include/mnl.h"
 #include "internal.h"
 #include "nr_driver.h"
+
+namespace {
+// NVTX range for one phase of the Newton iteration (profiling per NR phase); no cost
+// unless a tool (nsys, ncu --nvtx) is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace mnl {
 
@@ -314,6 +324,7 @@ struct DeviceOps {
   cudaEvent_t ev[3];
 
   int eval_theta(double* l, double* g2) {
+    NvtxRange nvtx_range("mnl: pass 1 (l, g at theta)");
     double scal[3];
     const int rc = run_eval(W, D, ep, X, Y, Z, choice, W.theta, &pk, true, W.grad, nullptr, scal, st, ex);
     *l = scal[0];
@@ -322,6 +333,7 @@ struct DeviceOps {
   }
 
   int eval_trial(int j, double* l, double* g2) {
+    NvtxRange nvtx_range("mnl: step control trial (l, g at theta + delta / 2^j)");
     if (launch_axpy_pow2(D.n_p, W.theta, W.delta, j, W.trial, st) != cudaSuccess) return MNL_ERR_CUDA;
     double scal[3];
     const int rc = run_eval(W, D, ep, X, Y, Z, choice, W.trial, &pk, true, W.grad, nullptr, scal, st, ex);
@@ -341,6 +353,7 @@ struct DeviceOps {
 
   // A = -H (summed across ranks), A = L L^T, delta = A^{-1} g
   int direction_newton(bool* not_spd) {
+    NvtxRange nvtx_range("mnl: Newton direction (Hessian + Cholesky solve)");
     const int n = D.n_p;
     cudaEventRecord(ev[0], st);
     if (ex) {  // each rank's packed upper triangle of -H, summed, then mirrored into A
@@ -370,6 +383,7 @@ struct DeviceOps {
 
   // truncated Newton: CG on (-H) delta = g with H v products, never forming H
   int direction_cg(bool* not_spd) {
+    NvtxRange nvtx_range("mnl: truncated-Newton direction (CG on H v)");
     const int n = D.n_p;
     cudaEventRecord(ev[0], st);
     double* r = W.cg;
