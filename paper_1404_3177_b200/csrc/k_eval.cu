@@ -529,27 +529,34 @@ struct YzsState {
   int s_issue, slot_i;     // next position to stage and its slot (lane 0 only)
   int lg_cnt;              // deferred logs: lane lg_cnt receives the next individual's (uy - m, s)
   double lg_a, lg_s;
+  // lane 0's issue cursor: the next row to stage, its Y and Z rows, and the strides to the next one
+  int64_t gi;
+  const char *py, *pz;
+  unsigned by, bz;  // bytes of one Y / Z row (K f 8, K d 8)
 };
-// lane 0: stage the next position of this warp's sequence; false if it does not exist
-__device__ __forceinline__ bool yzs_issue(const EvalArgs& A, YzsState& st, int w) {
-  const int s = st.s_issue;
-  const int64_t gi = (blockIdx.x + (int64_t)(s / YZS_R) * gridDim.x) * YZS_TI + w * YZS_R + (s % YZS_R);
-  if (gi >= A.N) return false;
-  const unsigned by = (unsigned)A.K * A.f * 8u, bz = (unsigned)A.K * A.d * 8u;
+// lane 0: stage the next position of this warp's sequence (rows w R .. w R + R - 1 of every tile
+// this CTA visits); false if it does not exist. The cursor advances by one row inside a tile and
+// by gridDim.x * TI - (R - 1) rows to the next tile (no 64-bit products per row).
+__device__ __forceinline__ bool yzs_issue(const EvalArgs& A, YzsState& st) {
+  if (st.gi >= A.N) return false;
   const unsigned bar = st.bar_s + 8u * st.slot_i;
   const unsigned dst = st.ring_s + 8u * (unsigned)(st.slot_i * A.SLOT);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's previous generic accesses
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(by + bz) : "memory");
-  if (by)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(st.by + st.bz) : "memory");
+  if (st.by)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(A.Y + gi * A.K * A.f), "r"(by), "r"(bar)
+                 "l"(st.py), "r"(st.by), "r"(bar)
                  : "memory");
-  if (bz)
+  if (st.bz)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     dst + by),
-                 "l"(A.Z + gi * A.K * A.d), "r"(bz), "r"(bar)
+                     dst + st.by),
+                 "l"(st.pz), "r"(st.bz), "r"(bar)
                  : "memory");
-  st.s_issue = s + 1;
+  const int s = st.s_issue++;
+  const int64_t step = (s % YZS_R == YZS_R - 1) ? (int64_t)gridDim.x * YZS_TI - (YZS_R - 1) : 1;
+  st.gi += step;
+  st.py += step * st.by;
+  st.pz += step * st.bz;
   st.slot_i = (st.slot_i + 1 == A.NS) ? 0 : st.slot_i + 1;
   return true;
 }
@@ -569,9 +576,19 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
   bool kok[KPL];  // lane's alternatives exist (always for kk < KPL - 1: K > 32 (KPL - 1))
 #pragma unroll
   for (int kk = 0; kk < KPL; ++kk) kok[kk] = (kk < KPL - 1) || (lane + 32 * kk < K);
+  // the row offsets this lane reads: alternative lane + 32 kk, clamped to K - 1 where it does not
+  // exist (finite data; those lanes' utilities are -inf and their residuals 0, so the values drop
+  // out) -- the shared loads need no predicate
+  int ky[KPL], kz[KPL];
+#pragma unroll
+  for (int kk = 0; kk < KPL; ++kk) {
+    const int k = kok[kk] ? lane + 32 * kk : K - 1;
+    ky[kk] = k * f;
+    kz[kk] = k * d;
+  }
   __syncwarp();
   if (lane == 0)  // stage ahead into the slots released by the previous rows
-    while (st.s_issue <= st.s_cur + A.NS - 1 && yzs_issue(A, st, w)) {
+    while (st.s_issue <= st.s_cur + A.NS - 1 && yzs_issue(A, st)) {
     }
   int y[NI];
   int64_t gi[NI];
@@ -615,8 +632,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
         for (int j = 0; j < NI; ++j)
 #pragma unroll
           for (int kk = 0; kk < KPL; ++kk)
-            v[h][j][kk] = kok[kk] ? *reinterpret_cast<const double2*>(ys[j] + (lane + 32 * kk) * f + e + 2 * h)
-                                  : make_double2(0.0, 0.0);
+            v[h][j][kk] = *reinterpret_cast<const double2*>(ys[j] + ky[kk] + e + 2 * h);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double g0 = gamma[e + 2 * h], g1 = gamma[e + 2 * h + 1];
@@ -634,8 +650,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
       for (int j = 0; j < NI; ++j)
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
-          const double2 v = kok[kk] ? *reinterpret_cast<const double2*>(ys[j] + (lane + 32 * kk) * f + e)
-                                    : make_double2(0.0, 0.0);
+          const double2 v = *reinterpret_cast<const double2*>(ys[j] + ky[kk] + e);
           ua[j][kk] = fma(v.x, g0, ua[j][kk]);
           ub[j][kk] = fma(v.y, g1, ub[j][kk]);
         }
@@ -649,9 +664,9 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
       for (int t = 0; t < 4; ++t)
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
-          ac[t][kk] = kok[kk] ? alpha[(lane + 32 * kk) * d + c0 + t] : 0.0;
+          ac[t][kk] = alpha[kz[kk] + c0 + t];
 #pragma unroll
-          for (int j = 0; j < NI; ++j) z[t][j][kk] = kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
+          for (int j = 0; j < NI; ++j) z[t][j][kk] = zs[j][kz[kk] + c0 + t];
         }
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -670,8 +685,8 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
           for (int j = 0; j < NI; ++j)
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
-              const double z = kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
-              const double ac = kok[kk] ? alpha[(lane + 32 * kk) * d + c0 + t] : 0.0;
+              const double z = zs[j][kz[kk] + c0 + t];
+              const double ac = alpha[kz[kk] + c0 + t];
               if (t & 1) ub[j][kk] = fma(z, ac, ub[j][kk]);
               else ua[j][kk] = fma(z, ac, ua[j][kk]);
             }
@@ -783,9 +798,8 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
             for (int j = 0; j < NI; ++j)
 #pragma unroll
               for (int kk = 0; kk < KPL; ++kk)
-                v[h][j][kk] = (kok[kk] && h < nh)
-                                  ? *reinterpret_cast<const double2*>(ys[j] + (lane + 32 * kk) * f + e + 2 * h)
-                                  : make_double2(0.0, 0.0);
+                v[h][j][kk] = h < nh ? *reinterpret_cast<const double2*>(ys[j] + ky[kk] + e + 2 * h)
+                                      : make_double2(0.0, 0.0);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             double g0 = 0.0, g1 = 0.0;
@@ -824,7 +838,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
 #pragma unroll
         for (int j = 0; j < NI; ++j)
 #pragma unroll
-          for (int kk = 0; kk < KPL; ++kk) z[t][j][kk] = kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0;
+          for (int kk = 0; kk < KPL; ++kk) z[t][j][kk] = zs[j][kz[kk] + c0 + t];
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -842,7 +856,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
           for (int kk = 0; kk < KPL; ++kk) {
             double a = alp[kk][c0 + t];
 #pragma unroll
-            for (int j = 0; j < NI; ++j) a = fma(kok[kk] ? zs[j][(lane + 32 * kk) * d + c0 + t] : 0.0, r[j][kk], a);
+            for (int j = 0; j < NI; ++j) a = fma(zs[j][kz[kk] + c0 + t], r[j][kk], a);
             alp[kk][c0 + t] = a;
           }
         }
@@ -922,6 +936,11 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     yst.slot = yst.par = yst.s_cur = yst.s_issue = yst.slot_i = yst.lg_cnt = 0;
     yst.lg_a = 0.0;
     yst.lg_s = 1.0;
+    yst.by = (unsigned)A.K * A.f * 8u;
+    yst.bz = (unsigned)A.K * A.d * 8u;
+    yst.gi = (int64_t)blockIdx.x * YZS_TI + w * YZS_R;
+    yst.py = reinterpret_cast<const char*>(A.Y) + yst.gi * yst.by;
+    yst.pz = reinterpret_cast<const char*>(A.Z) + yst.gi * yst.bz;
 #pragma unroll
     for (int kk = 0; kk < KPL; ++kk)
 #pragma unroll
@@ -934,7 +953,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     }
     __syncwarp();
     if (lane == 0)  // only lane 0 tracks the issue pointer
-      while (yst.s_issue < A.NS && yzs_issue(A, yst, w)) {
+      while (yst.s_issue < A.NS && yzs_issue(A, yst)) {
       }
   }
 
