@@ -36,7 +36,9 @@ namespace {
 constexpr int NW = 8;    // warps per CTA
 // individuals per tile: 8 warps x 8 rows, halved for K > 128 or with alternative-varying data
 // (whose per-warp row staging needs the shared memory)
-__host__ __device__ constexpr int tile_rows(int kpl, bool yz) { return (kpl >= 8 && yz) ? 16 : ((kpl >= 8 || yz) ? 32 : 64); }
+// (K > 128, KPL = 8: 16 rows, utilities stashed in shared memory like the Y/Z paths -- holding the
+// 32 alternative blocks of a row in registers spilled)
+__host__ __device__ constexpr int tile_rows(int kpl, bool yz) { return kpl >= 8 ? 16 : (yz ? 32 : 64); }
 
 struct EvalArgs {
   int64_t N;
@@ -904,9 +906,10 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
   double* Rs = Xs + 2 * TI * XS;                // [TI][KPS]  residuals
   // [TI][KPS] utilities from phase B (YZS: in place in Rs, each lane overwrites its own u by r)
   double* Ps = YZS ? Rs : Rs + TI * KPS;
+  constexpr bool SPLITB = YZS || KPL >= 8;  // phase B split over row blocks x alternative groups, u stashed
   // [NWK][KPL][d][32] alpha-gradient, lane-private, then [NWK][f][32] gamma-gradient (e >= 8);
   // absent in stream mode (A.Rg: k_yz_grad forms those gradients) and in the YZS path (registers)
-  double* Wa_s = Rs + ((d + f) && !YZS ? 2 * TI * KPS : TI * KPS);
+  double* Wa_s = Rs + (((d + f) || KPL >= 8) && !YZS ? 2 * TI * KPS : TI * KPS);
   double* Wa = Wa_s;
   double* Cf = Wa_s + (YZS || A.Rg ? 0 : NWK * KPL * d * 32 + NWK * f * 32);  // [K*d + f]  alpha, gamma
   int* chs = reinterpret_cast<int*>(Cf + K * d + f + 1);  // [2][TI] choices
@@ -1033,15 +1036,15 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     // ---------------- phase B: u = X~ B on DMMA, then softmax / loglik / residuals ----------------
     // YZS (16-row tiles): the warps split 2 row blocks x NG groups of alternative blocks (groups
     // beyond NBN idle)
-    constexpr int RB = YZS_TI / 8;  // YZS: 8-row blocks of the tile
+    constexpr int RB = YZS_TI / 8;  // SPLITB (16-row tiles): 8-row blocks of the tile
     constexpr int NG = NWK / RB;
-    constexpr int NBW = YZS ? (NBN >= NG ? NBN / NG : 1) : NBN;  // alternative blocks per warp
-    const int il = YZS ? 8 * (w % RB) + c8 : (8 * w + c8) % TI;  // this lane's individual (C-fragment row)
-    const int nb0 = YZS ? (w / RB) * NBW : 0;
-    const bool in_b = YZS ? nb0 < NBN : 8 * w < TI;  // warps without a block skip phase B
-    double u[NBN][2];
+    constexpr int NBW = SPLITB ? (NBN >= NG ? NBN / NG : 1) : NBN;  // alternative blocks per warp
+    const int il = SPLITB ? 8 * (w % RB) + c8 : (8 * w + c8) % TI;  // this lane's individual (C-fragment row)
+    const int nb0 = SPLITB ? (w / RB) * NBW : 0;
+    const bool in_b = SPLITB ? nb0 < NBN : 8 * w < TI;  // warps without a block skip phase B
+    double u[NBW][2];
 #pragma unroll
-    for (int nb = 0; nb < NBN; ++nb) u[nb][0] = u[nb][1] = 0.0;
+    for (int nb = 0; nb < NBW; ++nb) u[nb][0] = u[nb][1] = 0.0;
     for (int a0 = 0; a0 < (in_b ? QP : 0); a0 += 4) {
       const double av = X_t[il * XS + a0 + r4];
 #pragma unroll
@@ -1054,8 +1057,9 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     }
     const bool valid = in_b && il < nt;
     const int64_t i = i0 + il;
-    if (YZS || (d + f)) {
-      // ---- alternative-varying data present: stash u, then phase E (lanes over alternatives) ----
+    if (SPLITB || (d + f)) {
+      // ---- alternative-varying data present (or K > 128): stash u, then phase E (lanes over
+      // alternatives) ----
       if (in_b) {
 #pragma unroll
         for (int nb = 0; nb < NBW; ++nb)
@@ -1075,7 +1079,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
       }
       if constexpr (!YZS)
         if (!done) phase_e<KPL, HV>(A, Ps, Rs, ch_t, Red + w * (8 * 33), alpha, gamma, Wa, gam, l_s, l_c, i0, nt, KPS, w, lane);
-    } else {
+    } else if constexpr (!SPLITB) {
     if constexpr (HV) {
       // Hessian-vector product: u holds s_ik = (J_i v)_k; with P_i from the last evaluation
       // (Pr), r_ik = -P_ik (s_ik - sum_l P_il s_il), so that the gradient contractions below
@@ -1544,7 +1548,7 @@ static size_t eval_smem(const Dims& D, int kpl, bool yzs, int ns, bool stream = 
   const int slot = D.K * (D.f + D.d);
   const int nw = yzs ? NWY : NW;
   size_t n = (size_t)eval_qp(D) * KPS + 2 * (size_t)TI * eval_xs(D) + (size_t)TI * KPS +
-             ((D.d + D.f) && !yzs ? (size_t)TI * KPS : 0) +
+             (((D.d + D.f) || kpl >= 8) && !yzs ? (size_t)TI * KPS : 0) +
              (yzs || stream ? 0 : (size_t)nw * kpl * D.d * 32 + (size_t)nw * D.f * 32) +
              (size_t)D.K * D.d + D.f + 1 + TI +  // + 2*TI ints
              ((D.d + D.f) && !yzs ? (size_t)nw * 8 * 33 : 0);
@@ -1650,7 +1654,9 @@ static cudaError_t launch_eval_core(const Dims& D, const EvalPlan& plan, const d
     MNL_EVAL_CASE(1)
     MNL_EVAL_CASE(2)
     MNL_EVAL_CASE(4)
-    MNL_EVAL_CASE(8)
+    case 8:  // eval_plan never picks cm = 8 for K > 128 (its register rule), so it is not instantiated
+      if (hv) return plan.cm == 2 ? launch_k<8, 2, true, false>(plan, a, st) : launch_k<8, 4, true, false>(plan, a, st);
+      return plan.cm == 2 ? launch_k<8, 2, false, false>(plan, a, st) : launch_k<8, 4, false, false>(plan, a, st);
   }
 #undef MNL_EVAL_CM
 #undef MNL_EVAL_CASE
