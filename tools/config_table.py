@@ -3,7 +3,7 @@
 Hessian time and TFLOP/s, Newton iteration and full-fit time, next to the CPU oracle on this host.
 
 GPU times: CUDA events (library-internal for the Hessian phases), median of `reps` after warm-up.
-Oracle: the same functions the tests use (oracle/), full-size where it finishes in about a minute,
+Oracle: the plain C oracle the tests use (oracle/oracle.c), full-size where it finishes in about a minute,
 otherwise a leading sample of the individuals with the time scaled by N / sample (all costs are
 linear in N); the sample is printed with each number.
 """
@@ -83,6 +83,7 @@ def gpu_row(cfg, reps=5):
 
 def oracle_row(cfg, budget_s=60.0):
     import oracle as O
+    from oracle import coracle as OC  # the plain C oracle (liboracle.so), every host core
     prob = datagen.make(cfg)
     s = prob.spec
     n = s.N
@@ -92,16 +93,16 @@ def oracle_row(cfg, budget_s=60.0):
             n = cand
             D = O.Data(prob.X[:n], prob.Y[:n], prob.Z[:n], prob.choice[:n], s.K)
             t0 = time.perf_counter()
-            O.mnl_eval(D, prob.theta_true)
+            OC.mnl_eval(D, prob.theta_true)
             te = time.perf_counter() - t0
             if te < budget_s / 4 or cand == 1000:
                 break
     scale = s.N / n
     t0 = time.perf_counter()
-    fit = O.newton_fit(D, tol=1e-6, max_iter=1)
+    OC.newton_fit(D, coef0=None, tol=1e-300, max_iter=1)
     t_iter = time.perf_counter() - t0
-    return dict(cfg=cfg, oracle_sample=n, oracle_eval_s=te * scale, oracle_s_per_iter=t_iter * scale,
-                oracle_threads=os.cpu_count())
+    return dict(cfg=cfg, oracle="C (oracle/oracle.c)", oracle_sample=n, oracle_eval_s=te * scale,
+                oracle_s_per_iter=t_iter * scale, oracle_threads=OC.set_threads(0))
 
 
 if __name__ == "__main__":
