@@ -312,7 +312,7 @@ def run_ours(args):
         achieved = fl["j1_main"] / (gemm_avg / 1e3) / 1e12
         traffic = None
         try:
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic_r1.json"))).get(args.config)
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic_r2.json"))).get(args.config)
         except Exception:
             pass
         # e2e: the same step through the host-buffer C ABI (H2D of inputs + D2H of the result inside)
