@@ -516,14 +516,11 @@ __global__ void __launch_bounds__(256, 1) k_chol_dag(int n, int nt, const double
     __syncthreads();
     const bool bad = potrf_core(jb, dsm);  // ends with a CTA barrier
     if (tid == 0 && bad) atomicCAS(info, 0, j0 + 1);
-    double* out = Lt + tile_off(j, j);
-    for (int e = tid; e < NB * NB; e += 256) {
-      const int r = e >> 6, c = e & 63;
-      const bool in = r < jb && c <= r;
-      out[r * LDS + c] = in ? S[r][c] : 0.0;
-      const double xv = in ? X[r][c] : 0.0;
-      LinvP[(int64_t)j * TS + r * LDS + c] = xv;
-      Linv[(int64_t)j * NB * NB + e] = xv;
+    // what the next column's tasks wait for first: Linv_j (padded, for their trsm) and y_j
+    for (int e = tid; e < NB * NB / 2; e += 256) {
+      const int r = e >> 5, c = 2 * (e & 31);
+      const double x0 = (r < jb && c <= r) ? X[r][c] : 0.0, x1 = (r < jb && c + 1 <= r) ? X[r][c + 1] : 0.0;
+      *reinterpret_cast<double2*>(LinvP + (int64_t)j * TS + r * LDS + c) = make_double2(x0, x1);
     }
     if (want_y) {  // y_j = Linv_j (b_j - sum_k L_jk y_k)
       double sacc = 0.0;
@@ -546,6 +543,16 @@ __global__ void __launch_bounds__(256, 1) k_chol_dag(int n, int nt, const double
       }
     }
     publish(tri(j, j));
+    // then what only the kernels after this one read: L_jj (tile-major) and the unpadded Linv_j
+    double* out = Lt + tile_off(j, j);
+    for (int e = tid; e < NB * NB / 2; e += 256) {
+      const int r = e >> 5, c = 2 * (e & 31);
+      const bool in0 = r < jb && c <= r, in1 = r < jb && c + 1 <= r;
+      *reinterpret_cast<double2*>(out + r * LDS + c) = make_double2(in0 ? S[r][c] : 0.0, in1 ? S[r][c + 1] : 0.0);
+      *reinterpret_cast<double2*>(Linv + (int64_t)j * NB * NB + r * NB + c) =
+          make_double2(in0 ? X[r][c] : 0.0, in1 ? X[r][c + 1] : 0.0);
+    }
+    __syncthreads();  // S / X (the stage buffers) are reused by the next task
   }
 }
 
