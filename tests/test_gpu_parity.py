@@ -538,7 +538,10 @@ def test_recovery_of_true_coefficients(cfg):
     assert 0.9 <= rms <= 1.1, rms
 
 
-def _random_shapes(count=40, seed=2024):
+def _random_shapes(count=None, seed=None):
+    # MNL_STRESS_SHAPES / MNL_STRESS_SEED widen the sweep for stress runs (the committed suite: 40, 2024)
+    count = int(os.environ.get("MNL_STRESS_SHAPES", 40)) if count is None else count
+    seed = int(os.environ.get("MNL_STRESS_SEED", 2024)) if seed is None else seed
     rng = np.random.default_rng(seed)
     out = []
     for _ in range(count):
@@ -580,7 +583,9 @@ def test_eval_parity_random_shapes(shape):
     assert np.linalg.norm(hv - H_o @ v) <= 1e-10 * np.linalg.norm(H_o @ v)
 
 
-def _random_fit_shapes(count=10, seed=77):
+def _random_fit_shapes(count=None, seed=None):
+    count = int(os.environ.get("MNL_STRESS_FITS", 10)) if count is None else count
+    seed = int(os.environ.get("MNL_STRESS_SEED", 77)) if seed is None else seed
     rng = np.random.default_rng(seed)
     out = []
     while len(out) < count:
