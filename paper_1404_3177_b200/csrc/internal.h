@@ -127,14 +127,17 @@ cudaError_t launch_sym_pack(int n, const double* H, double* out, cudaStream_t st
 cudaError_t launch_sym_unpack(int n, const double* in, double* H, cudaStream_t st);
 
 // ---- k_chol.cu -------------------------------------------------------------------------
-// Factorisation state (inverse diagonal blocks, grid-barrier words, side stream): one per workspace.
+// Factorisation state (tile-major factor, inverse diagonal blocks, tile / block flags, the forward
+// solution): one per workspace.
 struct CholCtx;
 CholCtx* chol_ctx_create();
 void chol_ctx_destroy(CholCtx*);
-// In-place lower Cholesky of the SPD n x n matrix A (lda), info: device int, set != 0 on failure.
+// Lower Cholesky of the SPD n x n matrix A (lda) written into A's lower triangle (the tile-DAG
+// factorisation, then a tile-major -> row-major copy); info: device int, set != 0 on failure.
 cudaError_t launch_cholesky(CholCtx* cc, int n, double* A, int lda, int* info, cudaStream_t st);
-// Factor A in place and solve (L L^T) x = b in the same pass (forward solve fused into the
-// panels, backward solve as one wavefront kernel). x may alias b.
+// Solve A x = b: the tile-DAG factorisation of A (A itself is only read; the factor stays in the
+// context's tile-major copy) with the forward solve fused into its diagonal tiles, then the
+// backward solve (one kernel; nothing more for n <= 64). x may alias b.
 cudaError_t launch_cholesky_solve_fused(CholCtx* cc, int n, double* A, int lda, int* info, const double* b,
                                         double* x, cudaStream_t st);
 // se_j = sqrt([(L L^T)^{-1}]_jj) for the factor L in the lower triangle of L (lda); the strict upper

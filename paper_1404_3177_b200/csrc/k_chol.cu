@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(256) k_trtri_blocks(int n, const double* A, in
 
 
 // 64 x 64 tile A[row0 + r][col0 + c] -> T[r][c] (zero for r >= nr or c >= nc), all 16 loads of a
-// thread in flight at once (clamped addresses, masked values; L2 loads: other CTAs of the
-// persistent factorisation wrote the tile, and trsm rewrites it)
+// thread in flight at once (clamped addresses, masked values; L2 loads: k_inv_diag stores blocks of
+// L^{-1} into the upper triangle, on cache lines it may already hold from reading L)
 __device__ __forceinline__ void load_tile(double (*T)[LDS], const double* A, int lda, int row0, int col0, int nr,
                                           int nc) {
   const int tid = threadIdx.x;
