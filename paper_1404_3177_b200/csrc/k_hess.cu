@@ -439,14 +439,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // 0..NWARP-1 only load fragments and issue DMMA. No CTA-wide barrier inside the loop: a stage is
 // refilled as soon as the NWARP consumer warps have released it. Item metadata travels with the
 // stage (written before the producer's release-arrive, read after the consumers' acquire-wait).
-template <int BN, int KC, int S>
+template <int BN, int KC, int S, int BMT = BM>
 __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P, const double* __restrict__ afrag) {
-  // 128 -> 2x4 warps of 64x32; 112 -> 8x1 of 16x112; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32; 48 -> 8x1 of 16x48
+  // BMT = 128: 128 -> 2x4 warps of 64x32; 112 -> 8x1 of 16x112; 96 -> 4x2 of 32x48; 64 -> 4x2 of 32x32;
+  // 48 -> 8x1 of 16x48. BMT = 64 (few weight pairs): 128 -> 2x4 of 32x32; 96 -> 4x2 of 16x48;
+  // 64 -> 2x4 of 32x16.
   constexpr int NWARP = 8;
-  constexpr int WARPS_M = (BN == 128) ? 2 : ((BN == 48 || BN == 112) ? 8 : 4), WARPS_N = NWARP / WARPS_M;
-  constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  constexpr int WARPS_M = BMT == 64 ? (BN == 96 ? 4 : 2)
+                                    : ((BN == 128) ? 2 : ((BN == 48 || BN == 112) ? 8 : 4)),
+                WARPS_N = NWARP / WARPS_M;
+  constexpr int WTM = BMT / WARPS_M, WTN = BN / WARPS_N;
   constexpr int MT = WTM / 8, NTL = WTN / 8;
-  constexpr int KS = KC / 4, PBA = BM / 16, PBB = BN / 16;
+  constexpr int KS = KC / 4, PBA = BMT / 16, PBB = BN / 16;
   constexpr int GA_D = KS * PBA * 64, GB_D = KS * PBB * 64;
   extern __shared__ __align__(128) double sm[];  // [S][GA_D + GB_D]
   __shared__ __align__(8) uint64_t full[S], empty[S];
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P
       double* Cb = P.C + split * P.split_stride;
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        const int64_t row = (int64_t)tm * BM + wm * WTM + i * 8 + cl;
+        const int64_t row = (int64_t)tm * BMT + wm * WTM + i * 8 + cl;
 #pragma unroll
         for (int j = 0; j < NTL; ++j) {
           const int col = tn * BN + wn * WTN + j * 8 + 2 * r4;
@@ -795,6 +799,7 @@ struct GemmJob {
   double* bfrag = nullptr;  // [tilesN][nchunks][GB_D]
   int dnseg = 0, dseg_id[3] = {0, 0, 0};  // stage layout the descriptors were built against
   bool agen = true;  // A operand uses the general generator form (J1)
+  int BM = mnl::BM;  // M-tile height: 128, or 64 for a pipelined J1 with few weight pairs
   int MA, MB, tilesM, tilesN, splits;
   // N-slabs (k_pipe_gemm jobs whose whole-N operands do not fit): the fragment buffers hold
   // slab_chunks chunks; the operands are materialised and consumed one slab at a time, each slab
@@ -879,14 +884,14 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   J.nwarp = 8;
   J.MA = (int)A.size();
   J.MB = (int)B.size();
-  J.tilesM = (J.MA + BM - 1) / BM;
+  J.tilesM = (J.MA + J.BM - 1) / J.BM;
   J.tilesN = (J.MB + BN - 1) / BN;
   J.nchunks = pk.Npad / KC;
   if (J.slab_chunks <= 0 || J.slab_chunks >= J.nchunks) J.slab_chunks = J.nchunks;
   J.nslab = (int)((J.nchunks + J.slab_chunks - 1) / J.slab_chunks);
   J.splits = choose_splits(J.tilesM * J.tilesN, J.slab_chunks, sms, 4);
   J.ldc = J.tilesN * BN;
-  J.split_stride = (int64_t)J.tilesM * BM * J.ldc;
+  J.split_stride = (int64_t)J.tilesM * J.BM * J.ldc;
   J.nseg = nseg;
   int off = 0;
   for (int s = 0; s < nseg; ++s) {
@@ -898,7 +903,7 @@ static bool setup_job(GemmJob& J, const std::vector<ColDesc>& A, const std::vect
   // descriptors padded to whole tiles; padding columns generate exact zeros
   std::vector<ColDesc> hA(A), hB(B);
   ColDesc zero{0, 0, 0, 0, 0.0, 0.0};
-  hA.resize((size_t)J.tilesM * BM, zero);
+  hA.resize((size_t)J.tilesM * J.BM, zero);
   hB.resize((size_t)J.tilesN * BN, zero);
   if (cudaMalloc(&J.dA, hA.size() * sizeof(ColDesc)) != cudaSuccess) return false;
   if (cudaMalloc(&J.dB, hB.size() * sizeof(ColDesc)) != cudaSuccess) return false;
@@ -982,6 +987,18 @@ static int64_t frag_slab_chunks(size_t per_chunk, int64_t nch) {
   return (nch + nslab - 1) / nslab;
 }
 
+// Tile widths of the 64-row k_pipe_gemm: the widest of {128, 96, 64} within 5 % of the smallest padding.
+static int choose_bn_pipe64(int MB) {
+  int64_t min_pad = -1;
+  for (int bn : {128, 96, 64}) {
+    const int64_t pad = (int64_t)(MB + bn - 1) / bn * bn;
+    if (min_pad < 0 || pad < min_pad) min_pad = pad;
+  }
+  for (int bn : {128, 96, 64})
+    if ((double)((MB + bn - 1) / bn * bn) <= 1.05 * (double)min_pad) return bn;
+  return 64;
+}
+
 // Tile widths k_pipe_gemm is instantiated for: the widest of {128, 112, 96, 64, 48} within 5% of the
 // smallest padded width.
 static int choose_bn_pipe(int MB) {
@@ -1025,19 +1042,23 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       // (8 N 128 tilesM bytes) is small next to the GEMM (~23/vech of it at the measured rates):
       // vech >= 256. Otherwise materialise only the design-only B (once per design) if it fits.
       GemmJob& J = hp->j1;
-      const int tilesM = (int)((A.size() + BM - 1) / BM);
       const int64_t nch = pk.Npad / KC;
       const bool pipe_ok = KC == 32 && nv >= 256 && frag_fits && !getenv("MNL_NO_PIPE");
-      int bn1 = split ? 128 : (pipe_ok ? choose_bn_pipe(nv) : choose_bn(nv));
-      const int bnt_p = split ? choose_bn_pipe(rem) : 0;
+      // M-tile height of the pipelined GEMM: 64 when it pads the weight pairs clearly less than 128
+      // (c3: 190 pairs -> 192 rows instead of 256); the tile widths then come from {128, 96, 64}
+      const int np = (int)A.size();
+      const int bm = (pipe_ok && (np + 63) / 64 * 64 < 0.95 * ((np + 127) / 128 * 128)) ? 64 : BM;
+      const int tilesM = (np + bm - 1) / bm;
+      int bn1 = split ? 128 : (pipe_ok ? (bm == 64 ? choose_bn_pipe64(nv) : choose_bn_pipe(nv)) : choose_bn(nv));
+      const int bnt_p = split ? (bm == 64 ? choose_bn_pipe64(rem) : choose_bn_pipe(rem)) : 0;
       double *af = nullptr, *bf = nullptr, *tbf = nullptr;
       int64_t slab = 0;
       if (pipe_ok) {  // both operands materialised, whole-N or in N-slabs of the same size
         const size_t per_chunk =
-            ((size_t)tilesM * BM + (size_t)((hp->n1a + bn1 - 1) / bn1) * bn1 + bnt_p) * KC * sizeof(double);
+            ((size_t)tilesM * bm + (size_t)((hp->n1a + bn1 - 1) / bn1) * bn1 + bnt_p) * KC * sizeof(double);
         slab = frag_slab_chunks(per_chunk, nch);
         if (slab > 0) {
-          af = alloc_frag_chunks(tilesM, BM, slab, KC, &bytes);
+          af = alloc_frag_chunks(tilesM, bm, slab, KC, &bytes);
           bf = af ? alloc_frag_chunks((hp->n1a + bn1 - 1) / bn1, bn1, slab, KC, &bytes) : nullptr;
           tbf = (bf && split) ? alloc_frag_chunks(1, bnt_p, slab, KC, &bytes) : nullptr;
           if (!bf || (split && !tbf)) {
@@ -1056,6 +1077,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
       J.afrag = af;
       J.bfrag = bf;
       J.own_afrag = true;
+      J.BM = af ? bm : BM;  // in-kernel generation (k_gen_gemm) is built for 128-row tiles
       J.mat_a = af != nullptr;
       J.mat_b = bf != nullptr;
       J.slab_chunks = slab;
@@ -1076,6 +1098,7 @@ HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
         T.mat_a = T.mat_b = tbf != nullptr;
         T.slab_chunks = J.slab_chunks;
         T.b_design = J.b_design;
+        T.BM = T.mat_a ? J.BM : BM;  // reads j1's weight fragments
         T.dnseg = 2;
         T.dseg_id[0] = 0;
         T.dseg_id[1] = 1;
@@ -1271,10 +1294,10 @@ static cudaError_t run_gemm(const GemmJob& J, const Packed& pk, unsigned* counte
   return cudaGetLastError();
 }
 
-template <int BN>
+template <int BN, int BMT = BM>
 static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaStream_t st, int slab) {
-  constexpr int KC = 32, S = (200 * 1024) / ((KC / 4) * (BM / 16 + BN / 16) * 64 * 8);  // stages in ~200 KB
-  constexpr size_t smem = (size_t)S * (KC / 4) * (BM / 16 + BN / 16) * 64 * sizeof(double);
+  constexpr int KC = 32, S = (200 * 1024) / ((KC / 4) * (BMT / 16 + BN / 16) * 64 * 8);  // stages in ~200 KB
+  constexpr size_t smem = (size_t)S * (KC / 4) * (BMT / 16 + BN / 16) * 64 * sizeof(double);
   GemmParams P{};
   P.tilesM = J.tilesM;
   P.tilesN = J.tilesN;
@@ -1289,12 +1312,12 @@ static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaSt
   P.skip_off = J.skip_off;
   static uint64_t attr_mask = 0;
   cudaError_t e = set_once_per_device(attr_mask, [smem] {
-    return cudaFuncSetAttribute(k_pipe_gemm<BN, KC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_pipe_gemm<BN, KC, S, BMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (e != cudaSuccess) return e;
   const int items = J.tilesM * J.tilesN * J.splits;
   cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
-  k_pipe_gemm<BN, KC, S><<<std::min(items, sms), 8 * 32 + 32, smem, st>>>(P, J.afrag);
+  k_pipe_gemm<BN, KC, S, BMT><<<std::min(items, sms), 8 * 32 + 32, smem, st>>>(P, J.afrag);
   count_launch();
   return cudaGetLastError();
 }
@@ -1303,7 +1326,11 @@ static cudaError_t run_pipe(const GemmJob& J, unsigned* counter, int sms, cudaSt
 static cudaError_t run_gemm_only(const GemmJob& J, const Packed& pk, unsigned* counter, int sms, cudaStream_t st,
                                  int slab = 0) {
   cudaError_t e;
-  if (J.mat_a) {
+  if (J.mat_a && J.BM == 64) {
+    if (J.BN == 128) e = run_pipe<128, 64>(J, counter, sms, st, slab);
+    else if (J.BN == 96) e = run_pipe<96, 64>(J, counter, sms, st, slab);
+    else e = run_pipe<64, 64>(J, counter, sms, st, slab);
+  } else if (J.mat_a) {
     if (J.BN == 128) e = run_pipe<128>(J, counter, sms, st, slab);
     else if (J.BN == 96) e = run_pipe<96>(J, counter, sms, st, slab);
     else if (J.BN == 112) e = run_pipe<112>(J, counter, sms, st, slab);
@@ -1362,7 +1389,7 @@ static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStr
   F.desc = a_side ? J.dA : J.dB;
   F.out = a_side ? J.afrag : J.bfrag;
   F.tiles = a_side ? J.tilesM : J.tilesN;
-  F.BT = a_side ? BM : J.BN;
+  F.BT = a_side ? J.BM : J.BN;
   F.KC = J.KC;
   F.nchunks = J.slab_chunks;  // buffer stride; this launch covers slab `slab`
   F.c_base = (int64_t)slab * J.slab_chunks;
