@@ -140,6 +140,8 @@ typedef struct {
   double min_margin;        /* R7 audit: min over every line-search decision (accepted or rejected) of
                                |l_j - (l - tau)| / max(1,|l|); a decision closer than ~1e-13 to its
                                threshold could flip under a different summation order (+inf if none) */
+  double loglik_per_iter[64];     /* l at the iterate that starts Newton iteration t (t < min(iters, 64)) */
+  double grad_norm_per_iter[64];  /* ||g||_2 at that iterate (before its Hessian is formed) */
 } mnl_fit_stats;
 
 /* Why a fit stopped: the first of the paper's three conditions met. */

@@ -48,11 +48,14 @@ class FitStats(ctypes.Structure):
                 ("hess_ms", ctypes.c_double), ("chol_ms", ctypes.c_double), ("eval_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("gemm_ms", ctypes.c_double),
                 ("halvings_per_iter", ctypes.c_int32 * 64), ("delta_loglik", ctypes.c_double),
-                ("stop_reason", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("min_margin", ctypes.c_double)]
+                ("stop_reason", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("min_margin", ctypes.c_double),
+                ("loglik_per_iter", ctypes.c_double * 64), ("grad_norm_per_iter", ctypes.c_double * 64)]
 
     def as_dict(self) -> dict:
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "halvings_per_iter"}
-        d["halvings_per_iter"] = list(self.halvings_per_iter[: min(self.iters, 64)])
+        per_iter = ("halvings_per_iter", "loglik_per_iter", "grad_norm_per_iter")
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in per_iter}
+        for k in per_iter:
+            d[k] = list(getattr(self, k)[: min(self.iters, 64)])
         return d
 
 

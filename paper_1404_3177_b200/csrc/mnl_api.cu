@@ -502,6 +502,8 @@ int fit_impl(Workspace& W, int64_t N, int32_t K, int32_t p, int32_t f, int32_t d
     S.delta_loglik = R.delta_loglik;
     S.stop_reason = R.stop_reason;
     S.min_margin = R.min_margin;
+    memcpy(S.loglik_per_iter, R.loglik_per_iter, sizeof(S.loglik_per_iter));
+    memcpy(S.grad_norm_per_iter, R.grad_norm_per_iter, sizeof(S.grad_norm_per_iter));
     S.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     S.eval_ms = S.total_ms - S.hess_ms - S.chol_ms;
     *stats = S;

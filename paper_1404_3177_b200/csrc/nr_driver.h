@@ -31,6 +31,8 @@ struct NrReport {
   int32_t halvings_per_iter[64] = {};
   double loglik = 0.0, grad_norm = 0.0, delta_loglik = 0.0;
   double min_margin = INFINITY;  // R7 audit: min |l_j - (l - tau)| / max(1,|l|) over every decision
+  // l and ||g||_2 at the iterate that starts Newton iteration t (before its Hessian), t < 64
+  double loglik_per_iter[64] = {}, grad_norm_per_iter[64] = {};
 };
 
 // Ops must provide (all values global, i.e. after any exchange across ranks):
@@ -54,6 +56,10 @@ int nr_fit(Ops& ops, const NrOptions& o, NrReport* S) {
     if (std::sqrt(g2) < o.gtol) { S->stop_reason = kStopGtol; break; }
     if (ftol_met) { S->stop_reason = kStopFtol; break; }
     if (S->iters == o.max_iter) { status = kMaxIter; S->stop_reason = kStopMaxIter; break; }
+    if (S->iters < 64) {
+      S->loglik_per_iter[S->iters] = l;
+      S->grad_norm_per_iter[S->iters] = std::sqrt(g2);
+    }
     bool not_spd = false;
     rc = ops.direction(&not_spd);
     if (rc) break;

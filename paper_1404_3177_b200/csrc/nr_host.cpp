@@ -18,6 +18,7 @@ typedef struct {
   int32_t iters, halvings, evals, status, stop_reason;
   int32_t halvings_per_iter[64];
   double loglik, grad_norm, delta_loglik, min_margin;
+  double loglik_per_iter[64], grad_norm_per_iter[64];  // at the iterate starting each iteration
 } nr_host_report;
 
 int nr_fit_host(const nr_host_ops* ops, double gtol, double ftol, int32_t max_iter, nr_host_report* out) {
@@ -52,6 +53,10 @@ int nr_fit_host(const nr_host_ops* ops, double gtol, double ftol, int32_t max_it
   out->grad_norm = R.grad_norm;
   out->delta_loglik = R.delta_loglik;
   out->min_margin = R.min_margin;
+  for (int i = 0; i < 64; ++i) {
+    out->loglik_per_iter[i] = R.loglik_per_iter[i];
+    out->grad_norm_per_iter[i] = R.grad_norm_per_iter[i];
+  }
   return st;
 }
 

@@ -93,7 +93,8 @@ class HostReport(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("halvings", ctypes.c_int32), ("evals", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("stop_reason", ctypes.c_int32),
                 ("halvings_per_iter", ctypes.c_int32 * 64), ("loglik", ctypes.c_double),
-                ("grad_norm", ctypes.c_double), ("delta_loglik", ctypes.c_double), ("min_margin", ctypes.c_double)]
+                ("grad_norm", ctypes.c_double), ("delta_loglik", ctypes.c_double), ("min_margin", ctypes.c_double),
+                ("loglik_per_iter", ctypes.c_double * 64), ("grad_norm_per_iter", ctypes.c_double * 64)]
 
 
 _host = None
@@ -141,7 +142,9 @@ def run_host_driver(eval_theta, direction, eval_trial, accept, gtol=1e-6, ftol=0
     ops = HostOps(None, EVAL_FN(_e), DIR_FN(_d), TRIAL_FN(_t), ACCEPT_FN(_a))
     rep = HostReport()
     rc = _host_lib().nr_fit_host(ctypes.byref(ops), gtol, ftol, max_iter, ctypes.byref(rep))
-    out = {k: getattr(rep, k) for k, _ in HostReport._fields_ if k != "halvings_per_iter"}
-    out["halvings_per_iter"] = list(rep.halvings_per_iter[:min(rep.iters, 64)])
+    per_iter = ("halvings_per_iter", "loglik_per_iter", "grad_norm_per_iter")
+    out = {k: getattr(rep, k) for k, _ in HostReport._fields_ if k not in per_iter}
+    for k in per_iter:
+        out[k] = list(getattr(rep, k)[:min(rep.iters, 64)])
     out["rc"] = rc
     return out

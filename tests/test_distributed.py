@@ -108,7 +108,8 @@ def _worker(rank, world, port, shape, start_scale, out_path, nan_rank=None, bad_
     if rank == 0:
         np.savez(out_path, coef=ops.theta, iters=rep["iters"], status=rep["rc"],
                  halvings=np.array(rep["halvings_per_iter"]), same=all(torch.equal(c, coefs[0]) for c in coefs),
-                 min_margin=rep["min_margin"])
+                 min_margin=rep["min_margin"], lpi=np.array(rep["loglik_per_iter"]),
+                 gpi=np.array(rep["grad_norm_per_iter"]))
     dist.destroy_process_group()
 
 
@@ -136,6 +137,9 @@ def test_data_parallel_fit_equals_single_process_oracle(tmp_path, shape, start):
     assert list(r["halvings"]) == [h["halvings"] for h in ref.history]
     assert np.linalg.norm(r["coef"] - ref.coef) <= 1e-9 * np.linalg.norm(ref.coef)
     assert float(r["min_margin"]) > 1e-13       # R7 audit of the driver's decisions
+    # the per-iteration report (l, ||g|| at the iterate starting each iteration) vs the oracle's log
+    assert np.allclose(r["lpi"], [h["l"] for h in ref.history], rtol=1e-12, atol=0)
+    assert np.allclose(r["gpi"], [h["gnorm"] for h in ref.history], rtol=1e-8, atol=1e-12)
 
 
 def test_data_parallel_nonfinite_shard_rejects_on_every_rank(tmp_path):

@@ -266,6 +266,16 @@ def fit_parity(prob, fit_o, tol=1e-6, coef0=None):
     assert abs(r.loglik - fit_o["loglik"]) <= 1e-10 * abs(fit_o["loglik"])
     # R7 audit: no GPU accept/reject decision within 1e-13 |l| of its threshold
     assert r.stats["min_margin"] > 1e-13, r.stats["min_margin"]
+    # the per-iteration report against the oracle's log: l and ||g|| at the iterate starting each
+    # Newton iteration (the paper's est.stat quantities)
+    hist = fit_o.get("history")
+    if hist:
+        lg, gn = r.stats["loglik_per_iter"], r.stats["grad_norm_per_iter"]
+        g0 = hist[0]["gnorm"]
+        for t, h in enumerate(hist[:64]):
+            assert abs(lg[t] - h["l"]) <= 1e-10 * abs(h["l"]), (t, lg[t], h["l"])
+            tol = 1e-6 * h["gnorm"] if h["gnorm"] > 1e-3 * g0 else 1e-9 * g0
+            assert abs(gn[t] - h["gnorm"]) <= tol, (t, gn[t], h["gnorm"])
     return r
 
 
@@ -274,7 +284,8 @@ def test_fit_parity_small(cfg):
     prob = datagen.make(cfg)
     f = O.newton_fit(oracle_data(prob), tol=1e-6)
     assert f.status == O.MNL_OK
-    fit_parity(prob, dict(iters=f.iters, halvings=[h["halvings"] for h in f.history], coef=f.coef, loglik=f.loglik))
+    fit_parity(prob, dict(iters=f.iters, halvings=[h["halvings"] for h in f.history], coef=f.coef, loglik=f.loglik,
+                          history=f.history))
 
 
 def test_fit_parity_random_start_with_halvings():
@@ -293,8 +304,8 @@ def test_fit_parity_golden(cfg):
         pytest.skip(f"{path} not generated (tools/make_golden_fits.py)")
     g = json.load(open(path))
     prob = datagen.make(cfg)
-    fit_parity(prob, dict(iters=g["iters"], halvings=g["halvings"], coef=np.array(g["coef"]), loglik=g["loglik"]),
-               tol=g["tol"])
+    fit_parity(prob, dict(iters=g["iters"], halvings=g["halvings"], coef=np.array(g["coef"]), loglik=g["loglik"],
+                          history=g["history"]), tol=g["tol"])
 
 
 def test_fit_maxiter_and_zero_iter():
