@@ -60,14 +60,18 @@ __device__ __forceinline__ void smem_gemm(double* out, int lo, const double* Am,
 }
 
 // potrf_core: Cholesky of the jb x jb block in S (shared, LDR rows: the lower triangle, identity
-// beyond jb) fused with X = L^{-1}, by 16-column sub-panels (only those below jb): (1) warp 0
-// factors and inverts the 16 x 16 diagonal block (lane r owns row r of the block in registers; one
-// shared-memory broadcast per column; unscaled right-looking updates a_rk -= a_rc a_kc / a_cc, the
-// scaling by 1 / sqrt(a_cc) applied once at the end; then lane r solves for column r of L^{-1}),
-// (2) L21 = A21 X11^T and (3) A22 -= L21 L21^T on DMMA by all warps; finally (4) the off-diagonal
-// blocks of X on DMMA. S <- L (strict upper zeroed), X <- L^{-1}; returns (in thread 0) whether a
-// pivot was not positive (it is replaced by 1 to keep the values finite). Rows / columns >= jb of S
-// and X are left undefined when jb < 64 (callers mask them).
+// beyond jb, strict upper triangle zero) fused with X = L^{-1}, by 16-column blocks b, pipelined
+// across warp roles: warp 0 runs only the critical chain — factor and invert the 16 x 16 diagonal
+// block b (lane r owns row r of the block in registers; one shared-memory broadcast per column;
+// unscaled right-looking updates a_rk -= a_rc a_kc / a_cc, the scaling by 1 / sqrt(a_cc) applied
+// once at the end; then lane r solves for column r of L^{-1}) — while the seven other warps, on
+// DMMA, form L_{>b,b} = A_{>b,b} X_bb^T, update the next diagonal block first (which releases warp
+// 0 for block b + 1), then the rest of the trailing triangle and row block b of X
+// (X_{b,<b} = -X_bb L_{b,<b} X_{<b,<b}). Measured (clock64, one 64 x 64 block): 27.0k cycles, was
+// 35.6k with all warps stepping through the sub-panels together; warp 0's chain is the bound (its
+// 16 columns take 4.4k cycles alone, 6.6-7.1k beside the workers' shared-memory traffic). S <- L, X <- L^{-1}; returns (in thread 0) whether a pivot
+// was not positive (it is replaced by 1 to keep the values finite). Rows / columns >= jb of S and X
+// are left undefined when jb < 64 (callers mask them). All 256 threads call it.
 constexpr int SB = 16;
 
 // warp 0: the 16 x 16 diagonal block at (c0, c0): S <- L, X <- L^{-1}. Lanes 16..31 mirror 0..15.
@@ -83,15 +87,16 @@ __device__ __forceinline__ bool potrf16_warp(double (*S)[LDR], double (*X)[LDR],
     if (lane < SB) colb[lane] = a[c];  // column c (rows >= c are current)
     __syncwarp();
     double d = colb[c];
-    const bool b = !(d > 0.0) || !isfinite(d);
-    bad |= b;
-    if (b) d = 1.0;
+    const bool ok = d > 0.0 && d < INFINITY;
+    bad |= !ok;
+    d = ok ? d : 1.0;
     const double rs = rsqrt(d);
     rsv[c] = rs;
     const double f = a[c] * (rs * rs);  // a_rc / a_cc
+    // unpredicated: lane r also updates its strict upper part (k > r), which is masked below —
+    // per-lane predicates cost more issue slots than the extra FMAs
 #pragma unroll
-    for (int k = c + 1; k < SB; ++k)
-      if (r >= k) a[k] = fma(-f, colb[k], a[k]);
+    for (int k = c + 1; k < SB; ++k) a[k] = fma(-f, colb[k], a[k]);
     __syncwarp();
   }
 #pragma unroll
@@ -117,71 +122,100 @@ __device__ __forceinline__ bool potrf16_warp(double (*S)[LDR], double (*X)[LDR],
   return bad;
 }
 
+// Named barriers of potrf_core (id 0 is __syncthreads): kPanel = block b factored (warp 0 arrives,
+// the workers wait), kDiag = the next diagonal block updated (the workers arrive, warp 0 waits),
+// kWork = the seven worker warps only.
+constexpr int kPanel = 1, kDiag = 2, kWork = 3;
+#ifndef POTRF_TRACE
+#define POTRF_TRACE(i)
+#endif
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 __device__ __noinline__ bool potrf_core(int jb, double* dsm) {
   double(*S)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm);
   double(*X)[LDR] = reinterpret_cast<double(*)[LDR]>(dsm + NB * LDR);
-  __shared__ double T[NB][SB + 1];
+  __shared__ double T[NB][SB + 1];  // L_{r,b} for the row blocks r > b
+  __shared__ double M[SB][NB + 1];  // M_b = L_{b,<b} X_{<b,<b}
   __shared__ double colb[SB];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int lr = lane >> 2, lk = lane & 3;
   for (int e = tid; e < NB * NB; e += 256) X[e >> 6][e & 63] = 0.0;
   __syncthreads();
+  const int nbk = (jb + SB - 1) / SB;
   bool bad = false;
+  if (w == 0) {
+    // the critical chain: factor block b as soon as its last update (from panel b - 1) is in
 #pragma unroll 1
-  for (int c0 = 0; c0 < jb; c0 += SB) {
-    if (w == 0) bad |= potrf16_warp(S, X, c0, colb);  // (1)
-    __syncthreads();
-    const int r0 = c0 + SB, R = NB - r0;
-    if (R > 0) {
-      // (2) T = A21 X11^T (R x 16; warp w: 8 x 8 output tiles w, w + 8)
-      for (int tt = w; tt < (R / 8) * 2; tt += 8) {
-        const int tm = tt >> 1, tn = tt & 1;
-        double c0v = 0.0, c1v = 0.0;
+    for (int b = 0; b < nbk; ++b) {
+      POTRF_TRACE(2 * b);
+      if (b > 0) bar_sync(kDiag, 256);
+      POTRF_TRACE(2 * b + 1);
+      bad |= potrf16_warp(S, X, b * SB, colb);
+      __syncwarp();
+      bar_arrive(kPanel, 256);
+    }
+  } else {
+    // warp 4 shares warp 0's SM sub-partition: it only takes part in the barriers (-2 % measured)
+    const int wi = w == 4 ? 1000 : (w < 4 ? w - 1 : w - 2), nw = 6;
+#pragma unroll 1
+    for (int b = 0; b < nbk; ++b) {
+      bar_sync(kPanel, 256);  // L_bb, X_bb in; also: every worker is done with iteration b - 1
+      const int c0 = b * SB, r0 = c0 + SB, R = (nbk - 1 - b) * SB;
+      if (R > 0) {
+        // (2) T = A_{>b,b} X_bb^T
+        for (int tt = wi; tt < (R / 8) * 2; tt += nw) {
+          const int tm = tt >> 1, tn = tt & 1;
+          double c0v = 0.0, c1v = 0.0;
 #pragma unroll
-        for (int k0 = 0; k0 < SB; k0 += 4)
-          dmma(c0v, c1v, S[r0 + tm * 8 + lr][c0 + k0 + lk], X[c0 + tn * 8 + lr][c0 + k0 + lk]);
-        T[tm * 8 + lr][tn * 8 + 2 * lk] = c0v;
-        T[tm * 8 + lr][tn * 8 + 2 * lk + 1] = c1v;
-      }
-      __syncthreads();
-      for (int e = tid; e < R * SB; e += 256) S[r0 + e / SB][c0 + e % SB] = T[e / SB][e % SB];
-      // (3) A22 -= L21 L21^T: 8 x 8 tiles (mb >= nb) of the R x R trailing block, from T
-      const int MBk = R / 8;
-      for (int blk = w; blk < MBk * (MBk + 1) / 2; blk += 8) {
-        int mb = 0;
-        while ((mb + 1) * (mb + 2) / 2 <= blk) ++mb;
-        const int nb = blk - mb * (mb + 1) / 2;
-        double c0v = 0.0, c1v = 0.0;
+          for (int k0 = 0; k0 < SB; k0 += 4)
+            dmma(c0v, c1v, S[r0 + tm * 8 + lr][c0 + k0 + lk], X[c0 + tn * 8 + lr][c0 + k0 + lk]);
+          T[tm * 8 + lr][tn * 8 + 2 * lk] = c0v;
+          T[tm * 8 + lr][tn * 8 + 2 * lk + 1] = c1v;
+        }
+        bar_sync(kWork, 224);
+        for (int e = tid - 32; e < R * SB; e += 224) S[r0 + e / SB][c0 + e % SB] = T[e / SB][e % SB];
+        // (3a) the next diagonal block first (8 x 8 tiles (0,0), (1,0), (1,1)), then release warp 0
+        if (wi < 3) {
+          const int mb = wi > 0, nb_ = wi > 1;
+          double c0v = 0.0, c1v = 0.0;
 #pragma unroll
-        for (int k0 = 0; k0 < SB; k0 += 4) dmma(c0v, c1v, T[mb * 8 + lr][k0 + lk], T[nb * 8 + lr][k0 + lk]);
-        const int rr = r0 + mb * 8 + lr, cc = r0 + nb * 8 + 2 * lk;
-        if (cc <= rr) S[rr][cc] -= c0v;
-        if (cc + 1 <= rr) S[rr][cc + 1] -= c1v;
+          for (int k0 = 0; k0 < SB; k0 += 4) dmma(c0v, c1v, T[mb * 8 + lr][k0 + lk], T[nb_ * 8 + lr][k0 + lk]);
+          const int rr = r0 + mb * 8 + lr, cc = r0 + nb_ * 8 + 2 * lk;
+          if (cc <= rr) S[rr][cc] -= c0v;
+          if (cc + 1 <= rr) S[rr][cc + 1] -= c1v;
+        }
+        bar_sync(kWork, 224);
+        bar_arrive(kDiag, 256);
+        // (3b) the rest of the trailing lower triangle, while warp 0 factors block b + 1
+        const int MBk = R / 8;
+        for (int blk = 3 + wi; blk < MBk * (MBk + 1) / 2; blk += nw) {
+          int mb = 0;
+          while ((mb + 1) * (mb + 2) / 2 <= blk) ++mb;
+          const int nb_ = blk - mb * (mb + 1) / 2;
+          double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+          for (int k0 = 0; k0 < SB; k0 += 4) dmma(c0v, c1v, T[mb * 8 + lr][k0 + lk], T[nb_ * 8 + lr][k0 + lk]);
+          const int rr = r0 + mb * 8 + lr, cc = r0 + nb_ * 8 + 2 * lk;
+          if (cc <= rr) S[rr][cc] -= c0v;
+          if (cc + 1 <= rr) S[rr][cc + 1] -= c1v;
+        }
       }
-      __syncthreads();
+      // (4) row block b of X = L^{-1}: X_{b,<b} = -X_bb M_b, M_b = L_{b,<b} X_{<b,<b} (formed in the
+      // previous iteration); then M_{b+1} = L_{b+1,<=b} X_{<=b,<=b}, so that after the last
+      // diagonal block only one 16-deep product is left
+      if (b > 0) smem_gemm(&X[c0][0], LDR, &X[c0][c0], LDR, &M[0][0], NB + 1, SB, c0, SB, -1.0, wi, nw);
+      if (R > 0) {
+        bar_sync(kWork, 224);
+        smem_gemm(&M[0][0], NB + 1, &S[r0][0], LDR, &X[0][0], LDR, SB, r0, r0, 1.0, wi, nw);
+      }
     }
   }
-  // (4) off-diagonal blocks of X = L^{-1} on DMMA: X_ba = -X_bb (L_ba X_aa) for the 16-blocks of
-  // each 32-block, then for the two 32-blocks. The strict upper triangle of S is zeroed first.
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (c > r) S[r][c] = 0.0;
-  }
+  POTRF_TRACE(8);
   __syncthreads();
-  {
-    double(*T2)[33] = reinterpret_cast<double(*)[33]>(&T[0][0]);  // 32 x 33 view of T (64 x 17)
-    const int h = w >> 2, o = 32 * h;
-    smem_gemm(&T2[16 * h][0], 33, &S[o + 16][o], LDR, &X[o][o], LDR, 16, 16, 16, 1.0, w & 3, 4);
-    __syncthreads();
-    smem_gemm(&X[o + 16][o], LDR, &X[o + 16][o + 16], LDR, &T2[16 * h][0], 33, 16, 16, 16, -1.0, w & 3, 4);
-    __syncthreads();
-    if (jb > 32) {
-      smem_gemm(&T2[0][0], 33, &S[32][0], LDR, &X[0][0], LDR, 32, 32, 32, 1.0, w, 8);
-      __syncthreads();
-      smem_gemm(&X[32][0], LDR, &X[32][32], LDR, &T2[0][0], 33, 32, 32, 32, -1.0, w, 8);
-      __syncthreads();
-    }
-  }
+  POTRF_TRACE(9);
   return bad;
 }
 
