@@ -782,6 +782,149 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs A) {
   }
 }
 
+// ---- small problems (n_p <= 64): the whole Hessian in one launch --------------------------------
+// For a handful of parameters the three GEMMs above are latency: seven launches, split partials and
+// an assembly for a few hundred entries (c1: n_p = 18). Here every thread owns <= kSmallEpt entries
+// (r <= c) of -H and accumulates, individual by individual, the J-form of P:378-382 / App. B with the
+// Jacobian's sparsity written out: with m_r the value of column r in its own alternative's
+// utility (x~_ia for beta_k, z_ikc for alpha_k) and u_r = sum_k P_ik J_i[k][r] (P_ik m_r; ybar_ie
+// for gamma_e),
+//   -H_i[r][c] = [alt(r) = alt(c)] P_i,alt m_r m_c          (beta / alpha x beta / alpha)
+//              + P_i,alt(r) m_r y_i,alt(r),e                 (beta / alpha x gamma_e)
+//              + sum_k P_ik y_ike y_ike'                     (gamma_e x gamma_e')
+//              - u_r u_c.
+// CTA partials go to global scratch and the last CTA to finish sums them in CTA order (fixed order:
+// deterministic) into the caller's layout.
+constexpr int kSmallEpt = 9;     // entries per thread: 256 x 9 >= 64 x 65 / 2
+constexpr int kSmallTI = 16;     // individuals per staged tile
+constexpr int kSmallMaxKF = 128; // K f of a staged Y row (static shared memory < 48 KB)
+struct SmallArgs {
+  int64_t N;
+  int K, q, d, f, n_p, n_beta, off_gamma;
+  const double* Pr; int ldP;
+  const double* Xp; int ldX;
+  const double* Zp; int ldZ;
+  const double* Y;
+  double* part;  // [gridDim.x][vech]
+  unsigned* counter;
+  double* out;
+  int ld_out;    // < 0: packed upper triangle
+  double sign;
+};
+
+__global__ void __launch_bounds__(256) k_hess_small(const SmallArgs A) {
+  __shared__ double Ps[kSmallTI][65], Us[kSmallTI][64], Ms[kSmallTI][64];
+  __shared__ double Ys[kSmallTI][kSmallMaxKF];
+  __shared__ bool last;
+  const int tid = threadIdx.x, n = A.n_p, K = A.K, q = A.q, d = A.d, f = A.f;
+  const int V = n * (n + 1) / 2;
+  // column r -> (kind 0 beta / 1 alpha / 2 gamma, alternative, component)
+  auto cls = [&](int x, int& kind, int& k, int& idx) {
+    if (x < A.n_beta) { kind = 0; k = x / q + 1; idx = x - (k - 1) * q; }
+    else if (x < A.off_gamma) { kind = 1; k = (x - A.n_beta) / d; idx = x - A.n_beta - k * d; }
+    else { kind = 2; k = -1; idx = x - A.off_gamma; }
+  };
+  // this thread's entries j = tid + 256 t (row-major upper triangle order)
+  int er[kSmallEpt], ec[kSmallEpt];
+  double acc[kSmallEpt];
+#pragma unroll
+  for (int t = 0; t < kSmallEpt; ++t) {
+    acc[t] = 0.0;
+    er[t] = ec[t] = -1;
+    int j = tid + 256 * t;
+    if (j < V) {
+      int r = 0;
+      while (j >= n - r) { j -= n - r; ++r; }
+      er[t] = r;
+      ec[t] = r + j;
+    }
+  }
+  const int64_t ntiles = (A.N + kSmallTI - 1) / kSmallTI;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = tile * kSmallTI;
+    const int nt = (int)(A.N - i0 < kSmallTI ? A.N - i0 : kSmallTI);
+    __syncthreads();  // the previous tile's readers are done
+    // staging: read-only loads, unrolled so that each thread's loads are in flight together (one
+    // memory round trip per tile, not one per element)
+#pragma unroll 4
+    for (int e = tid; e < nt * K; e += 256) {
+      const int ii = e / K, k = e - ii * K;
+      Ps[ii][k] = __ldg(A.Pr + (i0 + ii) * A.ldP + k);
+    }
+#pragma unroll 4
+    for (int e = tid; e < nt * K * f; e += 256) {
+      const int ii = e / (K * f), o = e - ii * (K * f);
+      Ys[ii][o] = __ldg(A.Y + (i0 + ii) * (int64_t)(K * f) + o);
+    }
+#pragma unroll 4
+    for (int e = tid; e < nt * n; e += 256) {
+      const int ii = e / n, r = e - ii * n;
+      const int64_t i = i0 + ii;
+      int kind, k, idx;
+      cls(r, kind, k, idx);
+      const double P = __ldg(A.Pr + i * A.ldP + (kind == 2 ? K + idx : k));  // ybar_ie for gamma_e
+      const double m = kind == 0 ? __ldg(A.Xp + i * A.ldX + idx) : (kind == 1 ? __ldg(A.Zp + i * A.ldZ + k * d + idx) : 1.0);
+      Ms[ii][r] = m;
+      Us[ii][r] = P * m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < kSmallEpt; ++t) {
+      if (er[t] < 0) continue;
+      const int r = er[t], c = ec[t];
+      int kr, ar, ir, kc, ac, ic;
+      cls(r, kr, ar, ir);
+      cls(c, kc, ac, ic);
+      double s = 0.0;
+      for (int ii = 0; ii < nt; ++ii) {
+        double v = -Us[ii][r] * Us[ii][c];
+        if (kr != 2 && kc != 2) {
+          if (ar == ac) v = fma(Ps[ii][ar] * Ms[ii][r], Ms[ii][c], v);
+        } else if (kr != 2) {  // c is gamma_ic (r < c: gamma columns come last)
+          v = fma(Ps[ii][ar] * Ms[ii][r], Ys[ii][ar * f + ic], v);
+        } else {
+          for (int k = 0; k < K; ++k) v = fma(Ps[ii][k] * Ys[ii][k * f + ir], Ys[ii][k * f + ic], v);
+        }
+        s += v;
+      }
+      acc[t] += s;
+    }
+  }
+  double* my = A.part + (size_t)blockIdx.x * V;
+#pragma unroll
+  for (int t = 0; t < kSmallEpt; ++t)
+    if (er[t] >= 0) my[tid + 256 * t] = acc[t];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(A.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int t = 0; t < kSmallEpt; ++t) {
+    if (er[t] < 0) continue;
+    const int j = tid + 256 * t, r = er[t], c = ec[t];
+    double s = 0.0;
+    int b = 0;
+    for (; b + 8 <= (int)gridDim.x; b += 8) {  // 8 loads in flight, summed in CTA order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(A.part + (size_t)(b + u) * V + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; b < (int)gridDim.x; ++b) s += __ldcg(A.part + (size_t)b * V + j);
+    const double v = -A.sign * s;  // s = -H[r][c]
+    if (A.ld_out < 0) {
+      A.out[j] = v;  // row-major upper triangle: j is the packed index
+    } else {
+      A.out[(int64_t)r * A.ld_out + c] = v;
+      A.out[(int64_t)c * A.ld_out + r] = v;
+    }
+  }
+  if (tid == 0) *A.counter = 0u;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
@@ -821,6 +964,9 @@ struct GemmJob {
 };
 
 struct HessPlan {
+  bool small = false;  // n_p <= 64: k_hess_small, one launch (nothing below is used)
+  int small_grid = 0;
+  double* small_part = nullptr;
   bool has_j2;
   bool has_j2b = false;  // J2's Z/Y columns as whole main tiles + a narrow tail job (shares j2's A)
   int n2a = 0;           // Z/Y columns computed by j2
@@ -1012,10 +1158,34 @@ static int choose_bn_pipe(int MB) {
   return 48;
 }
 
+// k_hess_small serves problems whose Hessian is a few hundred to ~2000 entries and whose direct
+// per-individual work (N x vech x a few FMAs, + K per gamma-gamma entry) is small: there one launch
+// beats the GEMM pipeline's seven. MNL_NO_SMALL forces the general path (tests).
+static bool small_ok(const Dims& D) {
+  if (D.n_p > 64 || D.K > 65 || (int64_t)D.K * D.f > kSmallMaxKF || getenv("MNL_NO_SMALL")) return false;
+  const double V = D.n_p * (D.n_p + 1) / 2.0, G = D.f * (D.f + 1) / 2.0;
+  return (double)D.N * (3.0 * V + G * D.K) <= 5e8;
+}
+
 HessPlan* hess_plan_create(const Dims& D, const Packed& pk, int sms) {
   HessPlan* hp = new HessPlan();
   hp->sms = sms;
   const int K = D.K, q = D.q, d = D.d, f = D.f;
+  if (small_ok(D)) {
+    hp->small = true;
+    hp->small_grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (D.N + kSmallTI - 1) / kSmallTI));
+    const size_t vb = (size_t)D.n_p * (D.n_p + 1) / 2 * sizeof(double);
+    bool ok = cudaMalloc(&hp->small_part, vb * hp->small_grid) == cudaSuccess &&
+              cudaMalloc(&hp->counters, 2 * sizeof(unsigned)) == cudaSuccess &&
+              cudaMemset(hp->counters, 0, 2 * sizeof(unsigned)) == cudaSuccess;
+    for (auto& e : hp->ev) cudaEventCreate(&e);
+    hp->bytes = vb * hp->small_grid;
+    if (!ok) {
+      hess_plan_destroy(hp);
+      return nullptr;
+    }
+    return hp;
+  }
   // stage layouts: segment 0 = Pr, 1 = Xp, 2 = Zp; offsets are set per job below
   auto seg_ld = [&](int s) { return s == 0 ? pk.ldP : (s == 1 ? pk.ldX : pk.ldZ); };
   bool ok = true;
@@ -1244,6 +1414,7 @@ void hess_plan_destroy(HessPlan* hp) {
   free_job(hp->j2b);
   cudaFree(hp->Tpart);
   cudaFree(hp->T);
+  cudaFree(hp->small_part);
   cudaFree(hp->counters);
   for (auto& e : hp->ev)
     if (e) cudaEventDestroy(e);
@@ -1415,6 +1586,19 @@ static void launch_frag(const GemmJob& J, const Packed& pk, bool a_side, cudaStr
 cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const double* Y, double* out,
                            int ld_out, double sign, cudaStream_t st) {
   cudaEventRecord(hp->ev[7], st);
+  if (hp->small) {  // one launch; its time is reported as the J1 phase
+    cudaEventRecord(hp->ev[0], st);
+    SmallArgs A;
+    A.N = D.N; A.K = D.K; A.q = D.q; A.d = D.d; A.f = D.f; A.n_p = D.n_p;
+    A.n_beta = D.n_beta; A.off_gamma = D.off_gamma;
+    A.Pr = pk.Pr; A.ldP = pk.ldP; A.Xp = pk.Xp; A.ldX = pk.ldX; A.Zp = pk.Zp; A.ldZ = pk.ldZ; A.Y = Y;
+    A.part = hp->small_part; A.counter = hp->counters;
+    A.out = out; A.ld_out = ld_out; A.sign = sign;
+    k_hess_small<<<hp->small_grid, 256, 0, st>>>(A);
+    count_launch();
+    for (int i = 1; i <= 6; ++i) cudaEventRecord(hp->ev[i], st);
+    return cudaGetLastError();
+  }
   {  // operand materialisation: weights every evaluation, design-only products after a re-pack
     const GemmJob* jobs[4] = {&hp->j1, hp->has_j1b ? &hp->j1b : nullptr, hp->has_j2 ? &hp->j2 : nullptr,
                               hp->has_j2b ? &hp->j2b : nullptr};

@@ -167,6 +167,43 @@ def test_hessian_kernel_paths(mode):
         M.release()
 
 
+# n_p <= 64: the one-launch k_hess_small path (c1-sized; ragged tiles of 16, a single individual,
+# p = 0, K = 2, gamma-only and alpha-only designs, K f = 128 at the staging limit)
+SMALL_SHAPES = [(1000, 4, 3, 2, 1), (1, 3, 2, 1, 1), (17, 2, 5, 0, 0), (33, 5, 0, 2, 1), (4001, 8, 3, 2, 1),
+                (250, 6, 0, 3, 0), (300, 4, 0, 0, 2), (129, 16, 1, 8, 1), (70000, 3, 6, 4, 2)]
+
+
+@pytest.mark.parametrize("mode", ["default", "MNL_NO_SMALL"])
+def test_hessian_small_path(mode):
+    """Small problems (n_p <= 64) through the one-launch Hessian and, forced by MNL_NO_SMALL, through
+    the general GEMM path: both against the oracle's full Hessian at a perturbed theta, exactly
+    symmetric; the small path takes fewer launches."""
+    if mode != "default":
+        os.environ[mode] = "1"
+    M.release()
+    try:
+        for N, K, p, f, d in SMALL_SHAPES:
+            prob = datagen.custom(N, K, p, f, d, seed=11, coef_sd=0.3, require_all_classes=False)
+            assert prob.spec.n_params <= 64
+            D = oracle_data(prob)
+            dp = device_problem(prob)
+            th = datagen.perturbed_theta(prob, 0.1)
+            l_o, g_o, H_o = O.mnl_eval(D, th)
+            l, g, H = gpu_eval(dp, th)
+            check_lg(l, g, l_o, g_o)
+            rel = np.linalg.norm(H - H_o) / np.linalg.norm(H_o)
+            assert rel <= 1e-9, (mode, (N, K, p, f, d), rel)
+            assert np.array_equal(H, H.T)
+            launches = M.last_launch_count()
+            if mode == "default":
+                assert launches <= 4, launches  # pack, pass 1, its finalisation, k_hess_small
+            else:
+                assert launches >= 6, launches
+    finally:
+        os.environ.pop(mode, None)
+        M.release()
+
+
 def test_eval_without_grad_and_hess_and_determinism():
     prob = datagen.make("c2")
     dp = device_problem(prob)
