@@ -558,6 +558,41 @@ __global__ void __launch_bounds__(8 * 32 + 32, 1) k_pipe_gemm(const GemmParams P
   }
 }
 
+// Fixed-order split reduction with many splits over a small output (small problems split the
+// individuals over every SM): CTA = 32 element pairs x 8 groups of consecutive splits; each group
+// sums its splits in order, then the 8 group sums are added in group order (deterministic).
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(256) k_reduce_splits_wide(double* __restrict__ dst, const double* __restrict__ src,
+                                                            int64_t n, int S, int64_t stride) {
+  __shared__ double2 part[kRedGroups][32];
+  const int j = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = ((int64_t)blockIdx.x * 32 + j) * 2;
+  const int s0 = g * S / kRedGroups, s1 = (g + 1) * S / kRedGroups;
+  double2 acc = make_double2(0.0, 0.0);
+  if (e < n) {
+    int s = s0;
+    for (; s + 4 <= s1; s += 4) {  // 4 loads in flight, added in split order
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double2*>(src + (s + u) * stride + e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; }
+    }
+    for (; s < s1; ++s) {
+      const double2 v = *reinterpret_cast<const double2*>(src + s * stride + e);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+  }
+  part[g][j] = acc;
+  __syncthreads();
+  if (g == 0 && e < n) {
+    double2 t = part[0][j];
+    for (int h = 1; h < kRedGroups; ++h) { t.x += part[h][j].x; t.y += part[h][j].y; }
+    *reinterpret_cast<double2*>(dst + e) = t;
+  }
+}
+
 // Fixed-order split reduction: dst[e] = sum_s src[s * stride + e]  (stride even).
 __global__ void k_reduce_splits(double* __restrict__ dst, const double* __restrict__ src, int64_t n,
                                 int S, int64_t stride) {
@@ -1525,6 +1560,12 @@ static cudaError_t run_gemm_only(const GemmJob& J, const Packed& pk, unsigned* c
 // fixed-order sum of the job's split (x slab) partials
 static cudaError_t reduce_job(const GemmJob& J, cudaStream_t st) {
   const int64_t n = J.split_stride;
+  const int S = J.splits * J.nslab;
+  if (S >= 4 * kRedGroups && n % 2 == 0 && n < (int64_t)148 * 8 * 512) {  // many splits of a small output
+    k_reduce_splits_wide<<<(unsigned)((n / 2 + 31) / 32), 256, 0, st>>>(J.Cred, J.Cpart, n, S, J.split_stride);
+    count_launch();
+    return cudaGetLastError();
+  }
   const int blocks = (int)std::min<int64_t>((n / 2 + 255) / 256, 148 * 8);
   k_reduce_splits<<<blocks, 256, 0, st>>>(J.Cred, J.Cpart, n, J.splits * J.nslab, J.split_stride);
   count_launch();
@@ -1679,8 +1720,11 @@ cudaError_t launch_hessian(HessPlan* hp, const Dims& D, const Packed& pk, const 
       count_launch();
     }
     const int64_t n = (int64_t)D.K * E * F;
-    k_reduce_splits<<<(int)std::min<int64_t>((n / 2 + 256) / 256, 1024), 256, 0, st>>>(hp->T, hp->Tpart, n,
-                                                                                       hp->ar_splits, (n + 1) / 2 * 2);
+    if (hp->ar_splits >= 4 * kRedGroups && n % 2 == 0)
+      k_reduce_splits_wide<<<(unsigned)((n / 2 + 31) / 32), 256, 0, st>>>(hp->T, hp->Tpart, n, hp->ar_splits, n);
+    else
+      k_reduce_splits<<<(int)std::min<int64_t>((n / 2 + 256) / 256, 1024), 256, 0, st>>>(hp->T, hp->Tpart, n,
+                                                                                         hp->ar_splits, (n + 1) / 2 * 2);
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
