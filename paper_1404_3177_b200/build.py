@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libmnl.so")
 HOST_OUT = os.path.join(HERE, "lib", "libnrhost.so")   # the same NR driver over host callbacks (CPU tests)
-SOURCES = ["mnl_api.cu", "k_eval.cu", "k_hess.cu", "k_chol.cu"]
+SOURCES = ["mnl_api.cu", "k_eval.cu", "k_eval_w.cu", "k_hess.cu", "k_chol.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
@@ -20,6 +20,7 @@ def stale() -> bool:
         return True
     t = os.path.getmtime(OUT)
     deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "internal.h"),
+                                                       os.path.join(CSRC, "eval_common.h"),
                                                        os.path.join(CSRC, "nr_driver.h"),
                                                        os.path.join(HERE, "..", "include", "mnl.h")]
     return any(os.path.getmtime(p) > t for p in deps)
@@ -46,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     cflags = [f for f in FLAGS if f != "-shared"]
     jobs, text = [], ""
-    hdrs = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "nr_driver.h"),
+    hdrs = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "eval_common.h"), os.path.join(CSRC, "nr_driver.h"),
             os.path.join(HERE, "..", "include", "mnl.h")]
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))

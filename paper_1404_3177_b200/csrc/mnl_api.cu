@@ -248,7 +248,7 @@ int run_hessvec(Workspace& W, const Dims& D, const EvalPlan& ep, const double* X
   if (!grow(&W.part, &W.cpart, eval_part_doubles(ep))) return MNL_ERR_CUDA;
   cudaError_t e = launch_hessvec(D, ep, X, Y, Z, choice, v, pk, W.part, W.err, st);
   if (e != cudaSuccess) return MNL_ERR_CUDA;
-  e = launch_eval_finalize(D, ep, W.part, true, hv, nullptr, W.scal, W.err, W.counter, st);
+  e = launch_eval_finalize(D, ep, W.part, true, hv, nullptr, W.scal, W.err, W.counter, st, nullptr, true);
   if (e != cudaSuccess) return MNL_ERR_CUDA;
   if (ex && ex->fn(hv, D.n_p, st, ex->ctx) != 0) return MNL_ERR_CUDA;
   return MNL_OK;
