@@ -9,10 +9,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libmnl.so")
 HOST_OUT = os.path.join(HERE, "lib", "libnrhost.so")   # the same NR driver over host callbacks (CPU tests)
-SOURCES = ["mnl_api.cu", "k_eval.cu", "k_eval_w.cu", "k_hess.cu", "k_chol.cu"]
+SOURCES = ["mnl_api.cu", "k_eval.cu", "k_eval_w.cu", "k_eval_w1.cu", "k_eval_w2.cu", "k_hess.cu", "k_chol.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v",
+         *os.environ.get("MNL_NVCC_EXTRA", "").split()]
 
 
 def stale() -> bool:
@@ -47,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     cflags = [f for f in FLAGS if f != "-shared"]
     jobs, text = [], ""
-    hdrs = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "eval_common.h"), os.path.join(CSRC, "nr_driver.h"),
+    hdrs = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "eval_common.h"), os.path.join(CSRC, "k_eval_w.cu"), os.path.join(CSRC, "nr_driver.h"),
             os.path.join(HERE, "..", "include", "mnl.h")]
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))

@@ -63,9 +63,10 @@ void count_launch(int n = 1);
 // Per-CTA partials layout: [2 + n_p] doubles: l_sum, l_comp, grad[n_p].
 // Shared-memory layout (in doubles) of the group mapping (k_eval_w.cu); nwk = 0: not in use.
 struct EvalWLayout {
-  int nwk;                  // warps per CTA
+  int T, S, NBW;            // teams per CTA (0: not in use), warps per team, alternative blocks per warp
   int KS, RS, YS, ZS, XH;   // strides: beta table rows, residual rows, Y / Z ring slots, x block of a group
-  int off_cf, off_warp, warp_sz;
+  int off_gam, off_team, team_sz;
+  size_t smem;
 };
 struct EvalPlan {
   int grid, block, kpl, cm;
@@ -75,15 +76,14 @@ struct EvalPlan {
   int ti;       // individuals per tile
   size_t smem;
   int n_part;  // 2 + n_p
-  // the group mapping (k_eval_w.cu), used by launch_eval when w.nwk > 0 (not by launch_hessvec)
+  // the group mapping (k_eval_w.cu), used by launch_eval when w.T > 0 (not by launch_hessvec)
   EvalWLayout w;
   int w_grid;
-  size_t w_smem;
 };
 bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
 void eval_plan_w(const Dims& D, EvalPlan* plan, int device_sms);
 // CTA partial rows written by launch_eval (hv = false) / launch_hessvec (hv = true) with this plan
-inline int eval_nblk(const EvalPlan& ep, bool hv) { return (!hv && ep.w.nwk) ? ep.w_grid : ep.grid; }
+inline int eval_nblk(const EvalPlan& ep, bool hv) { return (!hv && ep.w.T) ? ep.w_grid : ep.grid; }
 // doubles of the `part` scratch a launch with this plan needs (CTA partials + stream-mode residual rows)
 inline size_t eval_part_doubles(const EvalPlan& ep) {
   return (size_t)(ep.grid > ep.w_grid ? ep.grid : ep.w_grid) * ep.n_part + ep.rg;
@@ -112,7 +112,17 @@ cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const doub
                                  bool want_grad, double* grad, double* loglik_out, double* scal,
                                  const int* err, unsigned* counter, cudaStream_t st,
                                  int* status_out = nullptr, bool hv = false);
+// The team mapping (k_eval_w.cu; its instantiations are split over three translation units by f).
 cudaError_t launch_eval_w(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
+                          const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
+                          double* part, int* err, cudaStream_t st);
+cudaError_t launch_eval_w_part0(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
+                          const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
+                          double* part, int* err, cudaStream_t st);
+cudaError_t launch_eval_w_part1(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
+                          const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
+                          double* part, int* err, cudaStream_t st);
+cudaError_t launch_eval_w_part2(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
                           double* part, int* err, cudaStream_t st);
 // Data-parallel exchange of one evaluation: xbuf [2 + n] = [l, bad-choice flag, g] from the

@@ -134,6 +134,73 @@ def test_eval_yz_paths(mode):
         os.environ.pop(mode, None)
 
 
+# Team mapping of pass 1 (k_eval_w.cu): shapes across its layout cases — K below, at and above the
+# 8-alternative blocks and the 16-alternative warps (one to four warps per team), a ragged last group
+# (N not a multiple of 8, re-read as the last 8 rows), N = 8 and 9, p = 0 / odd / 32 (the x column
+# blocks), f = 0 or d = 0, the capacity limits f = 16, d = 8, K = 64 (a single team per SM), and a
+# problem of several CTAs with more groups than teams.
+# (A ragged N needs (N - 8) p even; K d even: the bulk copies' 16-byte alignment.)
+TEAM_SHAPES = [(1000, 4, 3, 2, 1), (334, 50, 5, 10, 5), (2050, 6, 17, 2, 3), (65, 20, 0, 4, 0), (8, 4, 2, 2, 1),
+               (9, 6, 0, 2, 2), (24, 64, 1, 16, 8), (40, 34, 2, 6, 7), (130, 16, 32, 0, 2), (72, 17, 31, 2, 0),
+               (500, 9, 4, 8, 6), (60, 2, 2, 2, 1), (208, 48, 7, 12, 4), (256, 56, 30, 10, 5), (30000, 12, 9, 4, 3),
+               (20001, 50, 30, 10, 5)]
+
+
+@pytest.mark.parametrize("shape", TEAM_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_eval_team_mapping(shape):
+    """Pass 1 through the team mapping (forced for the shapes below its size thresholds) against the
+    oracle: loglik, gradient, and the probability rows / ybar through the full Hessian; then the
+    same numbers as the YZS / direct paths within the parity tolerances; the gradient pass and the
+    Hessian pass give bit-identical loglik and gradient."""
+    N, K, p, f, d = shape
+    prob = datagen.custom(N, K, p, f, d, seed=11, coef_sd=0.3, require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    th = datagen.perturbed_theta(prob, 0.2)
+    l_o, g_o, H_o = O.mnl_eval(D, th)
+    os.environ["MNL_FORCE_YZW"] = "1"
+    try:
+        l, g, H = gpu_eval(dp, th)
+        l2, g2, _ = gpu_eval(dp, th, hess=False)
+        l3, _, _ = M.mnl_eval(dp, dev(th), grad=False, hess=False)
+    finally:
+        os.environ.pop("MNL_FORCE_YZW", None)
+    check_lg(l, g, l_o, g_o)
+    assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+    assert l2 == l and np.array_equal(g2, g) and l3.item() == l
+    os.environ["MNL_NO_YZW"] = "1"
+    try:
+        l_y, g_y, _ = gpu_eval(dp, th, hess=False)
+    finally:
+        os.environ.pop("MNL_NO_YZW", None)
+    check_lg(l, g, l_y, g_y)
+
+
+def test_eval_team_mapping_bad_choice_and_nonfinite():
+    """The team mapping reports a choice outside 0..K-1 (MNL_ERR_ARG) and a NaN anywhere in Y or Z
+    (MNL_ERR_NONFINITE), also in a row of the ragged last group."""
+    N, K, p, f, d = 8201, 11, 3, 4, 2
+    prob = datagen.custom(N, K, p, f, d, seed=12, coef_sd=0.3, require_all_classes=False)
+    dp = device_problem(prob)
+    th = dev(prob.theta_true)
+    ch = dp.choice.clone()
+    ch[N - 1] = K
+    with pytest.raises(M.MnlError) as ei:
+        M.mnl_eval(M.problem(dp.X, dp.Y, dp.Z, ch, K=K), th, grad=True, hess=False)
+    assert ei.value.code == M.MNL_ERR_ARG
+    for i, k, e in [(0, 0, 0), (N // 2, K - 1, f - 1), (N - 1, 5, 1)]:
+        Y = dp.Y.clone()
+        Y[i, k, e] = float("nan")
+        with pytest.raises(M.MnlError) as ei:
+            M.mnl_eval(M.problem(dp.X, Y, dp.Z, dp.choice, K=K), th, grad=True, hess=False)
+        assert ei.value.code == M.MNL_ERR_NONFINITE
+    Z = dp.Z.clone()
+    Z[N - 3, 2, 1] = float("inf")
+    with pytest.raises(M.MnlError) as ei:
+        M.mnl_eval(M.problem(dp.X, dp.Y, Z, dp.choice, K=K), th, grad=True, hess=False)
+    assert ei.value.code == M.MNL_ERR_NONFINITE
+
+
 # Shapes that select each GEMM kernel: J2 materialised (K d + f >= 192) with a generated J1;
 # J1 split into 128-wide tiles + a 48-wide tail (vech 1326 = 10 x 128 + 46); vech 300 = 256 + 44;
 # vech 496 = 3 x 128 + a 112-wide tail.
