@@ -38,27 +38,48 @@ __device__ __forceinline__ void neu_add(double& s, double& c, double x) {
   s = t;
 }
 
-// e^x for the shifted utilities x = u - m <= ~0 (a2). x = n ln2 + r (|r| <= ln2/2, Cody-Waite with
-// fdlibm's split ln2, exact n ln2_hi), e^r by its Taylor polynomial to degree 12 (truncation
-// < 2e-16 relative) in Estrin form (short dependency chain), times 2^n built in the exponent field.
-// x < -708 (e^x < 3.3e-308, below the normal range) returns 0; NaN propagates; -inf gives 0.
-__device__ __forceinline__ double exp_shifted(double x) {
-  const double t = rint(x * 1.4426950408889634);
-  double r = fma(t, -6.93147180369123816490e-01, x);
-  r = fma(t, -1.90821492927058770002e-10, r);
+// Coefficients of the exponentials below, in constant memory: they enter the DFMAs as constant-bank
+// operands (no registers, no move instructions).
+__constant__ double c_exp[15] = {1.4426950408889634,            // log2 e
+                                 -6.93147180369123816490e-01,   // -ln2 (fdlibm's high part)
+                                 -1.90821492927058770002e-10,   // -ln2 (low part)
+                                 1.0 / 6.0,        0.5,
+                                 1.0 / 120.0,      1.0 / 24.0,
+                                 1.0 / 5040.0,     1.0 / 720.0,
+                                 1.0 / 362880.0,   1.0 / 40320.0,
+                                 1.0 / 39916800.0, 1.0 / 3628800.0,
+                                 1.0 / 479001600.0, 1.0};
+
+// 2^j for an integer j <= ~1000 (0 below the normal range)
+__device__ __forceinline__ double pow2_int(int j) { return __hiloint2double((max(j, -1023) + 1023) << 20, 0); }
+
+// e^r for |r| <= ~ln2/2: the Taylor polynomial to degree 12 (truncation < 2e-16 relative) in Estrin
+// form (short dependency chain).
+__device__ __forceinline__ double exp_poly(double r) {
   const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-  const double p01 = 1.0 + r;
-  const double p23 = fma(r, 1.0 / 6.0, 0.5);
-  const double p45 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  const double p67 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
-  const double p89 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
-  const double pab = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
+  const double p01 = c_exp[14] + r;
+  const double p23 = fma(r, c_exp[3], c_exp[4]);
+  const double p45 = fma(r, c_exp[5], c_exp[6]);
+  const double p67 = fma(r, c_exp[7], c_exp[8]);
+  const double p89 = fma(r, c_exp[9], c_exp[10]);
+  const double pab = fma(r, c_exp[11], c_exp[12]);
   const double q0 = fma(r2, p23, p01), q1 = fma(r2, p67, p45);
-  const double q2 = fma(r2, pab, p89), q3 = 1.0 / 479001600.0;
-  const double s0 = fma(r4, q1, q0), s1 = fma(r4, q3, q2);
-  const double e = fma(r8, s1, s0);
-  const double scale = __longlong_as_double((long long)(__double2int_rn(t) + 1023) << 52);
-  return x < -708.0 ? 0.0 : e * scale;
+  const double q2 = fma(r2, pab, p89);
+  const double s0 = fma(r4, q1, q0), s1 = fma(r4, c_exp[13], q2);
+  return fma(r8, s1, s0);
+}
+
+// e^x for the shifted utilities x = u - m <= ~0 (a2). x = n ln2 + r (|r| <= ln2/2, Cody-Waite with
+// fdlibm's split ln2, exact n ln2_hi), e^r by exp_poly, times 2^n built in the exponent field.
+// Branch-free (a branch per call would serialise the calls of a lane's alternatives): x below
+// -1000 (e^x = 0 in double; -inf for the alternatives >= K) is clamped, 2^n is 0 below the normal
+// range (e^x < 2.2e-308), and a NaN propagates.
+__device__ __forceinline__ double exp_shifted(double x) {
+  const double xc = x < -1000.0 ? -1000.0 : x;
+  const double t = rint(xc * c_exp[0]);
+  double r = fma(t, c_exp[1], xc);
+  r = fma(t, c_exp[2], r);
+  return exp_poly(r) * pow2_int(__double2int_rn(t));
 }
 
 // 1 / s for the softmax row sums s >= ~1 (the shifted maximum contributes ~1): the hardware

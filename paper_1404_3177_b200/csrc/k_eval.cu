@@ -141,7 +141,7 @@ __device__ __forceinline__ void phase_e(const EvalArgs& A, const double* Us, dou
       double ssum = 0.0;
   #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        const double e = kok[kk] ? exp_shifted(u[kk] - m) : 0.0;
+        const double e = exp_shifted(u[kk] - m);  // (u = -inf where the alternative does not exist: 0)
         ssum += e;
         u[kk] = e;
       }
@@ -321,7 +321,7 @@ __device__ __forceinline__ void phase_e_reg(const EvalArgs& A, const double* Us,
       double ssum = 0.0;
   #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        const double e = kok[kk] ? exp_shifted(u[kk] - m) : 0.0;
+        const double e = exp_shifted(u[kk] - m);  // (u = -inf where the alternative does not exist: 0)
         ssum += e;
         u[kk] = e;
       }
@@ -634,7 +634,7 @@ __device__ __forceinline__ void yzs_rows(const EvalArgs& A, double* Rs, const in
       ssum[j] = 0.0;
 #pragma unroll
       for (int kk = 0; kk < KPL; ++kk) {
-        const double e = kok[kk] ? exp_shifted(u[j][kk] - m) : 0.0;
+        const double e = exp_shifted(u[j][kk] - m);  // (u = -inf where the alternative does not exist: 0)
         ssum[j] += e;
         u[j][kk] = e;
       }
@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
       for (int h = 0; h < 2; ++h) {
         const int k = nb * 8 + 2 * r4 + h;
         if (k == y) uy = u[nb][h];
-        const double e = (k < K) ? exp_shifted(u[nb][h] - m) : 0.0;
+        const double e = exp_shifted(u[nb][h] - m);  // (u = -inf for k >= K: 0)
         u[nb][h] = e;
         ssum += e;
       }

@@ -74,49 +74,20 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
                : "memory");
 }
 
-// 2^j for an integer j <= ~1000 (0 below the normal range)
-__device__ __forceinline__ double pow2_int(int j) { return __hiloint2double((max(j, -1023) + 1023) << 20, 0); }
-// ... for an integer-valued double (the conversion saturates; NaN gives 2^0)
+// 2^j for an integer-valued double (the conversion saturates; NaN gives 2^0)
 __device__ __forceinline__ double pow2_nonpos(double j) { return pow2_int(min(__double2int_rn(j), 1000)); }
 
 // e^u 2^{-n} for an integer-valued double n with u - n ln 2 <= ~1 and finite u: u = t ln2 + r
-// (|r| <= ln2/2, Cody-Waite with fdlibm's split ln2), e^r by its Taylor polynomial to degree 12 in
-// Estrin form (as exp_shifted), times 2^{t - n} built in the exponent field (0 below the normal
-// range). Branch-free, so that the calls of a lane's alternatives interleave; the coefficients sit
-// in constant memory (operands of the DFMAs, no registers). NaN and +-inf give NaN.
-__constant__ double c_exp[15] = {1.4426950408889634,
-                                 -6.93147180369123816490e-01,
-                                 -1.90821492927058770002e-10,
-                                 1.0 / 6.0,
-                                 0.5,
-                                 1.0 / 120.0,
-                                 1.0 / 24.0,
-                                 1.0 / 5040.0,
-                                 1.0 / 720.0,
-                                 1.0 / 362880.0,
-                                 1.0 / 40320.0,
-                                 1.0 / 39916800.0,
-                                 1.0 / 3628800.0,
-                                 1.0 / 479001600.0,
-                                 1.0};
+// (|r| <= ln2/2, Cody-Waite with fdlibm's split ln2), e^r by exp_poly, times 2^{t - n} built in the
+// exponent field (0 below the normal range). Branch-free, so that the calls of a lane's
+// alternatives interleave. NaN and +-inf give NaN. live = false (an alternative >= K): times 0.
 __device__ __forceinline__ double exp_scaled(double u, double n, bool live) {
   const double t = rint(u * c_exp[0]);
   double r = fma(t, c_exp[1], u);
   r = fma(t, c_exp[2], r);
-  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-  const double p01 = c_exp[14] + r;
-  const double p23 = fma(r, c_exp[3], c_exp[4]);
-  const double p45 = fma(r, c_exp[5], c_exp[6]);
-  const double p67 = fma(r, c_exp[7], c_exp[8]);
-  const double p89 = fma(r, c_exp[9], c_exp[10]);
-  const double pab = fma(r, c_exp[11], c_exp[12]);
-  const double q0 = fma(r2, p23, p01), q1 = fma(r2, p67, p45);
-  const double q2 = fma(r2, pab, p89);
-  const double s0 = fma(r4, q1, q0), s1 = fma(r4, c_exp[13], q2);
-  const double e = fma(r8, s1, s0);
   // t - n is exact (integers below 2^53); the conversion saturates; NaN converts to 0
-  const int ji = live ? min(__double2int_rn(t - n), 1000) : -2000;  // not live: times 0
-  return e * pow2_int(ji);
+  const int ji = live ? min(__double2int_rn(t - n), 1000) : -2000;
+  return exp_poly(r) * pow2_int(ji);
 }
 
 template <int NBW, int F2, int D, bool WP>

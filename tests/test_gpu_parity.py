@@ -179,7 +179,7 @@ def test_eval_team_mapping(shape):
 def test_eval_team_mapping_bad_choice_and_nonfinite():
     """The team mapping reports a choice outside 0..K-1 (MNL_ERR_ARG) and a NaN anywhere in Y or Z
     (MNL_ERR_NONFINITE), also in a row of the ragged last group."""
-    N, K, p, f, d = 8201, 11, 3, 4, 2
+    N, K, p, f, d = 8204, 11, 4, 4, 2
     prob = datagen.custom(N, K, p, f, d, seed=12, coef_sd=0.3, require_all_classes=False)
     dp = device_problem(prob)
     th = dev(prob.theta_true)
@@ -195,7 +195,7 @@ def test_eval_team_mapping_bad_choice_and_nonfinite():
             M.mnl_eval(M.problem(dp.X, Y, dp.Z, dp.choice, K=K), th, grad=True, hess=False)
         assert ei.value.code == M.MNL_ERR_NONFINITE
     Z = dp.Z.clone()
-    Z[N - 3, 2, 1] = float("inf")
+    Z[N - 3, 2, 1] = float("nan")
     with pytest.raises(M.MnlError) as ei:
         M.mnl_eval(M.problem(dp.X, dp.Y, Z, dp.choice, K=K), th, grad=True, hess=False)
     assert ei.value.code == M.MNL_ERR_NONFINITE
