@@ -992,23 +992,26 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
         if (in_b) *reinterpret_cast<double2*>(Rrow + k) = R2;
       }
     } else {
-    int y = valid ? ch_t[il] : 0;
+    int y = valid ? ch_t[il] : -1;  // -1 (a row beyond N): no alternative matches, residuals 0
     if (valid && (y < 0 || y >= K)) {
       atomicOr(A.err, 1);
       y = 0;
     }
+    // shift by the (fp32-rounded) maximum: any shift is exact for the softmax, it only has to keep
+    // e^{u - m} <= ~1 (R12); the fp32 maximum costs two instructions per alternative off the FP64
+    // pipe, which the DMMAs of the other warps need
+    float mf = -INFINITY;
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int k = nb * 8 + 2 * r4 + h;
         if (k >= K) u[nb][h] = -INFINITY;
+        mf = fmaxf(mf, (float)u[nb][h]);
       }
-    double m = -INFINITY;
-#pragma unroll
-    for (int nb = 0; nb < NBN; ++nb) m = fmax(m, fmax(u[nb][0], u[nb][1]));
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, 1));
+    mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, 2));
+    const double m = (double)mf;
     double ssum = 0.0, uy = 0.0;
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb)
@@ -1025,18 +1028,17 @@ __global__ void __launch_bounds__((YZS ? NWY : NW) * 32, 1) k_eval_kernel(const 
     uy += __shfl_xor_sync(0xffffffffu, uy, 1);
     uy += __shfl_xor_sync(0xffffffffu, uy, 2);
     if (valid && r4 == 0) neu_add(l_s, l_c, uy - (m + log(ssum)));
-    const double inv_s = recip_ge1(ssum);
+    // a row beyond N: P = 0 and (y = -1) r = 0; an alternative >= K: e = 0, so P = r = 0
+    const double inv_s = valid ? recip_ge1(ssum) : 0.0;
     double* Rrow = Rs + il * KPS;
 #pragma unroll
     for (int nb = 0; nb < NBN; ++nb) {
       const int k = nb * 8 + 2 * r4;
       double2 P2, R2;
-      P2.x = valid ? u[nb][0] * inv_s : 0.0;
-      P2.y = valid ? u[nb][1] * inv_s : 0.0;
-      R2.x = valid ? ((k == y ? 1.0 : 0.0) - P2.x) : 0.0;
-      R2.y = valid ? ((k + 1 == y ? 1.0 : 0.0) - P2.y) : 0.0;
-      if (k >= K) { P2.x = 0.0; R2.x = 0.0; }
-      if (k + 1 >= K) { P2.y = 0.0; R2.y = 0.0; }
+      P2.x = __dmul_rn(u[nb][0], inv_s);  // (rounded products: the same r with and without the P rows)
+      P2.y = __dmul_rn(u[nb][1], inv_s);
+      R2.x = (k == y ? 1.0 : 0.0) - P2.x;
+      R2.y = (k + 1 == y ? 1.0 : 0.0) - P2.y;
       if (in_b) *reinterpret_cast<double2*>(Rrow + k) = R2;
       if (A.writeP && valid) {
         double* pr = A.Pr + i * A.ldP + k;
