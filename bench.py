@@ -514,7 +514,7 @@ def pass1_extra(cfg: str, seed: int, reps: int = 20):
     f = M.mnl_newton_fit(dp, tol=1e-6, method="cg")
     t_cg = time.perf_counter() - t0
     return {"config": f"{cfg}: N={s.N} K={s.K} p={s.p} f={s.f} d={s.d} n_p={s.n_params}",
-            "pass1_roofline": {"kernel": "k_eval_kernel (fused a1-a4 pass, gradient, no Hessian)", "bound": "hbm",
+            "pass1_roofline": {"kernel": "k_eval_w (fused a1-a4 pass, team mapping; gradient, no Hessian)", "bound": "hbm",
                                "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                                "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": ms},
             "cg_fit": {"fit_s": t_cg, "iters": f.iters, "cg_iters": f.stats["cg_iters"], "status": f.status,
