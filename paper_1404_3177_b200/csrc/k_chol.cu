@@ -419,11 +419,14 @@ __global__ void __launch_bounds__(256, 1) k_chol_dag(int n, int nt, const double
   auto wait_flag = [&](int fi) {
     while (ld_acquire(flags + fi) != epoch) __nanosleep(64);
   };
+  // next_task == nullptr: a single tile (n <= 64) in a single CTA, launched plainly: no task
+  // counter, and info is cleared here instead of by a memset before the launch
+  if (!next_task && tid == 0) *info = 0;
   int g = 0, grp0 = 0;
-  for (;;) {
+  for (int it = 0;; ++it) {
     // dynamic dealing in the topological order: a CTA takes the next task when it is free (the
     // tasks it waits on were all taken before it, by running CTAs, so this cannot deadlock)
-    if (tid == 0) task_s = atomicAdd(next_task, 1);
+    if (tid == 0) task_s = next_task ? atomicAdd(next_task, 1) : it;
     __syncthreads();
     const int t = task_s;
     __syncthreads();
@@ -975,6 +978,14 @@ cudaError_t factor_dag(CholCtx& c, int n, const double* A, int lda, int* info, c
   const int ntask = nt * (nt + 1) / 2 - (nt - 1);  // the sub-diagonal tiles ride with the diagonal tasks
   const int grid = std::min(ntask, c.sms * c.occ);
   int epoch = ++c.depoch;
+  if (nt == 1) {
+    // one tile: one CTA, nothing to wait for -- a plain launch, no memsets (c1's Newton step: the
+    // whole solve in this one launch)
+    k_chol_dag<<<1, 256, kDagSmem, st>>>(n, nt, A, lda, c.Lt, c.LinvP, c.Linv, b, c.ybuf, x, info, c.dflags, epoch,
+                                         nullptr);
+    count_launch();
+    return cudaGetLastError();
+  }
   int* next_task = c.dflags + c.cap_lt;  // past every flag slot (never read as a flag)
   cudaMemsetAsync(info, 0, sizeof(int), st);
   cudaMemsetAsync(next_task, 0, sizeof(int), st);
