@@ -76,14 +76,14 @@ struct EvalPlan {
   int ti;       // individuals per tile
   size_t smem;
   int n_part;  // 2 + n_p
-  // the group mapping (k_eval_w.cu), used by launch_eval when w.T > 0 (not by launch_hessvec)
+  // the group mapping (k_eval_w.cu), used by launch_eval and launch_hessvec when w.T > 0
   EvalWLayout w;
   int w_grid;
 };
 bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
 void eval_plan_w(const Dims& D, EvalPlan* plan, int device_sms);
-// CTA partial rows written by launch_eval (hv = false) / launch_hessvec (hv = true) with this plan
-inline int eval_nblk(const EvalPlan& ep, bool hv) { return (!hv && ep.w.T) ? ep.w_grid : ep.grid; }
+// CTA partial rows written by launch_eval / launch_hessvec with this plan
+inline int eval_nblk(const EvalPlan& ep, bool) { return ep.w.T ? ep.w_grid : ep.grid; }
 // doubles of the `part` scratch a launch with this plan needs (CTA partials + stream-mode residual rows)
 inline size_t eval_part_doubles(const EvalPlan& ep) {
   return (size_t)(ep.grid > ep.w_grid ? ep.grid : ep.w_grid) * ep.n_part + ep.rg;
@@ -115,16 +115,16 @@ cudaError_t launch_eval_finalize(const Dims& D, const EvalPlan& plan, const doub
 // The team mapping (k_eval_w.cu; its instantiations are split over three translation units by f).
 cudaError_t launch_eval_w(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
-                          double* part, int* err, cudaStream_t st);
+                          bool hv, double* part, int* err, cudaStream_t st);
 cudaError_t launch_eval_w_part0(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
-                          double* part, int* err, cudaStream_t st);
+                          bool hv, double* part, int* err, cudaStream_t st);
 cudaError_t launch_eval_w_part1(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
-                          double* part, int* err, cudaStream_t st);
+                          bool hv, double* part, int* err, cudaStream_t st);
 cudaError_t launch_eval_w_part2(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
-                          double* part, int* err, cudaStream_t st);
+                          bool hv, double* part, int* err, cudaStream_t st);
 // Data-parallel exchange of one evaluation: xbuf [2 + n] = [l, bad-choice flag, g] from the
 // finalised scalars [l, ||g||^2, flag] (+ g, or zeros if grad is null); after the all-reduce,
 // grad (if not null) <- the summed g and scal <- [l, ||g||^2, flag] of the sums.

@@ -1570,13 +1570,14 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
                         const double* Z, const int32_t* choice, const double* coef,
                         const Packed* pk, bool want_grad, bool writeP, double* part, int* err,
                         cudaStream_t st) {
-  if (plan.w.T) return launch_eval_w(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, part, err, st);
+  if (plan.w.T) return launch_eval_w(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, false, part, err, st);
   return launch_eval_impl(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, false, part, err, st);
 }
 
 cudaError_t launch_hessvec(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                            const int32_t* choice, const double* v, const Packed* pk, double* part, int* err,
                            cudaStream_t st) {
+  if (plan.w.T) return launch_eval_w(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
   return launch_eval_impl(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
 }
 

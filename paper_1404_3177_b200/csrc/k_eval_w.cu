@@ -90,7 +90,7 @@ __device__ __forceinline__ double exp_scaled(double u, double n, bool live) {
   return exp_poly(r) * pow2_int(ji);
 }
 
-template <int NBW, int F2, int D, bool WP>
+template <int NBW, int F2, int D, bool WP, bool HV>
 __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalArgs A, const EvalWLayout L) {
   extern __shared__ __align__(16) double sm[];
   constexpr int f = 2 * F2;
@@ -221,6 +221,19 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
       if (valid && r4 == 0 && wt == 0) atomicOr(A.err, 1);
       y = 0;
     }
+    // Hessian-vector product: P_i of the last evaluation (its loads land behind the wait)
+    double pk[NBW][2];
+    if constexpr (HV) {
+#pragma unroll
+      for (int nb = 0; nb < NBW; ++nb) {
+        const double* pr = A.Pr + gi * A.ldP + 8 * (wt * NBW + nb) + 2 * r4;
+        double2 P2 = make_double2(0.0, 0.0);
+        if (ok(nb, 1)) P2 = __ldg(reinterpret_cast<const double2*>(pr));
+        else if (ok(nb, 0)) P2.x = __ldg(pr);
+        pk[nb][0] = P2.x;
+        pk[nb][1] = P2.y;
+      }
+    }
     mbar_wait(bar_s + 8u * half, upar);
     const double* xb = Xb + half * XH;
     const double* yb = Yr + (half * GR + c8) * YS;
@@ -290,6 +303,28 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
           }
       }
     }
+    double r[NBW][2];
+    const int yl = y - 8 * wt * NBW;  // y relative to this warp's alternatives
+    if constexpr (HV) {
+      // ---- Hessian-vector product: u holds s_ik = (J_i v)_k; r_ik = -P_ik (s_ik - sum_l P_il s_il), so
+      // that the gradient contractions below accumulate H v (P:462-476 applied to v); one exchange
+      // of the partial sums over the team ----
+      double ps = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NBW; ++nb) ps = fma(pk[nb][1], u[nb][1], fma(pk[nb][0], u[nb][0], ps));
+      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+      if (r4 == 0) Ex[((half * S + wt) * GR + c8) * 2] = ps;
+      asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_n) : "memory");
+      const double* ex = Ex + (half * S * GR + c8) * 2;
+      double pt = (r4 < S ? ex[r4 * GR * 2] : 0.0) + (r4 + 4 < S ? ex[(r4 + 4) * GR * 2] : 0.0);
+      pt += __shfl_xor_sync(0xffffffffu, pt, 1);
+      pt += __shfl_xor_sync(0xffffffffu, pt, 2);
+#pragma unroll
+      for (int nb = 0; nb < NBW; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) r[nb][h] = valid ? -pk[nb][h] * (u[nb][h] - pt) : 0.0;
+    } else {
     // ---- a2 / a3: softmax over the team, loglik ----
     float mf = -INFINITY;
 #pragma unroll
@@ -304,7 +339,6 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
     // cannot occur: its first block starts below K)
     const double nt = rint((double)mf * 1.4426950408889634);
     double ssum = 0.0;
-    const int yl = y - 8 * wt * NBW;  // y relative to this warp's alternatives
 #pragma unroll
     for (int nb = 0; nb < NBW; ++nb)
 #pragma unroll
@@ -340,7 +374,6 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
       neu_add(l_s, l_c, fma(nmax, -1.90821492927058770002e-10, fma(nmax, -6.93147180369123816490e-01, uy)) - log(stot));
     }
     const double cs = pow2_nonpos(nt - nmax) * recip_ge1(stot);
-    double r[NBW][2];
 #pragma unroll
     for (int nb = 0; nb < NBW; ++nb) {
       const int k = 8 * nb + 2 * r4;
@@ -355,6 +388,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
         else if (ok(nb, 0)) pr[0] = P0;
       }
     }
+    }  // !HV
     if (A.want_grad || WP) {
       // ---- a4: gamma gradient sum_k y_ke r_k in the same layout; WP: ybar_e = y_{y,e} - that sum ----
 #pragma unroll
@@ -516,15 +550,15 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
   }
 }
 
-template <int NBW, int F2, int D, bool WP>
+template <int NBW, int F2, int D, bool WP, bool HV>
 cudaError_t launch_w(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static uint64_t attr_mask = 0;
   cudaError_t e = set_once_per_device(attr_mask, [] {
-    return cudaFuncSetAttribute(k_eval_w<NBW, F2, D, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return cudaFuncSetAttribute(k_eval_w<NBW, F2, D, WP, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (e != cudaSuccess) return e;
   const EvalWLayout& L = plan.w;
-  k_eval_w<NBW, F2, D, WP><<<plan.w_grid, L.S * L.T * 32, L.smem, st>>>(a, L);
+  k_eval_w<NBW, F2, D, WP, HV><<<plan.w_grid, L.S * L.T * 32, L.smem, st>>>(a, L);
   count_launch();
   return cudaGetLastError();
 }
@@ -604,18 +638,19 @@ void eval_plan_w(const Dims& D, EvalPlan* plan, int sms) {
 
 cudaError_t MNL_W_PART_FN(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
-                          double* part, int* err, cudaStream_t st) {
+                          bool hv, double* part, int* err, cudaStream_t st) {
   EvalArgs a{};
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = D.f; a.d = D.d; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.X = X; a.Y = Y; a.Z = Z; a.choice = choice; a.coef = coef;
-  a.Pr = writeP ? pk->Pr : nullptr;
-  a.ldP = writeP ? pk->ldP : 0;
-  a.want_grad = want_grad; a.writeP = writeP;
+  a.Pr = (writeP || hv) ? pk->Pr : nullptr;
+  a.ldP = (writeP || hv) ? pk->ldP : 0;
+  a.want_grad = want_grad; a.writeP = writeP && !hv;
   a.part = part; a.n_part = plan.n_part; a.err = err;
-#define MNL_W_LAUNCH(F2_, D_)                                                    \
-  if (D.f == 2 * F2_ && D.d == D_)                                                \
-    return writeP ? launch_w<2, F2_, D_, true>(plan, a, st) : launch_w<2, F2_, D_, false>(plan, a, st);
+#define MNL_W_LAUNCH(F2_, D_)                                                      \
+  if (D.f == 2 * F2_ && D.d == D_)                                                  \
+    return hv ? launch_w<2, F2_, D_, false, true>(plan, a, st)                       \
+              : (writeP ? launch_w<2, F2_, D_, true, false>(plan, a, st) : launch_w<2, F2_, D_, false, false>(plan, a, st));
   MNL_W_SHAPES(MNL_W_LAUNCH)
 #undef MNL_W_LAUNCH
   return cudaErrorInvalidValue;
@@ -624,9 +659,9 @@ cudaError_t MNL_W_PART_FN(const Dims& D, const EvalPlan& plan, const double* X, 
 #if MNL_W_PART == 0
 cudaError_t launch_eval_w(const Dims& D, const EvalPlan& plan, const double* X, const double* Y, const double* Z,
                           const int32_t* choice, const double* coef, const Packed* pk, bool want_grad, bool writeP,
-                          double* part, int* err, cudaStream_t st) {
+                          bool hv, double* part, int* err, cudaStream_t st) {
   auto fn = D.f < 6 ? launch_eval_w_part0 : (D.f < 12 ? launch_eval_w_part1 : launch_eval_w_part2);
-  return fn(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, part, err, st);
+  return fn(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, hv, part, err, st);
 }
 #endif
 

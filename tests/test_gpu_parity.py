@@ -149,7 +149,7 @@ TEAM_SHAPES = [(1000, 4, 3, 2, 1), (334, 50, 5, 10, 5), (2050, 6, 17, 2, 3), (65
 @pytest.mark.parametrize("shape", TEAM_SHAPES, ids=lambda s: "x".join(map(str, s)))
 def test_eval_team_mapping(shape):
     """Pass 1 through the team mapping (forced for the shapes below its size thresholds) against the
-    oracle: loglik, gradient, and the probability rows / ybar through the full Hessian; then the
+    oracle: loglik, gradient, the probability rows / ybar through the full Hessian, and H v; then the
     same numbers as the YZS / direct paths within the parity tolerances; the gradient pass and the
     Hessian pass give bit-identical loglik and gradient."""
     N, K, p, f, d = shape
@@ -163,10 +163,13 @@ def test_eval_team_mapping(shape):
         l, g, H = gpu_eval(dp, th)
         l2, g2, _ = gpu_eval(dp, th, hess=False)
         l3, _, _ = M.mnl_eval(dp, dev(th), grad=False, hess=False)
+        v = np.random.default_rng(5).standard_normal(D.n_p)
+        hv = M.mnl_hessvec(dp, dev(th), dev(v)).cpu().numpy()  # the Hessian-vector mode of the same kernel
     finally:
         os.environ.pop("MNL_FORCE_YZW", None)
     check_lg(l, g, l_o, g_o)
     assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+    assert np.linalg.norm(hv - H_o @ v) <= 1e-10 * np.linalg.norm(H_o @ v)
     assert l2 == l and np.array_equal(g2, g) and l3.item() == l
     os.environ["MNL_NO_YZW"] = "1"
     try:
