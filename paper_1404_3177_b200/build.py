@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libmnl.so")
 HOST_OUT = os.path.join(HERE, "lib", "libnrhost.so")   # the same NR driver over host callbacks (CPU tests)
-SOURCES = ["mnl_api.cu", "k_eval.cu", "k_eval_w.cu", "k_eval_w1.cu", "k_eval_w2.cu", "k_hess.cu", "k_chol.cu"]
+SOURCES = ["mnl_api.cu", "k_eval.cu", "k_eval_w.cu", "k_eval_w1.cu", "k_eval_w2.cu", "k_eval_x.cu", "k_hess.cu", "k_chol.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v",

@@ -79,14 +79,23 @@ struct EvalPlan {
   // the group mapping (k_eval_w.cu), used by launch_eval and launch_hessvec when w.T > 0
   EvalWLayout w;
   int w_grid;
+  // the two-group X-only kernel (k_eval_x.cu), used when x_grid > 0
+  int x_grid, x_cm, x_scr;
+  size_t x_smem;
 };
 bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
 void eval_plan_w(const Dims& D, EvalPlan* plan, int device_sms);
+void eval_plan_x(const Dims& D, EvalPlan* plan, int device_sms);
+// The two-group X-only kernel (k_eval_x.cu): evaluation (hv = false) or Hessian-vector product.
+cudaError_t launch_eval_x(const Dims& D, const EvalPlan& plan, const double* X, const int32_t* choice,
+                          const double* coef, const Packed* pk, bool want_grad, bool writeP, bool hv, double* part,
+                          int* err, cudaStream_t st);
 // CTA partial rows written by launch_eval / launch_hessvec with this plan
-inline int eval_nblk(const EvalPlan& ep, bool) { return ep.w.T ? ep.w_grid : ep.grid; }
+inline int eval_nblk(const EvalPlan& ep, bool) { return ep.w.T ? ep.w_grid : (ep.x_grid ? ep.x_grid : ep.grid); }
 // doubles of the `part` scratch a launch with this plan needs (CTA partials + stream-mode residual rows)
 inline size_t eval_part_doubles(const EvalPlan& ep) {
-  return (size_t)(ep.grid > ep.w_grid ? ep.grid : ep.w_grid) * ep.n_part + ep.rg;
+  const int g = ep.grid > ep.w_grid ? ep.grid : ep.w_grid;
+  return (size_t)(g > ep.x_grid ? g : ep.x_grid) * ep.n_part + ep.rg;
 }
 // Pass 1 (a1-a4): utilities, softmax, loglik partials, gradient partials (if want_grad),
 // and the probability rows Pr (if writeP). part: [grid][n_part].

@@ -1502,6 +1502,7 @@ bool eval_plan(const Dims& D, EvalPlan* plan, int sms) {
   plan->grid = (int)grid;
   plan->n_part = 2 + D.n_p;
   eval_plan_w(D, plan, sms);
+  eval_plan_x(D, plan, sms);
   return true;
 }
 
@@ -1571,6 +1572,7 @@ cudaError_t launch_eval(const Dims& D, const EvalPlan& plan, const double* X, co
                         const Packed* pk, bool want_grad, bool writeP, double* part, int* err,
                         cudaStream_t st) {
   if (plan.w.T) return launch_eval_w(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, false, part, err, st);
+  if (plan.x_grid) return launch_eval_x(D, plan, X, choice, coef, pk, want_grad, writeP, false, part, err, st);
   return launch_eval_impl(D, plan, X, Y, Z, choice, coef, pk, want_grad, writeP, false, part, err, st);
 }
 
@@ -1578,6 +1580,7 @@ cudaError_t launch_hessvec(const Dims& D, const EvalPlan& plan, const double* X,
                            const int32_t* choice, const double* v, const Packed* pk, double* part, int* err,
                            cudaStream_t st) {
   if (plan.w.T) return launch_eval_w(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
+  if (plan.x_grid) return launch_eval_x(D, plan, X, choice, v, pk, true, false, true, part, err, st);
   return launch_eval_impl(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
 }
 

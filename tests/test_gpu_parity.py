@@ -179,6 +179,43 @@ def test_eval_team_mapping(shape):
     check_lg(l, g, l_y, g_y)
 
 
+# X-only models through the two-group kernel (k_eval_x.cu): K in 32 / 64 / 128 columns, every
+# accumulator depth (q = 1 .. 64), ragged 32-row tiles, a single individual, several CTAs.
+XG_SHAPES = [(1000, 4, 3, 0, 0), (333, 100, 6, 0, 0), (65, 33, 50, 0, 0), (8200, 20, 7, 0, 0), (31, 128, 2, 0, 0),
+             (1, 2, 5, 0, 0), (40, 64, 63, 0, 0), (97, 3, 0, 0, 0), (20000, 10, 20, 0, 0), (5000, 65, 31, 0, 0)]
+
+
+@pytest.mark.parametrize("shape", XG_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_eval_x_two_groups(shape):
+    """X-only pass 1 through the two-group kernel (forced below its size threshold) against the
+    oracle: loglik, gradient, the probability rows through the full Hessian, H v; bit-identical
+    loglik and gradient from the gradient pass and the Hessian pass; and against the 64-row kernel."""
+    N, K, p, f, d = shape
+    prob = datagen.custom(N, K, p, f, d, seed=13, coef_sd=0.3, require_all_classes=False)
+    D = oracle_data(prob)
+    dp = device_problem(prob)
+    th = datagen.perturbed_theta(prob, 0.2)
+    l_o, g_o, H_o = O.mnl_eval(D, th)
+    os.environ["MNL_FORCE_XG"] = "1"
+    try:
+        l, g, H = gpu_eval(dp, th)
+        l2, g2, _ = gpu_eval(dp, th, hess=False)
+        v = np.random.default_rng(5).standard_normal(D.n_p)
+        hv = M.mnl_hessvec(dp, dev(th), dev(v)).cpu().numpy()
+    finally:
+        os.environ.pop("MNL_FORCE_XG", None)
+    check_lg(l, g, l_o, g_o)
+    assert np.linalg.norm(H - H_o) <= 1e-9 * np.linalg.norm(H_o)
+    assert np.linalg.norm(hv - H_o @ v) <= 1e-10 * np.linalg.norm(H_o @ v)
+    assert l2 == l and np.array_equal(g2, g)
+    os.environ["MNL_NO_XG"] = "1"
+    try:
+        l_y, g_y, _ = gpu_eval(dp, th, hess=False)
+    finally:
+        os.environ.pop("MNL_NO_XG", None)
+    check_lg(l, g, l_y, g_y)
+
+
 def test_eval_team_mapping_bad_choice_and_nonfinite():
     """The team mapping reports a choice outside 0..K-1 (MNL_ERR_ARG) and a NaN anywhere in Y or Z
     (MNL_ERR_NONFINITE), also in a row of the ragged last group."""
