@@ -80,7 +80,7 @@ struct EvalPlan {
   EvalWLayout w;
   int w_grid;
   // the two-group X-only kernel (k_eval_x.cu), used when x_grid > 0
-  int x_grid, x_cm, x_scr;
+  int x_grid, x_cm, x_scr, x_hv;  // x_hv: also for launch_hessvec
   size_t x_smem;
 };
 bool eval_plan(const Dims& D, EvalPlan* plan, int device_sms);
@@ -91,7 +91,9 @@ cudaError_t launch_eval_x(const Dims& D, const EvalPlan& plan, const double* X, 
                           const double* coef, const Packed* pk, bool want_grad, bool writeP, bool hv, double* part,
                           int* err, cudaStream_t st);
 // CTA partial rows written by launch_eval / launch_hessvec with this plan
-inline int eval_nblk(const EvalPlan& ep, bool) { return ep.w.T ? ep.w_grid : (ep.x_grid ? ep.x_grid : ep.grid); }
+inline int eval_nblk(const EvalPlan& ep, bool hv) {
+  return ep.w.T ? ep.w_grid : ((ep.x_grid && (!hv || ep.x_hv)) ? ep.x_grid : ep.grid);
+}
 // doubles of the `part` scratch a launch with this plan needs (CTA partials + stream-mode residual rows)
 inline size_t eval_part_doubles(const EvalPlan& ep) {
   const int g = ep.grid > ep.w_grid ? ep.grid : ep.w_grid;

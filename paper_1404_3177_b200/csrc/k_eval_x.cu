@@ -280,6 +280,7 @@ void eval_plan_x(const Dims& D, EvalPlan* plan, int sms) {
   plan->x_grid = 0;
   plan->x_smem = 0;
   plan->x_cm = 0;
+  plan->x_hv = 0;
   if (D.d + D.f != 0 || D.K > 128 || D.K < 2 || getenv("MNL_NO_XG")) return;
   int kpl = 1;
   while (32 * kpl < D.K) kpl *= 2;
@@ -304,6 +305,7 @@ void eval_plan_x(const Dims& D, EvalPlan* plan, int sms) {
   plan->x_smem = total;
   plan->x_cm = cm;
   plan->x_scr = (int)grp_doubles;
+  plan->x_hv = getenv("MNL_FORCE_XG") != nullptr;
 }
 
 cudaError_t launch_eval_x(const Dims& D, const EvalPlan& plan, const double* X, const int32_t* choice,
