@@ -17,6 +17,9 @@
 // individual, so the row softmax is lane-local plus two shuffles) and a quarter of the
 // alternative blocks in X~^T R (accumulators in registers for the whole kernel). The two groups'
 // partials are added in a fixed order at the end, then over the CTAs by k_eval_finalize.
+// The kernel is instantiated on the number of 8-alternative blocks NBN = ceil(K / 8) itself (c4:
+// 13, not the 16 of K padded to 128 columns: run-time guards around the padding blocks cost more
+// than they save) and on the depth CM of a warp's X~^T R accumulators.
 #include <algorithm>
 #include <cstdlib>
 
@@ -38,14 +41,22 @@ __device__ __forceinline__ void group_sync(int grp) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * XW) : "memory");
 }
 
-template <int KPL, int CM, bool HV>
+// row stride of the beta table and the residual rows: >= 8 nbn, = 4 or 12 (mod 16) doubles
+// (conflict-free 4 x 8 fragment gathers)
+__host__ __device__ constexpr int x_kps(int nbn) {
+  int s = 8 * nbn;
+  while (s % 16 != 4 && s % 16 != 12) ++s;
+  return s;
+}
+
+template <int NBN, int CM>
 __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   extern __shared__ __align__(16) double sm[];
-  constexpr int KP = 32 * KPL, KPS = KP + 4;   // alternatives padded; row stride = 4 (mod 16)
-  constexpr int NBN = KP / 8;                   // 8-wide alternative blocks
-  constexpr int WN = NBN < XW ? NBN : XW;       // phase-C warp grid of a group: WN x WM warps
+  constexpr bool HV = false;                    // (the Hessian-vector product stays with k_eval.cu)
+  constexpr int KPS = x_kps(NBN);
+  constexpr int WN = NBN >= 4 ? 4 : (NBN >= 2 ? 2 : 1);  // phase-C warp grid of a group: WN x WM warps
   constexpr int WM = XW / WN;
-  constexpr int CN = NBN / WN;                  // alternative blocks per warp in phase C
+  constexpr int CN = (NBN + WN - 1) / WN;       // alternative blocks per warp in phase C (the last may not exist)
   const int K = A.K, q = A.q, p = A.p, QP = A.QP, XS = A.XS;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int grp = w / XW, wg = w % XW, gtid = tid - grp * (32 * XW);
@@ -206,14 +217,16 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
       for (int ks = 0; ks < XT / 4; ++ks) {
         double bf[CN];
 #pragma unroll
-        for (int j = 0; j < CN; ++j) bf[j] = Rs[(4 * ks + r4) * KPS + (cwn + WN * j) * 8 + c8];
+        for (int j = 0; j < CN; ++j)
+          bf[j] = (j < CN - 1 || cwn + WN * j < NBN) ? Rs[(4 * ks + r4) * KPS + (cwn + WN * j) * 8 + c8] : 0.0;
 #pragma unroll
         for (int mi = 0; mi < CM; ++mi) {
           const int mb = cwm + WM * mi;
           if (mb < MB) {
             const double af = X_t[(4 * ks + r4) * XS + mb * 8 + c8];
 #pragma unroll
-            for (int j = 0; j < CN; ++j) dmma884(G[mi][j][0], G[mi][j][1], af, bf[j]);
+            for (int j = 0; j < CN; ++j)
+              if (j < CN - 1 || cwn + WN * j < NBN) dmma884(G[mi][j][0], G[mi][j][1], af, bf[j]);
           }
         }
       }
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int k = (cwn + WN * j) * 8 + 2 * r4 + h;
-            if (a < q && k >= 1 && k < K) Vg[(k - 1) * q + a] = G[mi][j][h];
+            if (a < q && k >= 1 && k < K && cwn + WN * j < NBN) Vg[(k - 1) * q + a] = G[mi][j][h];
           }
       }
     }
@@ -259,14 +272,14 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   for (int idx = tid; idx < A.n_p; idx += blockDim.x) out[2 + idx] = V[idx] + V[A.n_p + idx];
 }
 
-template <int KPL, int CM, bool HV>
+template <int NBN, int CM>
 cudaError_t launch_x(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static uint64_t attr_mask = 0;
   cudaError_t e = set_once_per_device(attr_mask, [] {
-    return cudaFuncSetAttribute(k_eval_x<KPL, CM, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return cudaFuncSetAttribute(k_eval_x<NBN, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (e != cudaSuccess) return e;
-  k_eval_x<KPL, CM, HV><<<plan.x_grid, XG * XW * 32, plan.x_smem, st>>>(a);
+  k_eval_x<NBN, CM><<<plan.x_grid, XG * XW * 32, plan.x_smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
@@ -282,12 +295,10 @@ void eval_plan_x(const Dims& D, EvalPlan* plan, int sms) {
   plan->x_cm = 0;
   plan->x_hv = 0;
   if (D.d + D.f != 0 || D.K > 128 || D.K < 2 || getenv("MNL_NO_XG")) return;
-  int kpl = 1;
-  while (32 * kpl < D.K) kpl *= 2;
-  const int KPS = 32 * kpl + 4, QP = x_qp(D), XS = pad4mod16(QP);
-  const int nbn = 4 * kpl, wn = nbn < XW ? nbn : XW, wm = XW / wn, cn = nbn / wn;
+  const int nbn = (D.K + 7) / 8, KPS = x_kps(nbn), QP = x_qp(D), XS = pad4mod16(QP);
+  const int wn = nbn >= 4 ? 4 : (nbn >= 2 ? 2 : 1), wm = XW / wn, cn = (nbn + wn - 1) / wn;
   const int mb = (QP + 7) / 8;
-  int cm = 1;
+  int cm = 4;  // instantiated depths: 4 and 8
   while (cm * wm < mb) cm *= 2;
   // register budget: the phase-C accumulators (cm x cn blocks) + the phase-B row (nbn blocks)
   if (cm > 8 || 2 * cm * cn + 2 * nbn > 100) return;
@@ -305,42 +316,29 @@ void eval_plan_x(const Dims& D, EvalPlan* plan, int sms) {
   plan->x_smem = total;
   plan->x_cm = cm;
   plan->x_scr = (int)grp_doubles;
-  plan->x_hv = getenv("MNL_FORCE_XG") != nullptr;
 }
 
 cudaError_t launch_eval_x(const Dims& D, const EvalPlan& plan, const double* X, const int32_t* choice,
                           const double* coef, const Packed* pk, bool want_grad, bool writeP, bool hv, double* part,
                           int* err, cudaStream_t st) {
+  if (hv) return cudaErrorInvalidValue;
   EvalArgs a{};
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = 0; a.d = 0; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = x_qp(D); a.XS = pad4mod16(a.QP); a.SCR = plan.x_scr;
   a.X = X; a.choice = choice; a.coef = coef;
-  a.Pr = (writeP || hv) ? pk->Pr : nullptr;
-  a.ldP = (writeP || hv) ? pk->ldP : 0;
-  a.want_grad = want_grad; a.writeP = writeP && !hv;
+  a.Pr = writeP ? pk->Pr : nullptr;
+  a.ldP = writeP ? pk->ldP : 0;
+  a.want_grad = want_grad; a.writeP = writeP;
   a.part = part; a.n_part = plan.n_part; a.err = err;
-  int kpl = 1;
-  while (32 * kpl < D.K) kpl *= 2;
-#define MNL_X_CM(KPL_, HV_)                                                \
-  switch (plan.x_cm) {                                                     \
-    case 1: return launch_x<KPL_, 1, HV_>(plan, a, st);                    \
-    case 2: return launch_x<KPL_, 2, HV_>(plan, a, st);                    \
-    case 4: return launch_x<KPL_, 4, HV_>(plan, a, st);                    \
-    case 8: return launch_x<KPL_, 8, HV_>(plan, a, st);                    \
-  }                                                                        \
-  break;
-#define MNL_X_KPL(KPL_)                                                    \
-  case KPL_:                                                               \
-    if (hv) { MNL_X_CM(KPL_, true) }                                       \
-    MNL_X_CM(KPL_, false)
-  switch (kpl) {
-    MNL_X_KPL(1)
-    MNL_X_KPL(2)
-    MNL_X_KPL(4)
+#define MNL_X_NBN(NBN_)                                                                                       \
+  case NBN_:                                                                                                  \
+    return plan.x_cm == 4 ? launch_x<NBN_, 4>(plan, a, st) : launch_x<NBN_, 8>(plan, a, st);
+  switch ((D.K + 7) / 8) {
+    MNL_X_NBN(1) MNL_X_NBN(2) MNL_X_NBN(3) MNL_X_NBN(4) MNL_X_NBN(5) MNL_X_NBN(6) MNL_X_NBN(7) MNL_X_NBN(8)
+    MNL_X_NBN(9) MNL_X_NBN(10) MNL_X_NBN(11) MNL_X_NBN(12) MNL_X_NBN(13) MNL_X_NBN(14) MNL_X_NBN(15) MNL_X_NBN(16)
   }
-#undef MNL_X_CM
-#undef MNL_X_KPL
+#undef MNL_X_NBN
   return cudaErrorInvalidValue;
 }
 
