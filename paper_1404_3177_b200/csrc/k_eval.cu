@@ -1580,8 +1580,6 @@ cudaError_t launch_hessvec(const Dims& D, const EvalPlan& plan, const double* X,
                            const int32_t* choice, const double* v, const Packed* pk, double* part, int* err,
                            cudaStream_t st) {
   if (plan.w.T) return launch_eval_w(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
-  // (the two-group kernel's H v variant is no faster than this file's — c4 1.19 vs 1.16 ms per
-  // product; it runs only when forced, for the tests)
   if (plan.x_grid && plan.x_hv) return launch_eval_x(D, plan, X, choice, v, pk, true, false, true, part, err, st);
   return launch_eval_impl(D, plan, X, Y, Z, choice, v, pk, true, false, true, part, err, st);
 }

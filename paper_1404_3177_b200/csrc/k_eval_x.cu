@@ -49,10 +49,9 @@ __host__ __device__ constexpr int x_kps(int nbn) {
   return s;
 }
 
-template <int NBN, int CM>
+template <int NBN, int CM, bool HV>
 __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   extern __shared__ __align__(16) double sm[];
-  constexpr bool HV = false;                    // (the Hessian-vector product stays with k_eval.cu)
   constexpr int KPS = x_kps(NBN);
   constexpr int WN = NBN >= 4 ? 4 : (NBN >= 2 ? 2 : 1);  // phase-C warp grid of a group: WN x WM warps
   constexpr int WM = XW / WN;
@@ -272,14 +271,14 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   for (int idx = tid; idx < A.n_p; idx += blockDim.x) out[2 + idx] = V[idx] + V[A.n_p + idx];
 }
 
-template <int NBN, int CM>
+template <int NBN, int CM, bool HV>
 cudaError_t launch_x(const EvalPlan& plan, const EvalArgs& a, cudaStream_t st) {
   static uint64_t attr_mask = 0;
   cudaError_t e = set_once_per_device(attr_mask, [] {
-    return cudaFuncSetAttribute(k_eval_x<NBN, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return cudaFuncSetAttribute(k_eval_x<NBN, CM, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (e != cudaSuccess) return e;
-  k_eval_x<NBN, CM><<<plan.x_grid, XG * XW * 32, plan.x_smem, st>>>(a);
+  k_eval_x<NBN, CM, HV><<<plan.x_grid, XG * XW * 32, plan.x_smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
@@ -316,24 +315,25 @@ void eval_plan_x(const Dims& D, EvalPlan* plan, int sms) {
   plan->x_smem = total;
   plan->x_cm = cm;
   plan->x_scr = (int)grp_doubles;
+  plan->x_hv = 1;
 }
 
 cudaError_t launch_eval_x(const Dims& D, const EvalPlan& plan, const double* X, const int32_t* choice,
                           const double* coef, const Packed* pk, bool want_grad, bool writeP, bool hv, double* part,
                           int* err, cudaStream_t st) {
-  if (hv) return cudaErrorInvalidValue;
   EvalArgs a{};
   a.N = D.N; a.K = D.K; a.p = D.p; a.f = 0; a.d = 0; a.q = D.q; a.n_p = D.n_p;
   a.off_alpha = D.off_alpha; a.off_gamma = D.off_gamma;
   a.QP = x_qp(D); a.XS = pad4mod16(a.QP); a.SCR = plan.x_scr;
   a.X = X; a.choice = choice; a.coef = coef;
-  a.Pr = writeP ? pk->Pr : nullptr;
-  a.ldP = writeP ? pk->ldP : 0;
-  a.want_grad = want_grad; a.writeP = writeP;
+  a.Pr = (writeP || hv) ? pk->Pr : nullptr;
+  a.ldP = (writeP || hv) ? pk->ldP : 0;
+  a.want_grad = want_grad; a.writeP = writeP && !hv;
   a.part = part; a.n_part = plan.n_part; a.err = err;
 #define MNL_X_NBN(NBN_)                                                                                       \
   case NBN_:                                                                                                  \
-    return plan.x_cm == 4 ? launch_x<NBN_, 4>(plan, a, st) : launch_x<NBN_, 8>(plan, a, st);
+    if (hv) return plan.x_cm == 4 ? launch_x<NBN_, 4, true>(plan, a, st) : launch_x<NBN_, 8, true>(plan, a, st); \
+    return plan.x_cm == 4 ? launch_x<NBN_, 4, false>(plan, a, st) : launch_x<NBN_, 8, false>(plan, a, st);
   switch ((D.K + 7) / 8) {
     MNL_X_NBN(1) MNL_X_NBN(2) MNL_X_NBN(3) MNL_X_NBN(4) MNL_X_NBN(5) MNL_X_NBN(6) MNL_X_NBN(7) MNL_X_NBN(8)
     MNL_X_NBN(9) MNL_X_NBN(10) MNL_X_NBN(11) MNL_X_NBN(12) MNL_X_NBN(13) MNL_X_NBN(14) MNL_X_NBN(15) MNL_X_NBN(16)
