@@ -20,4 +20,4 @@ python tools/prof_eval.py c4 3 > gpurun_out/prof_eval4_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:k_eval_x -s 2 -c 1 \
     -o gpurun_out/eval_c4_xonly_r2 -f python tools/prof_eval.py c4 3 > gpurun_out/ncu_eval4.log 2>&1; echo "c4 eval capture rc=$?"
 timeout 900 python tools/config_table.py > gpurun_out/config_table_r2.json 2> gpurun_out/config_table.err; echo "config table rc=$?"
-bash tools/gpu_w3.sh > gpurun_out/team_vs_yzs.log 2>&1; cat gpurun_out/team_vs_yzs.log
+bash tools/gpu_pass1_team_vs_yzs.sh > gpurun_out/team_vs_yzs.log 2>&1; cat gpurun_out/team_vs_yzs.log
