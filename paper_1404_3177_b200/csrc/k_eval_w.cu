@@ -10,7 +10,7 @@
 // A TEAM of S warps works on groups of 8 consecutive individuals, the 8 rows of one DMMA m-block;
 // warp t of the team owns the alternative blocks t NBW .. t NBW + NBW - 1 (8 alternatives each).
 // There is no CTA barrier in the main loop:
-//   * the team's first warp bulk-copies the group's 8 Y rows, 8 Z rows and its 8 x p block of X
+//   * the team's last warp bulk-copies the group's 8 Y rows, 8 Z rows and its 8 x p block of X
 //     into the team's ring (two halves of 8 slots; a "full" mbarrier with the byte count and an
 //     "empty" mbarrier the S warps arrive on per half): while group n is computed, group n + 1 is
 //     in flight (whole rows, 16-byte multiples, DRAM bytes = algorithmic bytes);
@@ -98,6 +98,9 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int r4 = lane & 3, c8 = lane >> 2;
   const int S = L.S, team = w / S, wt = w - team * S, nteams = L.T;
+  // the team's last warp stages the ring and sums the loglik: it is the one whose alternative
+  // blocks may lie (partly) beyond K, i.e. the one with the least other work
+  const int lead = S - 1;
   const int KS = L.KS, RS = L.RS, YS = L.YS, ZS = L.ZS, XH = L.XH;
   double* Bs = sm;                                  // [PP][KS]  Bs[a][k] = beta_k[1 + a], x column a (column 0: base)
   double* gamma_s = sm + L.off_gam;                 // [f]
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
     Bs[idx] = (a < p && k >= 1 && k < K) ? A.coef[(k - 1) * q + a + 1] : 0.0;
   }
   for (int idx = tid; idx < f; idx += blockDim.x) gamma_s[idx] = A.coef[A.off_gamma + idx];
-  if (wt == 0 && lane == 0) {
+  if (wt == lead && lane == 0) {
     mbar_init(bars, 1);
     mbar_init(bars + 1, 1);
     mbar_init(bars + 2, S);
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
   const unsigned by = (unsigned)(K * f) * 8u, bz = (unsigned)Kd * 8u, bx = (unsigned)(GR * p) * 8u;
   const int64_t ngroups = (A.N + GR - 1) / GR;
   const int64_t tg = (int64_t)blockIdx.x * nteams + team, tstride = (int64_t)gridDim.x * nteams;
-  // the team's first warp stages group g into ring half `half`. A ragged last group is read as the
+  // the team's lead warp stages group g into ring half `half`. A ragged last group is read as the
   // last 8 rows of the data; its rows below g * 8 are masked where they are used.
   auto issue = [&](int64_t g, int half) {
     int64_t i0 = g * GR;
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
       if (bx) bulk_g2s(xb_s + 8u * (unsigned)(half * XH), A.X + i0 * p, bx, bar);
     }
   };
-  if (wt == 0) {
+  if (wt == lead) {
     if (tg < ngroups) issue(tg, 0);
     if (tg + tstride < ngroups) issue(tg + tstride, 1);
   }
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
     int y = y_next;
     y_next = choice_of(g + tstride);
     if (y < 0 || y >= K) {
-      if (valid && r4 == 0 && wt == 0) atomicOr(A.err, 1);
+      if (valid && r4 == 0 && wt == lead) atomicOr(A.err, 1);
       y = 0;
     }
     // Hessian-vector product: P_i of the last evaluation (its loads land behind the wait)
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
       stot += __shfl_xor_sync(0xffffffffu, stot, 1);
       stot += __shfl_xor_sync(0xffffffffu, stot, 2);
     }
-    if (valid && r4 == 0 && wt == 0) {
+    if (valid && r4 == 0 && wt == lead) {
       const double uy = Uy[half * GR + c8];
       // l_i = u_y - n ln2 - log s (ln2 split as in exp_scaled)
       neu_add(l_s, l_c, fma(nmax, -1.90821492927058770002e-10, fma(nmax, -6.93147180369123816490e-01, uy)) - log(stot));
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
     __syncwarp();  // every lane is done with this half (ring, x block) and with the residual rows
     if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s + 8u * (2 + half)) : "memory");
-    if (wt == 0 && g + 2 * tstride < ngroups) {
+    if (wt == lead && g + 2 * tstride < ngroups) {
       mbar_wait(bar_s + 8u * (2 + half), upar);  // all S warps have left the half
       issue(g + 2 * tstride, half);
     }
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(NBW == 1 ? 448 : 256, 1) k_eval_w(const EvalAr
   double* V = sm + L.off_team;                          // [T][n_p]   beta / alpha entries per team
   double* Vg = V + (size_t)nteams * A.n_p;             // [nw][W_F]  gamma partial per warp
   double* LL = Vg + nw * W_F;                          // [T 8][2]   loglik partials
-  if (wt == 0 && r4 == 0) {
+  if (wt == lead && r4 == 0) {
     LL[2 * (team * GR + c8)] = l_s;
     LL[2 * (team * GR + c8) + 1] = l_c;
   }
