@@ -55,7 +55,15 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   constexpr int KPS = x_kps(NBN);
   constexpr int WN = NBN >= 4 ? 4 : (NBN >= 2 ? 2 : 1);  // phase-C warp grid of a group: WN x WM warps
   constexpr int WM = XW / WN;
-  constexpr int CN = (NBN + WN - 1) / WN;       // alternative blocks per warp in phase C (the last may not exist)
+  // alternative blocks per warp in phase C. With four warps across the blocks (NBN >= 4) a warp takes
+  // blocks wg, wg + 4, ... of the whole rounds, and the REM = NBN % 4 blocks left over are cut into
+  // their (m-block, block) cells, dealt evenly to the four warps (c4: 13 blocks = 3 rounds + 1 block
+  // of 7 cells, 2 + 2 + 2 + 1 — instead of one warp with a fourth whole block and three waiting at
+  // the group barrier). NBN < 4: blocks cwn, cwn + WN (the last may not exist).
+  constexpr bool SPLIT = WN == 4 && (NBN % 4) != 0;
+  constexpr int REM = SPLIT ? NBN % 4 : 0;
+  constexpr int CN = SPLIT ? NBN / 4 : (NBN + WN - 1) / WN;
+  constexpr int RC = SPLIT ? (REM * 8 + 3) / 4 : 1;  // cells per warp at most (MB <= 8)
   const int K = A.K, q = A.q, p = A.p, QP = A.QP, XS = A.XS;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int grp = w / XW, wg = w % XW, gtid = tid - grp * (32 * XW);
@@ -78,6 +86,16 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   for (int i = 0; i < CM; ++i)
 #pragma unroll
     for (int j = 0; j < CN; ++j) G[i][j][0] = G[i][j][1] = 0.0;
+  double Gr[RC][2];    // ... and this warp's cells of the left-over blocks
+  int cellA[RC], cellB[RC];  // their x~ column / alternative offsets (-1: no such cell)
+#pragma unroll
+  for (int t = 0; t < RC; ++t) {
+    Gr[t][0] = Gr[t][1] = 0.0;
+    const int cells = REM * MB, per = (cells + 3) / 4, e = wg * per + t;
+    const bool have = SPLIT && t < per && e < cells;
+    cellA[t] = have ? (e % MB) * 8 + c8 : -1;                    // m-block e % MB
+    cellB[t] = have ? (NBN - REM + e / MB) * 8 + c8 : -1;       // block NBN - REM + e / MB
+  }
   double l_s = 0.0, l_c = 0.0;  // Neumaier loglik of this lane's rows (lanes with r4 == 0)
 
   const int64_t ntiles = (A.N + XT - 1) / XT;
@@ -228,6 +246,12 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
               if (j < CN - 1 || cwn + WN * j < NBN) dmma884(G[mi][j][0], G[mi][j][1], af, bf[j]);
           }
         }
+        if constexpr (SPLIT) {
+#pragma unroll
+          for (int t = 0; t < RC; ++t)
+            if (cellA[t] >= 0)
+              dmma884(Gr[t][0], Gr[t][1], X_t[(4 * ks + r4) * XS + cellA[t]], Rs[(4 * ks + r4) * KPS + cellB[t]]);
+        }
       }
     }
   }
@@ -256,6 +280,18 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
           }
       }
     }
+  }
+  if (A.want_grad && SPLIT) {
+    double* Vg = V + (size_t)grp * A.n_p;
+#pragma unroll
+    for (int t = 0; t < RC; ++t)
+      if (cellA[t] >= 0) {
+        const int a = cellA[t];                      // = 8 m + c8
+        const int k0 = cellB[t] - c8 + 2 * r4;      // = 8 block + 2 r4
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (a < q && k0 + h >= 1 && k0 + h < K) Vg[(k0 + h - 1) * q + a] = Gr[t][h];
+      }
   }
   __syncthreads();
   if (tid == 0) {
