@@ -134,11 +134,11 @@ __global__ void __launch_bounds__(XG * XW * 32, 1) k_eval_x(const EvalArgs A) {
   for (int64_t tile = t0; tile < ntiles; tile += tstride, buf ^= 1) {
     const int64_t i0 = tile * XT;
     const int nt = (int)(A.N - i0 < XT ? A.N - i0 : XT);
-    group_sync(grp);  // the group is done with the previous tile (buffers, Rs)
-    if (tile + tstride < ntiles) prefetch(tile + tstride, buf ^ 1);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    // this tile's copies (issued one tile ago) have landed, and — the same barrier — the group is
+    // done with the previous tile: its buffer can take the next tile, Rs the next residuals
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     group_sync(grp);
+    if (tile + tstride < ntiles) prefetch(tile + tstride, buf ^ 1);
     const double* X_t = Xs + buf * XT * XS;
     const int* ch_t = chs + buf * XT;
 
