@@ -109,6 +109,29 @@ def test_argument_errors_are_reported_without_a_device(lib):
                                  fake, ctypes.byref(it), ctypes.byref(ll), None, None) == M.MNL_ERR_ARG
 
 
+def test_check_shape_sweep_runs_every_pass1_planner(lib):
+    """mnl_check_shape plans pass 1 on the host (k_eval.cu's paths, the team mapping, the two-group
+    X-only kernel): a sweep over the shape space, with and without the planners' size thresholds,
+    returns MNL_OK or MNL_ERR_ARG for every shape inside the documented limits (no crash, no hang)."""
+    seen = set()
+    for force in (False, True):
+        for k in ("MNL_FORCE_YZW", "MNL_FORCE_XG"):
+            if force:
+                os.environ[k] = "1"
+            else:
+                os.environ.pop(k, None)
+        try:
+            for N in (1, 7, 8, 9, 4096, 8192, 200000):
+                for K in (2, 3, 8, 9, 16, 17, 33, 50, 56, 57, 64, 65, 100, 128, 129, 256):
+                    for p in (0, 1, 30, 31, 32, 33, 63, 64):
+                        for f, d in ((0, 0), (2, 1), (10, 5), (16, 8), (3, 2), (18, 0), (0, 9)):
+                            seen.add(lib.mnl_check_shape(N, K, p, f, d))
+        finally:
+            os.environ.pop("MNL_FORCE_YZW", None)
+            os.environ.pop("MNL_FORCE_XG", None)
+    assert seen <= {M.MNL_OK, M.MNL_ERR_ARG} and M.MNL_OK in seen
+
+
 def test_library_is_sm100a_only():
     so = open(M.LIB_PATH, "rb").read()
     assert b"sm_100a" in so or b"compute_100a" in so
